@@ -1,0 +1,399 @@
+"""Benchmark of the hot path on BASELINE.json's workload.
+
+Metric (BASELINE.json): "SpMV GB/s & GFLOP/s per format; CRS->ELL/COO
+transform time in CRS-SpMV units".  Workload: config 2 (random rows, n=2^20,
+row lengths U{8..24}, columns uniform in [0,n), values N(0,1), seeded
+synthetic data -- the paper's SuiteSparse set is not available).
+
+A step = one SpMV y = A x in the best format for the matrix (every format is
+measured; the per-format table, the transform times in CRS-SpMV units and
+the AT decision are reported beside the headline).  `value` = algorithmic
+bytes of one SpMV (GPU layout) x steps / device time, inputs
+resident in HBM (the matrix, 222 MB, is larger than the 126 MB L2, so no
+flush is needed between steps).  `e2e` = the same metric through the
+reference-facing C ABI call spmvtk_spmv() with pinned HOST x / y, copies
+inside the timed region.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = ("SpMV GB/s & GFLOP/s per format; CRS→ELL/COO transform time in "
+          "CRS-SpMV units")
+PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback
+
+
+def hbm_peak():
+    try:
+        with open(PEAKS_FILE) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback"
+
+
+def spmv_bytes(fmt: str, n: int, nnz: int, nz: int = 0) -> int:
+    """Compulsory bytes of one SpMV in the GPU layout (fp64 values, int32
+    indices; x read once, y written once).  SURVEY.md §8(d)."""
+    if fmt == "crs":
+        return 12 * nnz + 4 * (n + 1) + 16 * n
+    if fmt in ("coo-row", "coo-col"):
+        return 16 * nnz + 16 * n
+    if fmt in ("ell-inner", "ell-outer", "ell-row"):
+        return 12 * n * nz + 16 * n  # padding included (north_star)
+    raise ValueError(fmt)
+
+
+def transform_bytes(to: str, n: int, nnz: int, nz: int = 0) -> int:
+    if to == "coo-row":
+        return 28 * nnz + 4 * n
+    if to == "ccs":
+        return 28 * nnz + 12 * n
+    if to == "coo-col":  # Phase I + column expansion (no CCS copy)
+        return 32 * nnz + 16 * n
+    if to in ("ell", "ell-row"):
+        return 12 * nnz + 4 * (n + 1) + 12 * n * nz + 4 * n
+    raise ValueError(to)
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int = 0):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+            time.sleep(0.15)
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            time.sleep(0.06)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[2:6]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+# --------------------------------------------------------------------------
+def cpu_reference_run(host, n, nnz, nz, per_call_repeats=3):
+    """The reference's own CPU path (oracle/_ref, compiled from the reference
+    sources) on this host's cores, on the same matrix."""
+    from oracle.oracle import Ref
+    ref = Ref()
+    cores = os.cpu_count() or 1
+    rp, ci, v = host.arrays(index_base=1)
+    h = ref.matrix(n, rp, ci, v)
+    del rp, ci, v
+    res = {}
+    # transforms: one cold conversion each (autotune.cpp:122-128, :197-214)
+    t_ell, ell = ref.measure_transformation(h, 4, 0)
+    t_coo, coo = ref.measure_transformation(h, 2, 0)
+    # SpMV: warm-up + median of repeats (autotune.cpp:95-120); CRS is
+    # sequential in the reference (autotune.cpp:186), the others use lanes
+    t_crs = ref.measure_spmv(h, 0, 1, per_call_repeats)
+    res["crs"] = (t_crs, 1)
+    res["ell-inner"] = (ref.measure_spmv(ell, 3, cores, per_call_repeats), cores)
+    res["ell-outer"] = (ref.measure_spmv(ell, 4, cores, per_call_repeats), cores)
+    res["coo-row"] = (ref.measure_spmv(coo, 1, cores, per_call_repeats), cores)
+    table = {}
+    for k, (t, lanes) in res.items():
+        b = spmv_bytes(k, n, nnz, nz)
+        table[k] = {"gbs": b / t / 1e9, "gflops": 2 * nnz / t / 1e9, "ms": t * 1e3, "lanes": lanes}
+    best = max(table, key=lambda k: table[k]["gbs"])
+    out = {"table": table, "best": best, "cores": cores,
+           "transforms": {"ell": {"ms": t_ell * 1e3, "tt": t_ell / t_crs},
+                          "coo-row": {"ms": t_coo * 1e3, "tt": t_coo / t_crs}},
+           "handles": (ref, h, ell, coo)}
+    return out
+
+
+def impl_reference(args):
+    rank, world, _ = dist_env()
+    if world > 1 and rank != 0:
+        return 0
+    from paper_2407_00019_b200 import spmvtk as sp
+    # host-side generation only: this arm never touches the GPU
+    host = sp.HostCrs(args.config, args.param, 0.0, args.seed)
+    n, nnz = host.n, host.nnz
+    rp, _, _ = host.arrays(index_base=0)
+    nz = int(np.max(np.diff(rp))) if n else 0
+    del rp
+    r = cpu_reference_run(host, n, nnz, nz)
+    ref, h, ell, coo = r.pop("handles")
+    best = r["best"]
+    kern = {"crs": 0, "coo-row": 1, "ell-inner": 3, "ell-outer": 4}[best]
+    handle = {"crs": h, "coo-row": coo, "ell-inner": ell, "ell-outer": ell}[best]
+    lanes = r["table"][best]["lanes"]
+    x = np.ones(n)
+    tw = time.perf_counter()
+    for _ in range(args.warmup):
+        ref.spmv(handle, kern, x, lanes)
+    t_one = (time.perf_counter() - tw) / max(1, args.warmup)
+    # bounded sample: at most ~60 s of CPU work whatever K is
+    steps = int(max(3, min(args.steps, 60.0 / max(t_one, 1e-9))))
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        ref.spmv(handle, kern, x, lanes)
+    dt = (time.perf_counter() - t0) / steps
+    args.steps_requested, args.steps = args.steps, steps
+    b = spmv_bytes(best, n, nnz, nz)
+    value = b / dt / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"baseline config {args.config}", "n": n, "nnz": nnz,
+                   "best_format": best},
+        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": lanes, "kind": "reference",
+                         "sample": f"{args.steps} SpMVs ({best}, {lanes} lanes) of the full "
+                                   f"config-{args.config} matrix; oracle/_ref = reference "
+                                   "compiled from its sources; std::thread lanes, no OpenMP"},
+        "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "formats": r["table"], "transforms": r["transforms"],
+    }
+    print(json.dumps(line))
+    return 0
+
+
+# --------------------------------------------------------------------------
+def impl_ours(args):
+    import torch
+
+    from paper_2407_00019_b200 import spmvtk as sp
+
+    rank, world, local = dist_env()
+    if world > 1:
+        from paper_2407_00019_b200 import dist
+        return dist.bench_main(args, rank, world, local)
+
+    torch.cuda.set_device(0)
+    stream = torch.cuda.current_stream()
+    sp.set_stream(stream.cuda_stream)
+    peak, peak_kind = hbm_peak()
+
+    host = sp.HostCrs(args.config, args.param, 0.0, args.seed)
+    m = host.upload()
+    d = m.describe()
+    n, nnz = d.n, d.nnz
+    st = m.row_stats()
+    nz = st.max_row
+
+    # ---- transforms: one cold conversion each (wall clock, synchronised)
+    handles = {"crs": m}
+    transforms = {}
+    for name, fmt in (("coo-row", sp.Format.COO_ROW), ("ccs", sp.Format.CCS),
+                      ("coo-col", sp.Format.COO_COL), ("ell", sp.Format.ELL),
+                      ("ell-row", sp.Format.ELL_ROWMAJOR)):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        h = m.convert(fmt)
+        torch.cuda.synchronize()
+        cold = time.perf_counter() - t0
+        # warm repeat (pool already holds the memory) for the device-side cost
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        h2 = m.convert(fmt)
+        ev1.record()
+        torch.cuda.synchronize()
+        warm = ev0.elapsed_time(ev1) * 1e-3
+        h2.free()
+        transforms[name] = {"cold_ms": cold * 1e3, "warm_ms": warm * 1e3,
+                            "gbs_warm": transform_bytes(name, n, nnz, nz) / warm / 1e9}
+        handles[name] = h
+
+    x = torch.from_numpy(sp.gen_vector(n, args.seed + 1)).cuda()
+    y = torch.empty(n, dtype=torch.float64, device="cuda")
+    kernels = {
+        "crs": (handles["crs"], sp.Kernel.CRS),
+        "coo-row": (handles["coo-row"], sp.Kernel.COO_ROW_OUTER),
+        "coo-col": (handles["coo-col"], sp.Kernel.COO_COL_OUTER),
+        "ell-inner": (handles["ell"], sp.Kernel.ELL_INNER),
+        "ell-outer": (handles["ell"], sp.Kernel.ELL_OUTER),
+        "ell-row": (handles["ell-row"], sp.Kernel.ELL_ROWMAJOR),
+    }
+
+    def run(name, count):
+        h, k = kernels[name]
+        for _ in range(count):
+            h.spmv_device(k, x.data_ptr(), y.data_ptr())
+
+    def timed(name, count):
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        ev0.record()
+        run(name, count)
+        ev1.record()
+        torch.cuda.synchronize()
+        return ev0.elapsed_time(ev1) * 1e-3 / count
+
+    table = {}
+    per_fmt_steps = max(20, min(args.steps, 500))
+    for name in kernels:
+        run(name, max(3, args.warmup))
+        t = timed(name, per_fmt_steps)
+        b = spmv_bytes(name, n, nnz, nz)
+        table[name] = {"gbs": b / t / 1e9, "gflops": 2 * nnz / t / 1e9, "ms": t * 1e3,
+                       "bytes": b, "frac": b / t / 1e9 / peak}
+    t_crs = table["crs"]["ms"] * 1e-3
+    for name, tr in transforms.items():
+        tr["tt_cold"] = tr["cold_ms"] * 1e-3 / t_crs
+        tr["tt_warm"] = tr["warm_ms"] * 1e-3 / t_crs
+    # AT model on GPU timings, ELL-inner variant (Eq. 1-3 as implemented)
+    t_ell = table["ell-inner"]["ms"] * 1e-3
+    t_trans = transforms["ell"]["cold_ms"] * 1e-3
+    sp_, tt_, r_ = sp.compute_metrics(t_crs, t_ell, t_trans)
+
+    best = max(table, key=lambda k: table[k]["gbs"])
+    launches_per_step = 1 if best != "ell-outer" else 2
+
+    # ---- headline: K steps of the best format, device time, inputs in HBM
+    run(best, args.warmup)
+    with ClockSampler(0) as clk:
+        t_step = timed(best, args.steps)
+    bytes_step = spmv_bytes(best, n, nnz, nz)
+    value = bytes_step / t_step / 1e9
+
+    # ---- e2e: through spmvtk_spmv() with pinned host buffers
+    xh = torch.from_numpy(sp.gen_vector(n, args.seed + 1)).pin_memory()
+    yh = torch.empty(n, dtype=torch.float64).pin_memory()
+    xn, yn = xh.numpy(), yh.numpy()
+    h, k = kernels[best]
+    e2e_steps = max(10, min(args.steps, 200))
+    for _ in range(3):
+        h.spmv(xn, k, 1, out=yn)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        h.spmv(xn, k, 1, out=yn)
+    t_e2e = (time.perf_counter() - t0) / e2e_steps
+    ych = y.cpu().numpy()
+    h.spmv_device(k, x.data_ptr(), y.data_ptr())
+    torch.cuda.synchronize()
+    assert np.allclose(yn, y.cpu().numpy(), rtol=1e-12, atol=0), "e2e result mismatch"
+    del ych
+
+    # ---- CPU baseline: the reference itself on this host (bounded sample)
+    cpu = None
+    if not args.no_cpu_baseline:
+        try:
+            r = cpu_reference_run(host, n, nnz, nz)
+            r.pop("handles")
+            b = r["table"][r["best"]]
+            cpu = {"value": b["gbs"], "unit": "GB/s", "cores": b["lanes"], "kind": "reference",
+                   "sample": (f"reference measure_spmv (warm-up + median of 3) per format on the "
+                              f"same config-{args.config} matrix; best = {r['best']} at "
+                              f"{b['lanes']} lanes of {r['cores']} cores; std::thread lanes "
+                              "(the reference has no OpenMP)"),
+                   "formats": r["table"], "transforms": r["transforms"]}
+        except Exception as e:  # reported, never silently replaced
+            cpu = {"value": None, "unit": "GB/s", "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"baseline config {args.config} (random rows U{{8..24}}, "
+                               f"n={n})" if args.config == 2 else f"baseline config {args.config}",
+                   "n": n, "nnz": nnz, "max_row": nz, "d_mat": st.d_mat, "format": best,
+                   "gflops": 2 * nnz / t_step / 1e9,
+                   "l2": "inputs larger than L2 (no flush)"},
+        "roofline": {"bound": "hbm", "achieved": value, "peak": peak, "unit": "GB/s",
+                     "frac": value / peak, "traffic": None, "peak_kind": peak_kind,
+                     "kernel": best, "bytes_per_launch": bytes_step},
+        "e2e": {"value": bytes_step / t_e2e / 1e9, "unit": "GB/s", "h2d_bytes_per_step": 8 * n,
+                "d2h_bytes_per_step": 8 * n, "ms_per_step": t_e2e * 1e3,
+                "api": "spmvtk_spmv (C ABI, pinned host x/y)"},
+        "gpu_launches": args.steps * launches_per_step,
+        "clocks": clk.summary(),
+        "formats": table, "transforms": transforms,
+        "at": {"variant": "ell-inner", "sp": sp_, "tt": tt_, "r": r_},
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--param", type=int, default=None)
+    ap.add_argument("--seed", type=int, default=2407)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.param is None:
+        args.param = {1: 256, 2: 1 << 20, 3: 128, 4: 1 << 22, 5: 1 << 21}[args.config]
+    if args.impl == "reference":
+        return impl_reference(args)
+    return impl_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,125 @@
+/* spmvtk_kernels.h -- the thin lower C ABI into the sm_100a kernels.
+ *
+ * Device pointers + sizes + a CUDA stream in, a status out (0 = launched;
+ * otherwise a cudaError_t value).  No allocation happens behind these calls
+ * except where a function says so.  All launches are asynchronous on
+ * `stream` (a cudaStream_t passed as void*; NULL = legacy default stream).
+ *
+ * Device layout ("GPU layout"): values fp64, every index and
+ * pointer int32 and 0-based; ELL slot offsets are int64.  The reference keeps
+ * 1-based int64 (/root/reference/proj/include/spmvtk/formats.hpp:10-14);
+ * spmvtk_k_narrow_index / spmvtk_k_widen_index convert at the boundary.
+ */
+#ifndef SPMVTK_KERNELS_H
+#define SPMVTK_KERNELS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- row statistics (formats.cpp:184-192 + stats.cpp:9-29 + the max of
+ * convert.cpp:74-76) ------------------------------------------------------
+ * acc (device, 3 x uint64) receives {max row length, sum, sum of squares};
+ * it is zeroed by the call.  rows with ptr[i+1] < ptr[i] set bit 63 of
+ * acc[0] (validation). */
+int spmvtk_k_row_stats(const int32_t* ptr, int64_t n, unsigned long long* acc,
+                       void* stream);
+
+/* dst[i] = (int32)(src[i] - base) ; src int64 (reference layout). */
+int spmvtk_k_narrow_index(const int64_t* src, int32_t* dst, int64_t len,
+                          int64_t base, void* stream);
+/* dst[i] = (int64)src[i] + base */
+int spmvtk_k_widen_index(const int32_t* src, int64_t* dst, int64_t len,
+                         int64_t base, void* stream);
+
+/* Counts indices outside [0, n) into *bad (device uint64, zeroed first). */
+int spmvtk_k_count_out_of_range(const int32_t* idx, int64_t len, int64_t n,
+                                unsigned long long* bad, void* stream);
+/* Counts positions p with key[p] < key[p-1] (ordering check). */
+int spmvtk_k_count_descents(const int32_t* key, int64_t len,
+                            unsigned long long* bad, void* stream);
+
+/* ---- transforms ---------------------------------------------------------*/
+
+/* Phase-II style pointer expansion (convert.cpp:15-20, :62-64):
+ * out_idx[p] = r for ptr[r] <= p < ptr[r+1]. */
+int spmvtk_k_expand_ptr(const int32_t* ptr, int64_t n, int64_t nnz,
+                        int32_t* out_idx, void* stream);
+
+/* CRS -> CCS Phase I (convert.cpp:24-53).  scratch must hold 2*(n+1) int32
+ * plus spmvtk_k_scan_scratch_bytes(n+1) bytes (see below).  Row indices come
+ * out ascending inside every column, exactly as the reference's cursor
+ * scatter. */
+size_t spmvtk_k_ccs_scratch_bytes(int64_t n);
+int spmvtk_k_crs_to_ccs(int64_t n, int64_t nnz, const int32_t* irp,
+                        const int32_t* icol, const double* val,
+                        int32_t* col_ptr, int32_t* row_idx, double* out_val,
+                        void* scratch, void* stream);
+
+/* Exclusive scan of n int32 counts into out[0..n] (out[n] = total). */
+size_t spmvtk_k_scan_scratch_bytes(int64_t n);
+int spmvtk_k_exclusive_scan(const int32_t* in, int32_t* out, int64_t n,
+                            void* scratch, void* stream);
+
+/* CRS -> ELL (convert.cpp:81-115), band-major: slot(k,i) = k*ld + i, with
+ * ld >= n (ld = n reproduces the reference array exactly).  Padding slots
+ * get value +0.0 and column = own row.  out_count[i] = row length. */
+int spmvtk_k_crs_to_ell_cm(int64_t n, int32_t nz, int64_t ld, const int32_t* irp,
+                           const int32_t* icol, const double* val,
+                           double* out_val, int32_t* out_col,
+                           int32_t* out_count, void* stream);
+/* Row-major ELL (no reference counterpart): slot(i,k) = i*nz + k. */
+int spmvtk_k_crs_to_ell_rm(int64_t n, int32_t nz, const int32_t* irp,
+                           const int32_t* icol, const double* val,
+                           double* out_val, int32_t* out_col,
+                           int32_t* out_count, void* stream);
+
+/* ---- SpMV (y is overwritten; every row of y is written) ----------------*/
+
+/* spmv_crs (spmv.cpp:64-75).  max_row = longest row (from row stats); rows
+ * longer than the vector kernel's limit go to a block-per-row pass, which
+ * needs `long_rows` (device int32 scratch of n+1 entries, may be NULL when
+ * max_row is small). */
+int spmvtk_k_spmv_crs(int64_t n, const int32_t* irp, const int32_t* icol,
+                      const double* val, const double* x, double* y,
+                      double mean_row, int32_t max_row, int32_t* long_rows,
+                      void* stream);
+/* spmv_coo_row_outer (spmv.cpp:79-101,111-115): row-sorted triplets,
+ * deterministic segmented reduction, no atomics. */
+int spmvtk_k_spmv_coo_row(int64_t n, int64_t nnz, const int32_t* row,
+                          const int32_t* col, const double* val,
+                          const double* x, double* y, void* stream);
+/* spmv_coo_col_outer (spmv.cpp:105-109): column-sorted triplets; y is
+ * zeroed, then fp64 reductions into y (order of additions not fixed). */
+int spmvtk_k_spmv_coo_col(int64_t n, int64_t nnz, const int32_t* row,
+                          const int32_t* col, const double* val,
+                          const double* x, double* y, void* stream);
+/* spmv_ell_inner (spmv.cpp:117-136): thread per row pair, bands in order,
+ * 128-bit loads; every slot (padding included) is multiplied. */
+int spmvtk_k_spmv_ell_cm(int64_t n, int32_t nz, int64_t ld, const double* val,
+                         const int32_t* col, const double* x, double* y,
+                         void* stream);
+/* spmv_ell_outer (spmv.cpp:138-158): bands split in `splits` contiguous
+ * chunks (partition_range rule), per-chunk partial vectors in `partial`
+ * (device, splits*n doubles), then an ascending-chunk reduction. */
+int spmvtk_k_spmv_ell_cm_split(int64_t n, int32_t nz, int64_t ld,
+                               const double* val, const int32_t* col,
+                               const double* x, double* y, int32_t splits,
+                               double* partial, void* stream);
+/* Row-major ELL SpMV (no reference counterpart). */
+int spmvtk_k_spmv_ell_rm(int64_t n, int32_t nz, const double* val,
+                         const int32_t* col, const double* x, double* y,
+                         void* stream);
+
+/* Forces every kernel of the library to be loaded (lazy module loading
+ * would otherwise charge the first timed call). */
+int spmvtk_k_preload(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SPMVTK_KERNELS_H */

@@ -1,0 +1,528 @@
+// capi.cpp -- the C ABI (include/spmvtk/spmvtk.h).
+//
+// Error firewall as in /root/reference/proj/src/capi.cpp:33-62: every entry
+// point catches, maps ErrorCode -> status (InvalidArgument -> USAGE,
+// MemoryLimit -> MEMORY_LIMIT, the rest -> DATA), stores what() in a
+// thread-local string and clears it on success.  No exception crosses the
+// ABI.  Handles own device memory (matrix.hpp).
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <fstream>
+#include <iterator>
+#include <limits>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "autotune.hpp"
+#include "generators.hpp"
+#include "matrix.hpp"
+#include "mmio.hpp"
+#include "runtime.hpp"
+#include "spmvtk/spmvtk.h"
+
+using namespace spmvtk;
+
+struct spmvtk_profile {
+  at::Profile p;
+};
+
+namespace {
+
+thread_local std::string t_error;
+
+spmvtk_status to_status(ErrorCode c) {
+  switch (c) {
+    case ErrorCode::InvalidArgument: return SPMVTK_ERR_USAGE;
+    case ErrorCode::MemoryLimit: return SPMVTK_ERR_MEMORY_LIMIT;
+    default: return SPMVTK_ERR_DATA;
+  }
+}
+
+template <typename F>
+spmvtk_status guarded(F&& f) {
+  try {
+    f();
+    t_error.clear();
+    return SPMVTK_OK;
+  } catch (const Error& e) {
+    t_error = e.what();
+    return to_status(e.code());
+  } catch (const std::bad_alloc&) {
+    t_error = "host allocation failed";
+    return SPMVTK_ERR_MEMORY_LIMIT;
+  } catch (const std::exception& e) {
+    t_error = e.what();
+    return SPMVTK_ERR_DATA;
+  }
+}
+
+void need(const void* p, const char* msg = "null argument") {
+  if (!p) throw Error(ErrorCode::InvalidArgument, msg);
+}
+
+const dev::Matrix& crs_of(const spmvtk_matrix* m) {
+  if (!m) throw Error(ErrorCode::InvalidArgument, "null matrix handle");
+  if (m->format != SPMVTK_FORMAT_CRS)
+    throw Error(ErrorCode::InvalidArgument, "operation requires a CRS handle");
+  return *m;
+}
+
+dev::Matrix* upload(const gen::HostCrs& h) {
+  if (h.wide())
+    return dev::crs_from_arrays(h.n, h.nnz(), h.row_ptr.data(), h.col_idx.data(), h.values.data(),
+                                8, h.base, false);
+  return dev::crs_from_arrays(h.n, h.nnz(), h.row_ptr32.data(), h.col32.data(), h.values.data(), 4,
+                              h.base, false);
+}
+
+bool valid_format(int f) { return f >= SPMVTK_FORMAT_CRS && f <= SPMVTK_FORMAT_ELL_ROWMAJOR; }
+bool valid_kernel(int k) { return k >= SPMVTK_KERNEL_CRS && k <= SPMVTK_KERNEL_ELL_ROWMAJOR; }
+
+// 1-based triplets of any handle (for the Matrix Market writer)
+void triplets(const dev::Matrix& m, std::vector<std::int64_t>& r, std::vector<std::int64_t>& c,
+              std::vector<double>& v) {
+  auto get_idx = [&](spmvtk_array a) {
+    std::int64_t len = dev::copy_array(m, a, nullptr, 0, 8, 1);
+    std::vector<std::int64_t> out(static_cast<std::size_t>(len));
+    dev::copy_array(m, a, out.data(), len, 8, 1);
+    return out;
+  };
+  std::int64_t vl = dev::copy_array(m, SPMVTK_ARRAY_VALUES, nullptr, 0, 8, 1);
+  std::vector<double> vals(static_cast<std::size_t>(vl));
+  dev::copy_array(m, SPMVTK_ARRAY_VALUES, vals.data(), vl, 8, 1);
+  switch (m.format) {
+    case SPMVTK_FORMAT_CRS:
+    case SPMVTK_FORMAT_CCS: {
+      auto ptr = get_idx(SPMVTK_ARRAY_POINTER);
+      auto idx = get_idx(m.format == SPMVTK_FORMAT_CRS ? SPMVTK_ARRAY_COL_IDX : SPMVTK_ARRAY_ROW_IDX);
+      std::vector<std::int64_t> seg(idx.size());
+      for (std::int64_t s = 1; s <= m.n; ++s)
+        for (std::int64_t p = ptr[s - 1]; p < ptr[s]; ++p) seg[static_cast<std::size_t>(p - 1)] = s;
+      if (m.format == SPMVTK_FORMAT_CRS) {
+        r = std::move(seg);
+        c = std::move(idx);
+      } else {
+        r = std::move(idx);
+        c = std::move(seg);
+      }
+      v = std::move(vals);
+      return;
+    }
+    case SPMVTK_FORMAT_COO_ROW:
+    case SPMVTK_FORMAT_COO_COL:
+      r = get_idx(SPMVTK_ARRAY_ROW_IDX);
+      c = get_idx(SPMVTK_ARRAY_COL_IDX);
+      v = std::move(vals);
+      return;
+    case SPMVTK_FORMAT_ELL:
+    case SPMVTK_FORMAT_ELL_ROWMAJOR: {
+      // drop exactly the padding slots using row_entry_count (convert.cpp:166-183)
+      auto col = get_idx(SPMVTK_ARRAY_COL_IDX);
+      std::int64_t cl = dev::copy_array(m, SPMVTK_ARRAY_ROW_ENTRY_COUNT, nullptr, 0, 8, 0);
+      std::vector<std::int64_t> cnt(static_cast<std::size_t>(cl));
+      dev::copy_array(m, SPMVTK_ARRAY_ROW_ENTRY_COUNT, cnt.data(), cl, 8, 0);
+      const std::int64_t nz = m.band_count;
+      for (std::int64_t i = 0; i < m.n; ++i)
+        for (std::int64_t k = 0; k < cnt[static_cast<std::size_t>(i)]; ++k) {
+          std::size_t s = m.format == SPMVTK_FORMAT_ELL ? static_cast<std::size_t>(k * m.n + i)
+                                                        : static_cast<std::size_t>(i * nz + k);
+          r.push_back(i + 1);
+          c.push_back(col[s]);
+          v.push_back(vals[s]);
+        }
+      return;
+    }
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* spmvtk_last_error(void) { return t_error.c_str(); }
+
+void spmvtk_matrix_free(spmvtk_matrix* m) {
+  if (!m) return;
+  // buffers may still be in use by work queued on any stream of this thread
+  cudaDeviceSynchronize();
+  delete m;
+}
+
+void spmvtk_profile_free(spmvtk_profile* p) { delete p; }
+
+spmvtk_status spmvtk_read_matrix_market(const char* path, spmvtk_matrix** out) {
+  return guarded([&] {
+    need(path);
+    need(out);
+    *out = upload(mm::read(path));
+  });
+}
+
+spmvtk_status spmvtk_write_matrix_market(const spmvtk_matrix* m, const char* path) {
+  return guarded([&] {
+    need(m);
+    need(path);
+    std::vector<std::int64_t> r, c;
+    std::vector<double> v;
+    triplets(*m, r, c, v);
+    mm::write(m->n, std::move(r), std::move(c), std::move(v), m->format != SPMVTK_FORMAT_CRS, path);
+  });
+}
+
+spmvtk_status spmvtk_gen_banded(int64_t n, int64_t half_width, spmvtk_matrix** out) {
+  return guarded([&] {
+    need(out, "null output");
+    *out = upload(gen::banded(n, half_width));
+  });
+}
+
+spmvtk_status spmvtk_gen_skewed(int64_t n, int64_t base_deg, int64_t heavy_rows,
+                                int64_t heavy_deg, uint64_t seed, spmvtk_matrix** out) {
+  return guarded([&] {
+    need(out, "null output");
+    *out = upload(gen::skewed(n, base_deg, heavy_rows, heavy_deg, seed));
+  });
+}
+
+spmvtk_status spmvtk_gen_cv_target(int64_t n, double mean_deg, double target_dmat,
+                                   uint64_t seed, spmvtk_matrix** out) {
+  return guarded([&] {
+    need(out, "null output");
+    *out = upload(gen::cv_target(n, mean_deg, target_dmat, seed));
+  });
+}
+
+spmvtk_format spmvtk_matrix_get_format(const spmvtk_matrix* m) {
+  return m ? m->format : SPMVTK_FORMAT_CRS;
+}
+
+spmvtk_status spmvtk_matrix_get_info(const spmvtk_matrix* m, spmvtk_matrix_info* out) {
+  return guarded([&] {
+    need(out, "null output");
+    const dev::Matrix& a = crs_of(m);
+    out->n = a.n;
+    out->nnz = a.nnz;
+    rt::Moments mo = dev::crs_moments(a);
+    out->max_row_entries = static_cast<int64_t>(mo.max);
+    out->ell_bytes = static_cast<uint64_t>(a.n) * mo.max * 16ull;
+    rt::RowStatsD s = rt::stats_from_moments(mo, a.n);
+    out->mu = s.mu;
+    out->sigma = s.sigma;
+    out->d_mat = s.d_mat;
+  });
+}
+
+spmvtk_status spmvtk_matrix_convert(const spmvtk_matrix* m, spmvtk_format to,
+                                    uint64_t max_bytes, spmvtk_matrix** out) {
+  return guarded([&] {
+    need(out, "null output");
+    const dev::Matrix& a = crs_of(m);
+    if (!valid_format(to)) throw Error(ErrorCode::InvalidArgument, "unknown target format");
+    *out = dev::convert(a, to, max_bytes);
+  });
+}
+
+spmvtk_status spmvtk_spmv(const spmvtk_matrix* m, spmvtk_kernel kernel, const double* x,
+                          int64_t len, int lanes, double* y, double* elapsed_seconds) {
+  return guarded([&] {
+    if (!m || !x || !y) throw Error(ErrorCode::InvalidArgument, "null argument");
+    if (!valid_kernel(kernel)) throw Error(ErrorCode::InvalidArgument, "unknown kernel id");
+    if (kernel != SPMVTK_KERNEL_CRS && lanes < 1)
+      throw Error(ErrorCode::InvalidArgument, "lane count must be at least 1");
+    if (len != m->n)
+      throw Error(ErrorCode::InvalidArgument, "vector length " + std::to_string(len) +
+                                                  " does not match matrix dimension " +
+                                                  std::to_string(m->n));
+    rt::init();
+    const std::size_t n = static_cast<std::size_t>(m->n);
+    rt::DevArray<double> dx(std::max<std::size_t>(n, 1), "x"), dy(std::max<std::size_t>(n, 1), "y");
+    rt::copy_to_device(dx.get(), x, n * sizeof(double));
+    rt::EventTimer timer;
+    timer.start();
+    dev::spmv_device(*m, kernel, dx.get(), dy.get());
+    double secs = timer.stop_seconds();
+    rt::copy_to_host(y, dy.get(), n * sizeof(double));
+    if (elapsed_seconds) *elapsed_seconds = secs;
+  });
+}
+
+spmvtk_status spmvtk_bench(const spmvtk_matrix* m, spmvtk_kernel variant, int lanes,
+                           int repeats, uint64_t max_bytes, spmvtk_bench_result* out) {
+  return guarded([&] {
+    need(out, "null output");
+    const dev::Matrix& a = crs_of(m);
+    if (!valid_kernel(variant)) throw Error(ErrorCode::InvalidArgument, "unknown kernel id");
+    at::Timings t = at::bench(a, variant, lanes, repeats, max_bytes);
+    at::Metrics cm = at::compute_metrics(t);
+    out->t_crs = t.t_crs;
+    out->t_ell = t.t_ell;
+    out->t_trans = t.t_trans;
+    out->sp = cm.sp;
+    out->tt = cm.tt;
+    out->r = cm.r;
+  });
+}
+
+spmvtk_status spmvtk_profile_build(const spmvtk_matrix* const* matrices,
+                                   const char* const* ids, size_t count,
+                                   spmvtk_kernel variant, int lanes, double c, int repeats,
+                                   uint64_t max_bytes, const char* machine_label,
+                                   spmvtk_profile** out) {
+  return guarded([&] {
+    if (!matrices || !ids || !out) throw Error(ErrorCode::InvalidArgument, "null argument");
+    if (!valid_kernel(variant)) throw Error(ErrorCode::InvalidArgument, "unknown kernel id");
+    std::vector<std::pair<std::string, const dev::Matrix*>> set;
+    for (size_t i = 0; i < count; ++i) set.emplace_back(ids[i] ? ids[i] : "", &crs_of(matrices[i]));
+    auto prof = std::make_unique<spmvtk_profile>();
+    prof->p = at::offline_profile(set, variant, lanes, c, repeats, max_bytes,
+                                  machine_label ? machine_label : "");
+    *out = prof.release();
+  });
+}
+
+spmvtk_status spmvtk_profile_write(const spmvtk_profile* p, const char* path) {
+  return guarded([&] {
+    if (!p || !path) throw Error(ErrorCode::InvalidArgument, "null argument");
+    std::ofstream f(path);
+    if (!f) throw Error(ErrorCode::Io, std::string("cannot open ") + path + " for writing");
+    f << at::profile_to_json(p->p) << '\n';
+    if (!f) throw Error(ErrorCode::Io, std::string("write failed: ") + path);
+  });
+}
+
+spmvtk_status spmvtk_profile_read(const char* path, spmvtk_profile** out) {
+  return guarded([&] {
+    if (!path || !out) throw Error(ErrorCode::InvalidArgument, "null argument");
+    std::ifstream f(path);
+    if (!f) throw Error(ErrorCode::Io, std::string("cannot open ") + path);
+    std::string text((std::istreambuf_iterator<char>(f)), std::istreambuf_iterator<char>());
+    auto prof = std::make_unique<spmvtk_profile>();
+    prof->p = at::profile_from_json(text);
+    *out = prof.release();
+  });
+}
+
+double spmvtk_profile_d_star(const spmvtk_profile* p) { return p ? p->p.d_star : 0.0; }
+double spmvtk_profile_c(const spmvtk_profile* p) { return p ? p->p.c : 0.0; }
+int spmvtk_profile_lanes(const spmvtk_profile* p) { return p ? p->p.lanes : 0; }
+spmvtk_kernel spmvtk_profile_kernel(const spmvtk_profile* p) {
+  return p ? p->p.kernel : SPMVTK_KERNEL_CRS;
+}
+size_t spmvtk_profile_record_count(const spmvtk_profile* p) { return p ? p->p.records.size() : 0; }
+
+spmvtk_status spmvtk_profile_record(const spmvtk_profile* p, size_t index,
+                                    spmvtk_record_view* out) {
+  return guarded([&] {
+    if (!p || !out) throw Error(ErrorCode::InvalidArgument, "null argument");
+    if (index >= p->p.records.size())
+      throw Error(ErrorCode::InvalidArgument, "record index out of range");
+    const at::Record& r = p->p.records[index];
+    const double nan = std::numeric_limits<double>::quiet_NaN();
+    out->matrix_id = r.matrix_id.c_str();
+    out->n = r.n;
+    out->nnz = r.nnz;
+    out->mu = r.mu;
+    out->sigma = r.sigma;
+    out->d_mat = r.d_mat;
+    out->excluded = r.excluded ? 1 : 0;
+    out->exclusion_reason = r.exclusion_reason ? r.exclusion_reason->c_str() : nullptr;
+    out->t_crs = r.timings ? r.timings->t_crs : nan;
+    out->t_ell = r.timings ? r.timings->t_ell : nan;
+    out->t_trans = r.timings ? r.timings->t_trans : nan;
+    out->sp = r.metrics ? r.metrics->sp : nan;
+    out->tt = r.metrics ? r.metrics->tt : nan;
+    out->r = r.metrics ? r.metrics->r : nan;
+  });
+}
+
+spmvtk_status spmvtk_select(const spmvtk_matrix* m, const spmvtk_profile* p,
+                            spmvtk_decision* decision, double* d_mat) {
+  return guarded([&] {
+    if (!p || !decision) throw Error(ErrorCode::InvalidArgument, "null argument");
+    const dev::Matrix& a = crs_of(m);
+    // fresh GPU reduction for the on-line phase (autotune.cpp:231-236)
+    rt::init();
+    rt::Moments mo = rt::row_moments(a.ptr.get(), a.n);
+    double dm = rt::stats_from_moments(mo, a.n).d_mat;
+    *decision = dm < p->p.d_star ? SPMVTK_USE_ELL : SPMVTK_USE_CRS;
+    if (d_mat) *d_mat = dm;
+  });
+}
+
+// ------------------------------ extensions -------------------------------
+
+void spmvtk_set_stream(void* stream) { rt::set_stream(static_cast<cudaStream_t>(stream)); }
+void* spmvtk_get_stream(void) { return rt::stream(); }
+
+spmvtk_status spmvtk_synchronize(void) {
+  return guarded([&] { rt::sync(); });
+}
+
+spmvtk_status spmvtk_matrix_from_crs(int64_t n, int64_t nnz, const void* row_ptr,
+                                     const void* col_idx, const double* values,
+                                     int index_width, int index_base, int on_device,
+                                     spmvtk_matrix** out) {
+  return guarded([&] {
+    need(out, "null output");
+    *out = dev::crs_from_arrays(n, nnz, row_ptr, col_idx, values, index_width, index_base,
+                                on_device != 0);
+  });
+}
+
+spmvtk_status spmvtk_matrix_describe(const spmvtk_matrix* m, spmvtk_matrix_desc* out) {
+  return guarded([&] {
+    need(m);
+    need(out);
+    out->format = m->format;
+    out->ordering = m->ordering;
+    out->n = m->n;
+    out->nnz = m->nnz;
+    out->band_count = m->band_count;
+    out->ld = m->ld;
+    out->device_bytes = m->device_bytes();
+  });
+}
+
+spmvtk_status spmvtk_matrix_copy_array(const spmvtk_matrix* m, spmvtk_array which, void* dst,
+                                       int64_t capacity, int index_width, int index_base,
+                                       int64_t* len) {
+  return guarded([&] {
+    need(m);
+    need(len);
+    if (index_base != 0 && index_base != 1)
+      throw Error(ErrorCode::InvalidArgument, "index_base must be 0 or 1");
+    *len = dev::copy_array(*m, which, dst, capacity, index_width, index_base);
+  });
+}
+
+spmvtk_status spmvtk_matrix_device_array(const spmvtk_matrix* m, spmvtk_array which, void** ptr,
+                                         int64_t* len) {
+  return guarded([&] {
+    need(m);
+    need(ptr);
+    std::int64_t l = dev::device_array(*m, which, ptr);
+    if (len) *len = l;
+  });
+}
+
+spmvtk_status spmvtk_spmv_device(const spmvtk_matrix* m, spmvtk_kernel kernel, const double* x,
+                                 double* y) {
+  return guarded([&] {
+    if (!m || ((!x || !y) && m->n > 0)) throw Error(ErrorCode::InvalidArgument, "null argument");
+    if (!valid_kernel(kernel)) throw Error(ErrorCode::InvalidArgument, "unknown kernel id");
+    dev::spmv_device(*m, kernel, x, y);
+  });
+}
+
+spmvtk_status spmvtk_matrix_row_stats(const spmvtk_matrix* m, spmvtk_row_stats* out) {
+  return guarded([&] {
+    need(out, "null output");
+    const dev::Matrix& a = crs_of(m);
+    rt::Moments mo = dev::crs_moments(a);
+    out->n = a.n;
+    out->nnz = a.nnz;
+    out->max_row = static_cast<int64_t>(mo.max);
+    rt::RowStatsD s = rt::stats_from_moments(mo, a.n);
+    out->mu = s.mu;
+    out->sigma = s.sigma;
+    out->d_mat = s.d_mat;
+  });
+}
+
+spmvtk_status spmvtk_gen_baseline(int config, int64_t param, double dparam, uint64_t seed,
+                                  spmvtk_matrix** out) {
+  return guarded([&] {
+    need(out, "null output");
+    *out = upload(gen::baseline(config, param, dparam, seed));
+  });
+}
+
+struct spmvtk_host_crs {
+  gen::HostCrs h;
+};
+
+spmvtk_status spmvtk_gen_baseline_host(int config, int64_t param, double dparam, uint64_t seed,
+                                       spmvtk_host_crs** out, int64_t* n, int64_t* nnz) {
+  return guarded([&] {
+    need(out, "null output");
+    auto h = std::make_unique<spmvtk_host_crs>();
+    h->h = gen::baseline(config, param, dparam, seed);
+    if (n) *n = h->h.n;
+    if (nnz) *nnz = h->h.nnz();
+    *out = h.release();
+  });
+}
+
+spmvtk_status spmvtk_host_crs_export(const spmvtk_host_crs* hc, int64_t* row_ptr,
+                                     int64_t* col_idx, double* values, int index_base) {
+  return guarded([&] {
+    need(hc);
+    const gen::HostCrs& h = hc->h;
+    const std::int64_t shift = index_base - h.base;
+    if (row_ptr)
+      for (std::int64_t i = 0; i <= h.n; ++i)
+        row_ptr[i] = (h.wide() ? h.row_ptr[i] : h.row_ptr32[i]) + shift;
+    if (col_idx)
+      for (std::int64_t p = 0; p < h.nnz(); ++p)
+        col_idx[p] = (h.wide() ? h.col_idx[p] : h.col32[p]) + shift;
+    if (values) std::memcpy(values, h.values.data(), h.values.size() * sizeof(double));
+  });
+}
+
+void spmvtk_host_crs_free(spmvtk_host_crs* h) { delete h; }
+
+spmvtk_status spmvtk_matrix_from_host_crs(const spmvtk_host_crs* h, spmvtk_matrix** out) {
+  return guarded([&] {
+    need(h);
+    need(out, "null output");
+    *out = upload(h->h);
+  });
+}
+
+spmvtk_status spmvtk_gen_vector(int64_t n, uint64_t seed, double* out) {
+  return guarded([&] {
+    need(out, "null output");
+    gen::vector_u11(n, seed, out);
+  });
+}
+
+spmvtk_status spmvtk_conversion_bytes(const spmvtk_matrix* m, spmvtk_format to,
+                                      uint64_t* reference_estimate, uint64_t* device_bytes) {
+  return guarded([&] {
+    const dev::Matrix& a = crs_of(m);
+    if (!valid_format(to)) throw Error(ErrorCode::InvalidArgument, "unknown target format");
+    if (reference_estimate) *reference_estimate = dev::reference_ell_estimate(a);
+    if (device_bytes) *device_bytes = dev::device_bytes_for(a, to);
+  });
+}
+
+spmvtk_status spmvtk_compute_metrics(double t_crs, double t_ell, double t_trans, double* sp,
+                                     double* tt, double* r) {
+  return guarded([&] {
+    at::Metrics m = at::compute_metrics(at::Timings{t_crs, t_ell, t_trans});
+    if (sp) *sp = m.sp;
+    if (tt) *tt = m.tt;
+    if (r) *r = m.r;
+  });
+}
+
+spmvtk_status spmvtk_amortization_iterations(double t_crs, double t_ell, double t_trans,
+                                             int64_t* k) {
+  return guarded([&] {
+    need(k);
+    auto v = at::amortization(at::Timings{t_crs, t_ell, t_trans});
+    *k = v ? *v : -1;
+  });
+}
+
+double spmvtk_find_d_star(const double* d_mat, const double* r, size_t count, double c) {
+  std::vector<std::pair<double, double>> pts;
+  for (size_t i = 0; i < count; ++i) pts.emplace_back(d_mat[i], r[i]);
+  return at::find_d_star(std::move(pts), c);
+}
+
+const char* spmvtk_version(void) { return "spmvtk-b200 0.1 (sm_100a)"; }
+
+}  // extern "C"

@@ -1,0 +1,94 @@
+// common.cuh -- shared device helpers for the sm_100a kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <climits>
+#include <cstdint>
+
+namespace spmvtk_dev {
+
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int kSMs = 148;  // B200: 2 dies x 74 SMs
+
+#define SPMVTK_LAUNCH_RETURN()                        \
+  do {                                                \
+    cudaError_t e__ = cudaGetLastError();             \
+    return e__ == cudaSuccess ? 0 : static_cast<int>(e__); \
+  } while (0)
+
+inline cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+// read-only, streaming loads (L1 no-allocate): matrix arrays are touched once
+__device__ __forceinline__ double ld_stream(const double* p) {
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ int ld_stream(const int* p) {
+  int v;
+  asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double2 ld_stream2(const double2* p) {
+  double2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];"
+               : "=d"(v.x), "=d"(v.y)
+               : "l"(p));
+  return v;
+}
+__device__ __forceinline__ int2 ld_stream2(const int2* p) {
+  int2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.s32 {%0, %1}, [%2];"
+               : "=r"(v.x), "=r"(v.y)
+               : "l"(p));
+  return v;
+}
+__device__ __forceinline__ int4 ld_stream4(const int4* p) {
+  int4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+// x gathers: keep them cacheable (x is small and reused)
+__device__ __forceinline__ double ld_x(const double* p) { return __ldg(p); }
+
+// streaming stores (evict-first from L1)
+__device__ __forceinline__ void st_stream(double* p, double v) {
+  asm volatile("st.global.L1::no_allocate.f64 [%0], %1;" ::"l"(p), "d"(v));
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v, int width = 32) {
+  for (int o = width / 2; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o, width);
+  return v;
+}
+
+// Fast unsigned division by a runtime-invariant divisor (Granlund-Montgomery,
+// as in Hacker's Delight 10-8).  Valid for every 32-bit x.
+struct FastDiv {
+  uint32_t d, m, s;
+  __host__ __device__ FastDiv() : d(1), m(0), s(0) {}
+  __host__ explicit FastDiv(uint32_t div) : d(div) {
+    s = 0;
+    while ((1u << s) < div) ++s;
+    // m = floor(2^32 * (2^s - d) / d) + 1
+    uint64_t num = (uint64_t(1) << 32) * ((uint64_t(1) << s) - div);
+    m = static_cast<uint32_t>(num / div + 1);
+  }
+  __device__ __forceinline__ uint32_t div(uint32_t x) const {
+    if (s == 0) return x;  // d == 1
+    uint32_t t = __umulhi(x, m);
+    return (t + ((x - t) >> 1)) >> (s - 1);
+  }
+};
+
+inline int grid_for(int64_t work, int block, int per_sm_blocks = 8) {
+  int64_t g = (work + block - 1) / block;
+  int64_t cap = static_cast<int64_t>(kSMs) * per_sm_blocks;
+  if (g > cap) g = cap;
+  return static_cast<int>(g < 1 ? 1 : g);
+}
+
+}  // namespace spmvtk_dev

@@ -1,0 +1,245 @@
+// kernels_util.cu -- row statistics, index-width conversion, validation
+// scans and the device exclusive scan used by the CCS transform.
+//
+// HBM-bound integer work: grid-stride loops sized to a multiple of the 148
+// SMs, warp-shuffle reductions, one atomic per warp.
+#include "common.cuh"
+#include "spmvtk/spmvtk_kernels.h"
+
+using namespace spmvtk_dev;
+
+namespace {
+
+// ---- row statistics ------------------------------------------------------
+// Reference: row_histogram (formats.cpp:184-192) feeds Welford in
+// stats_from_histogram (stats.cpp:9-29); max row length as in
+// estimate_ell_bytes / crs_to_ell (convert.cpp:74-76, :91-96).  The device
+// computes the exact integer moments {max, sum c, sum c^2}; the host turns
+// them into mu / sigma / d_mat (runtime.cpp: stats_from_moments).
+__global__ void __launch_bounds__(256) k_row_stats(const int32_t* __restrict__ ptr,
+                                                   int64_t n,
+                                                   unsigned long long* acc) {
+  unsigned long long mx = 0, s = 0, s2 = 0;
+  bool bad = false;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += stride) {
+    int32_t a = __ldg(ptr + i), b = __ldg(ptr + i + 1);
+    if (b < a) {
+      bad = true;  // non-monotone pointer array
+      continue;
+    }
+    unsigned long long c = static_cast<unsigned long long>(b - a);
+    mx = c > mx ? c : mx;
+    s += c;
+    s2 += c * c;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    unsigned long long om = __shfl_xor_sync(kFull, mx, o);
+    mx = om > mx ? om : mx;
+    s += __shfl_xor_sync(kFull, s, o);
+    s2 += __shfl_xor_sync(kFull, s2, o);
+  }
+  bad = __any_sync(kFull, bad);
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(acc + 0, mx | (bad ? (1ull << 63) : 0ull));
+    atomicAdd(acc + 1, s);
+    atomicAdd(acc + 2, s2);
+  }
+}
+
+__global__ void k_narrow(const int64_t* __restrict__ src, int32_t* __restrict__ dst,
+                         int64_t len, int64_t base) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < len;
+       i += stride)
+    dst[i] = static_cast<int32_t>(src[i] - base);
+}
+
+__global__ void k_widen(const int32_t* __restrict__ src, int64_t* __restrict__ dst,
+                        int64_t len, int64_t base) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < len;
+       i += stride)
+    dst[i] = static_cast<int64_t>(src[i]) + base;
+}
+
+__global__ void k_out_of_range(const int32_t* __restrict__ idx, int64_t len, int64_t n,
+                               unsigned long long* bad) {
+  unsigned long long cnt = 0;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < len;
+       i += stride) {
+    int32_t v = __ldg(idx + i);
+    cnt += (v < 0 || v >= n) ? 1 : 0;
+  }
+  cnt = warp_sum(cnt);
+  if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(bad, cnt);
+}
+
+__global__ void k_descents(const int32_t* __restrict__ key, int64_t len,
+                           unsigned long long* bad) {
+  unsigned long long cnt = 0;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x + 1; i < len;
+       i += stride)
+    cnt += (__ldg(key + i) < __ldg(key + i - 1)) ? 1 : 0;
+  cnt = warp_sum(cnt);
+  if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(bad, cnt);
+}
+
+// ---- exclusive scan (reduce-then-scan, tiles of 4096) --------------------
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 16;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+__device__ __forceinline__ int32_t block_exclusive_scan(int32_t v, int32_t* s_warp,
+                                                        int32_t* total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int32_t inc = v;
+  for (int d = 1; d < 32; d <<= 1) {
+    int32_t t = __shfl_up_sync(kFull, inc, d);
+    if (lane >= d) inc += t;
+  }
+  if (lane == 31) s_warp[wid] = inc;
+  __syncthreads();
+  if (wid == 0) {
+    int32_t w = (lane < kScanThreads / 32) ? s_warp[lane] : 0;
+    int32_t wi = w;
+    for (int d = 1; d < 32; d <<= 1) {
+      int32_t t = __shfl_up_sync(kFull, wi, d);
+      if (lane >= d) wi += t;
+    }
+    if (lane < kScanThreads / 32) s_warp[lane] = wi - w;
+    if (lane == kScanThreads / 32 - 1) *total = wi;
+  }
+  __syncthreads();
+  return s_warp[wid] + inc - v;
+}
+
+__device__ __forceinline__ void load_items(const int32_t* in, int64_t n, int64_t first,
+                                           int32_t (&it)[kScanItems]) {
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    int64_t i = first + j;
+    it[j] = i < n ? __ldg(in + i) : 0;
+  }
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_tiles(const int32_t* __restrict__ in,
+                                                             int64_t n, int32_t* tile_sums) {
+  __shared__ int32_t s_warp[kScanThreads / 32];
+  __shared__ int32_t total;
+  int32_t it[kScanItems];
+  int64_t first = static_cast<int64_t>(blockIdx.x) * kScanTile +
+                  static_cast<int64_t>(threadIdx.x) * kScanItems;
+  load_items(in, n, first, it);
+  int32_t s = 0;
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) s += it[j];
+  block_exclusive_scan(s, s_warp, &total);
+  if (threadIdx.x == 0) tile_sums[blockIdx.x] = total;
+}
+
+// single block: exclusive scan of the tile sums, in place
+__global__ void __launch_bounds__(kScanThreads) k_scan_tile_sums(int32_t* tile_sums,
+                                                                 int64_t tiles) {
+  __shared__ int32_t s_warp[kScanThreads / 32];
+  __shared__ int32_t total;
+  int32_t carry = 0;
+  for (int64_t base = 0; base < tiles; base += kScanThreads) {
+    int64_t i = base + threadIdx.x;
+    int32_t v = i < tiles ? tile_sums[i] : 0;
+    int32_t ex = block_exclusive_scan(v, s_warp, &total);
+    if (i < tiles) tile_sums[i] = ex + carry;
+    carry += total;
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_apply(const int32_t* __restrict__ in,
+                                                             int32_t* __restrict__ out,
+                                                             int64_t n,
+                                                             const int32_t* tile_sums,
+                                                             int64_t tiles) {
+  __shared__ int32_t s_warp[kScanThreads / 32];
+  __shared__ int32_t total;
+  int32_t it[kScanItems];
+  int64_t first = static_cast<int64_t>(blockIdx.x) * kScanTile +
+                  static_cast<int64_t>(threadIdx.x) * kScanItems;
+  load_items(in, n, first, it);
+  int32_t s = 0;
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) s += it[j];
+  int32_t run = block_exclusive_scan(s, s_warp, &total) + tile_sums[blockIdx.x];
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    int64_t i = first + j;
+    if (i < n) out[i] = run;
+    run += it[j];
+  }
+  if (blockIdx.x == tiles - 1 && threadIdx.x == kScanThreads - 1) out[n] = run;
+}
+
+}  // namespace
+
+extern "C" {
+
+int spmvtk_k_row_stats(const int32_t* ptr, int64_t n, unsigned long long* acc,
+                       void* stream) {
+  cudaStream_t s = as_stream(stream);
+  if (cudaMemsetAsync(acc, 0, 3 * sizeof(unsigned long long), s) != cudaSuccess)
+    SPMVTK_LAUNCH_RETURN();
+  if (n > 0) k_row_stats<<<grid_for(n, 256), 256, 0, s>>>(ptr, n, acc);
+  SPMVTK_LAUNCH_RETURN();
+}
+
+int spmvtk_k_narrow_index(const int64_t* src, int32_t* dst, int64_t len,
+                          int64_t base, void* stream) {
+  if (len > 0) k_narrow<<<grid_for(len, 256), 256, 0, as_stream(stream)>>>(src, dst, len, base);
+  SPMVTK_LAUNCH_RETURN();
+}
+
+int spmvtk_k_widen_index(const int32_t* src, int64_t* dst, int64_t len,
+                         int64_t base, void* stream) {
+  if (len > 0) k_widen<<<grid_for(len, 256), 256, 0, as_stream(stream)>>>(src, dst, len, base);
+  SPMVTK_LAUNCH_RETURN();
+}
+
+int spmvtk_k_count_out_of_range(const int32_t* idx, int64_t len, int64_t n,
+                                unsigned long long* bad, void* stream) {
+  cudaStream_t s = as_stream(stream);
+  cudaMemsetAsync(bad, 0, sizeof(unsigned long long), s);
+  if (len > 0) k_out_of_range<<<grid_for(len, 256), 256, 0, s>>>(idx, len, n, bad);
+  SPMVTK_LAUNCH_RETURN();
+}
+
+int spmvtk_k_count_descents(const int32_t* key, int64_t len,
+                            unsigned long long* bad, void* stream) {
+  cudaStream_t s = as_stream(stream);
+  cudaMemsetAsync(bad, 0, sizeof(unsigned long long), s);
+  if (len > 1) k_descents<<<grid_for(len, 256), 256, 0, s>>>(key, len, bad);
+  SPMVTK_LAUNCH_RETURN();
+}
+
+size_t spmvtk_k_scan_scratch_bytes(int64_t n) {
+  int64_t tiles = (n + kScanTile - 1) / kScanTile;
+  return static_cast<size_t>((tiles < 1 ? 1 : tiles) * sizeof(int32_t));
+}
+
+int spmvtk_k_exclusive_scan(const int32_t* in, int32_t* out, int64_t n,
+                            void* scratch, void* stream) {
+  cudaStream_t s = as_stream(stream);
+  if (n <= 0) {
+    cudaMemsetAsync(out, 0, sizeof(int32_t), s);
+    SPMVTK_LAUNCH_RETURN();
+  }
+  int64_t tiles = (n + kScanTile - 1) / kScanTile;
+  int32_t* sums = static_cast<int32_t*>(scratch);
+  k_scan_tiles<<<static_cast<unsigned>(tiles), kScanThreads, 0, s>>>(in, n, sums);
+  k_scan_tile_sums<<<1, kScanThreads, 0, s>>>(sums, tiles);
+  k_scan_apply<<<static_cast<unsigned>(tiles), kScanThreads, 0, s>>>(in, out, n, sums, tiles);
+  SPMVTK_LAUNCH_RETURN();
+}
+
+}  // extern "C"

@@ -1,0 +1,428 @@
+// matrix.cpp -- handle construction, conversions and SpMV dispatch.
+#include "matrix.hpp"
+
+#include <algorithm>
+#include <climits>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "spmvtk/spmvtk_kernels.h"
+
+namespace spmvtk::dev {
+
+using rt::DevArray;
+
+namespace {
+
+void* s() { return rt::stream(); }
+
+std::int64_t round_up(std::int64_t v, std::int64_t a) { return (v + a - 1) / a * a; }
+
+void require_int32_range(std::int64_t n, std::int64_t nnz) {
+  if (n < 0) throw Error(ErrorCode::InvalidArgument, "negative dimension");
+  if (n >= INT32_MAX || nnz >= INT32_MAX)
+    throw Error(ErrorCode::InvalidArgument,
+                "matrix exceeds the int32 device index range (n or nnz >= 2^31-1)");
+}
+
+// Copies an index array given in (width, base, location) into an int32
+// 0-based device array; narrowing / rebasing runs on the GPU.
+void upload_index(DevArray<std::int32_t>& dst, const void* src, std::int64_t len, int width,
+                  int base, bool on_device, const char* what) {
+  dst.reset(static_cast<std::size_t>(len), what);
+  if (len == 0) return;
+  if (width == 4) {
+    if (on_device)
+      rt::check(cudaMemcpyAsync(dst.get(), src, len * 4, cudaMemcpyDeviceToDevice, rt::stream()),
+                what);
+    else
+      rt::copy_to_device(dst.get(), src, len * 4);
+    if (base != 0) {
+      // rebase in place through the widening kernels' int32 path
+      DevArray<std::int64_t> tmp(static_cast<std::size_t>(len), what);
+      rt::check_launch(spmvtk_k_widen_index(dst.get(), tmp.get(), len, 0, s()), what);
+      rt::check_launch(spmvtk_k_narrow_index(tmp.get(), dst.get(), len, base, s()), what);
+    }
+  } else {
+    DevArray<std::int64_t> tmp(static_cast<std::size_t>(len), what);
+    if (on_device)
+      rt::check(cudaMemcpyAsync(tmp.get(), src, len * 8, cudaMemcpyDeviceToDevice, rt::stream()),
+                what);
+    else
+      rt::copy_to_device(tmp.get(), src, len * 8);
+    rt::check_launch(spmvtk_k_narrow_index(tmp.get(), dst.get(), len, base, s()), what);
+  }
+}
+
+unsigned long long count_bad_indices(const std::int32_t* idx, std::int64_t len, std::int64_t n) {
+  DevArray<unsigned long long> bad(1, "validation");
+  rt::check_launch(spmvtk_k_count_out_of_range(idx, len, n, bad.get(), s()), "validation");
+  unsigned long long h = 0;
+  rt::copy_to_host(&h, bad.get(), sizeof(h));
+  return h;
+}
+
+Matrix* new_matrix(spmvtk_format f, std::int64_t n, std::int64_t nnz) {
+  auto* m = new Matrix;
+  m->format = f;
+  m->n = n;
+  m->nnz = nnz;
+  cudaGetDevice(&m->device);
+  return m;
+}
+
+int ell_splits(std::int64_t n, std::int32_t nz) {
+  // band split only pays when row pairs alone cannot fill 148 SMs x 2048
+  const std::int64_t want = 148LL * 2048;
+  const std::int64_t pairs = (n + 1) / 2;
+  if (nz <= 1 || pairs >= want) return 1;
+  std::int64_t sp = (want + pairs - 1) / pairs;
+  return static_cast<int>(std::min<std::int64_t>(sp, nz));
+}
+
+}  // namespace
+
+const char* kernel_label(spmvtk_kernel k) {
+  switch (k) {
+    case SPMVTK_KERNEL_CRS: return "crs";
+    case SPMVTK_KERNEL_COO_ROW_OUTER: return "coo-row";
+    case SPMVTK_KERNEL_COO_COL_OUTER: return "coo-col";
+    case SPMVTK_KERNEL_ELL_INNER: return "ell-inner";
+    case SPMVTK_KERNEL_ELL_OUTER: return "ell-outer";
+    case SPMVTK_KERNEL_ELL_ROWMAJOR: return "ell-row";
+  }
+  return "unknown";
+}
+
+rt::Moments crs_moments(const Matrix& m) {
+  std::lock_guard<std::mutex> lk(m.mu);
+  if (!m.moments) m.moments = rt::row_moments(m.ptr.get(), m.n);
+  return *m.moments;
+}
+
+Matrix* crs_from_arrays(std::int64_t n, std::int64_t nnz, const void* row_ptr,
+                        const void* col_idx, const double* values, int index_width,
+                        int index_base, bool on_device) {
+  rt::init();
+  require_int32_range(n, nnz);
+  if (nnz < 0) throw Error(ErrorCode::InvalidArgument, "negative nnz");
+  if (index_width != 4 && index_width != 8)
+    throw Error(ErrorCode::InvalidArgument, "index_width must be 4 or 8");
+  if (index_base != 0 && index_base != 1)
+    throw Error(ErrorCode::InvalidArgument, "index_base must be 0 or 1");
+  if (!row_ptr || ((!col_idx || !values) && nnz > 0))
+    throw Error(ErrorCode::InvalidArgument, "null array");
+  std::unique_ptr<Matrix> m(new_matrix(SPMVTK_FORMAT_CRS, n, nnz));
+  upload_index(m->ptr, row_ptr, n + 1, index_width, index_base, on_device, "row_ptr upload");
+  upload_index(m->col, col_idx, nnz, index_width, index_base, on_device, "col_idx upload");
+  m->val.reset(static_cast<std::size_t>(nnz), "values upload");
+  if (nnz) {
+    rt::check(cudaMemcpyAsync(m->val.get(), values, nnz * sizeof(double),
+                              on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                              rt::stream()),
+              "values upload");
+  }
+  // validation on the GPU (formats.cpp:19-41 pointer rules, :43-52 ranges)
+  std::int32_t ends[2] = {0, 0};
+  rt::copy_to_host(&ends[0], m->ptr.get(), sizeof(std::int32_t));
+  rt::copy_to_host(&ends[1], m->ptr.get() + n, sizeof(std::int32_t));
+  if (ends[0] != 0) throw Error(ErrorCode::Validation, "row_ptr[1] != 1");
+  if (ends[1] != nnz)
+    throw Error(ErrorCode::Validation, "pointer array end " + std::to_string(ends[1] + 1) +
+                                           ", expected nnz+1 = " + std::to_string(nnz + 1));
+  rt::Moments mo = rt::row_moments(m->ptr.get(), n);
+  if (!mo.monotone) throw Error(ErrorCode::Validation, "row_ptr not nondecreasing");
+  m->moments = mo;
+  if (nnz && count_bad_indices(m->col.get(), nnz, n))
+    throw Error(ErrorCode::Validation, "column index out of range");
+  return m.release();
+}
+
+std::uint64_t reference_ell_estimate(const Matrix& crs) {
+  rt::Moments mo = crs_moments(crs);
+  return static_cast<std::uint64_t>(crs.n) * mo.max * 16ull;
+}
+
+std::uint64_t device_bytes_for(const Matrix& crs, spmvtk_format to) {
+  const std::uint64_t n = static_cast<std::uint64_t>(crs.n);
+  const std::uint64_t nnz = static_cast<std::uint64_t>(crs.nnz);
+  switch (to) {
+    case SPMVTK_FORMAT_CRS:
+    case SPMVTK_FORMAT_CCS: return 12 * nnz + 4 * (n + 1);
+    case SPMVTK_FORMAT_COO_ROW:
+    case SPMVTK_FORMAT_COO_COL: return 16 * nnz;
+    case SPMVTK_FORMAT_ELL: {
+      rt::Moments mo = crs_moments(crs);
+      return 12ull * static_cast<std::uint64_t>(round_up(crs.n, 32)) * mo.max + 4 * n;
+    }
+    case SPMVTK_FORMAT_ELL_ROWMAJOR: {
+      rt::Moments mo = crs_moments(crs);
+      return 12ull * n * mo.max + 4 * n;
+    }
+  }
+  return 0;
+}
+
+Matrix* convert(const Matrix& a, spmvtk_format to, std::uint64_t max_bytes) {
+  rt::init();
+  if (a.format != SPMVTK_FORMAT_CRS)
+    throw Error(ErrorCode::InvalidArgument, "operation requires a CRS handle");
+  const std::int64_t n = a.n, nnz = a.nnz;
+  switch (to) {
+    case SPMVTK_FORMAT_CRS: {
+      std::unique_ptr<Matrix> m(new_matrix(SPMVTK_FORMAT_CRS, n, nnz));
+      m->ptr.reset(n + 1, "CRS copy");
+      m->col.reset(nnz, "CRS copy");
+      m->val.reset(nnz, "CRS copy");
+      cudaStream_t st = rt::stream();
+      rt::check(cudaMemcpyAsync(m->ptr.get(), a.ptr.get(), a.ptr.bytes(), cudaMemcpyDeviceToDevice, st), "CRS copy");
+      rt::check(cudaMemcpyAsync(m->col.get(), a.col.get(), a.col.bytes(), cudaMemcpyDeviceToDevice, st), "CRS copy");
+      rt::check(cudaMemcpyAsync(m->val.get(), a.val.get(), a.val.bytes(), cudaMemcpyDeviceToDevice, st), "CRS copy");
+      std::lock_guard<std::mutex> lk(a.mu);
+      m->moments = a.moments;
+      return m.release();
+    }
+    case SPMVTK_FORMAT_COO_ROW: {
+      // convert.cpp:11-22: copy values / col_idx, expand row_ptr
+      std::unique_ptr<Matrix> m(new_matrix(SPMVTK_FORMAT_COO_ROW, n, nnz));
+      m->ordering = 0;
+      m->row.reset(nnz, "COO row_idx");
+      m->col.reset(nnz, "COO col_idx");
+      m->val.reset(nnz, "COO values");
+      cudaStream_t st = rt::stream();
+      if (nnz) {
+        rt::check(cudaMemcpyAsync(m->col.get(), a.col.get(), a.col.bytes(), cudaMemcpyDeviceToDevice, st), "COO copy");
+        rt::check(cudaMemcpyAsync(m->val.get(), a.val.get(), a.val.bytes(), cudaMemcpyDeviceToDevice, st), "COO copy");
+        rt::check_launch(spmvtk_k_expand_ptr(a.ptr.get(), n, nnz, m->row.get(), st), "expand rows");
+      }
+      return m.release();
+    }
+    case SPMVTK_FORMAT_CCS:
+    case SPMVTK_FORMAT_COO_COL: {
+      // Phase I (convert.cpp:24-53) into the output arrays directly; for
+      // COO-col Phase II (convert.cpp:55-66) expands col_ptr into col_idx
+      // and the CCS arrays become the COO arrays without a copy.
+      const bool coo = to == SPMVTK_FORMAT_COO_COL;
+      std::unique_ptr<Matrix> m(new_matrix(to, n, nnz));
+      m->row.reset(nnz, "CCS row_idx");
+      m->val.reset(nnz, "CCS values");
+      DevArray<std::int32_t> colptr(n + 1, "CCS col_ptr");
+      DevArray<unsigned char> scratch(spmvtk_k_ccs_scratch_bytes(n), "CCS scratch");
+      cudaStream_t st = rt::stream();
+      rt::check_launch(spmvtk_k_crs_to_ccs(n, nnz, a.ptr.get(), a.col.get(), a.val.get(),
+                                           colptr.get(), m->row.get(), m->val.get(),
+                                           scratch.get(), st),
+                       "CRS->CCS");
+      if (coo) {
+        m->ordering = 1;
+        m->col.reset(nnz, "COO col_idx");
+        if (nnz)
+          rt::check_launch(spmvtk_k_expand_ptr(colptr.get(), n, nnz, m->col.get(), st),
+                           "expand columns");
+      } else {
+        m->ptr = std::move(colptr);
+      }
+      return m.release();
+    }
+    case SPMVTK_FORMAT_ELL:
+    case SPMVTK_FORMAT_ELL_ROWMAJOR: {
+      // convert.cpp:81-115: guard, band_count = max row, padded scatter.
+      // The max row comes from a fresh GPU reduction (as the reference
+      // recomputes it), never from a cache.
+      rt::Moments mo = rt::row_moments(a.ptr.get(), n);
+      if (max_bytes != 0) {
+        std::uint64_t est = static_cast<std::uint64_t>(n) * mo.max * 16ull;
+        if (est > max_bytes)
+          throw Error(ErrorCode::MemoryLimit, "ELL footprint estimate " + std::to_string(est) +
+                                                  " bytes exceeds limit " +
+                                                  std::to_string(max_bytes));
+      }
+      if (mo.max > static_cast<std::uint64_t>(INT32_MAX))
+        throw Error(ErrorCode::InvalidArgument, "band count exceeds int32");
+      const std::int32_t nz = static_cast<std::int32_t>(mo.max);
+      const bool cm = to == SPMVTK_FORMAT_ELL;
+      std::unique_ptr<Matrix> m(new_matrix(to, n, nnz));
+      m->band_count = nz;
+      m->ld = cm ? round_up(n, 32) : n;
+      const std::size_t slots =
+          static_cast<std::size_t>(cm ? m->ld : n) * static_cast<std::size_t>(nz);
+      m->val.reset(slots, "ELL values");
+      m->col.reset(slots, "ELL col_idx");
+      m->count.reset(n, "ELL row_entry_count");
+      cudaStream_t st = rt::stream();
+      if (cm)
+        rt::check_launch(spmvtk_k_crs_to_ell_cm(n, nz, m->ld, a.ptr.get(), a.col.get(),
+                                                a.val.get(), m->val.get(), m->col.get(),
+                                                m->count.get(), st),
+                         "CRS->ELL");
+      else
+        rt::check_launch(spmvtk_k_crs_to_ell_rm(n, nz, a.ptr.get(), a.col.get(), a.val.get(),
+                                                m->val.get(), m->col.get(), m->count.get(), st),
+                         "CRS->ELL row-major");
+      return m.release();
+    }
+  }
+  throw Error(ErrorCode::InvalidArgument, "unknown target format");
+}
+
+void spmv_device(const Matrix& m, spmvtk_kernel kernel, const double* x, double* y) {
+  cudaStream_t st = rt::stream();
+  switch (kernel) {
+    case SPMVTK_KERNEL_CRS: {
+      if (m.format != SPMVTK_FORMAT_CRS)
+        throw Error(ErrorCode::InvalidArgument, "operation requires a CRS handle");
+      rt::Moments mo = crs_moments(m);
+      const double mean = m.n > 0 ? static_cast<double>(mo.sum) / static_cast<double>(m.n) : 0;
+      DevArray<std::int32_t> long_rows;
+      if (mo.max > 4096) long_rows.reset(m.n + 1, "CRS long-row queue");
+      rt::check_launch(spmvtk_k_spmv_crs(m.n, m.ptr.get(), m.col.get(), m.val.get(), x, y, mean,
+                                         static_cast<std::int32_t>(std::min<std::uint64_t>(mo.max, INT32_MAX)),
+                                         long_rows.get(), st),
+                       "spmv crs");
+      return;
+    }
+    case SPMVTK_KERNEL_COO_ROW_OUTER:
+      if (m.format != SPMVTK_FORMAT_COO_ROW && m.format != SPMVTK_FORMAT_COO_COL)
+        throw Error(ErrorCode::InvalidArgument, "kernel requires a row-major COO handle");
+      if (m.ordering != 0)
+        throw Error(ErrorCode::InvalidArgument,
+                    "spmv_coo_row_outer requires the matching COO ordering");
+      rt::check_launch(spmvtk_k_spmv_coo_row(m.n, m.nnz, m.row.get(), m.col.get(), m.val.get(),
+                                             x, y, st),
+                       "spmv coo-row");
+      return;
+    case SPMVTK_KERNEL_COO_COL_OUTER:
+      if (m.format != SPMVTK_FORMAT_COO_ROW && m.format != SPMVTK_FORMAT_COO_COL)
+        throw Error(ErrorCode::InvalidArgument, "kernel requires a column-major COO handle");
+      if (m.ordering != 1)
+        throw Error(ErrorCode::InvalidArgument,
+                    "spmv_coo_col_outer requires the matching COO ordering");
+      rt::check_launch(spmvtk_k_spmv_coo_col(m.n, m.nnz, m.row.get(), m.col.get(), m.val.get(),
+                                             x, y, st),
+                       "spmv coo-col");
+      return;
+    case SPMVTK_KERNEL_ELL_INNER:
+    case SPMVTK_KERNEL_ELL_OUTER: {
+      if (m.format != SPMVTK_FORMAT_ELL)
+        throw Error(ErrorCode::InvalidArgument, "kernel requires an ELL handle");
+      if (kernel == SPMVTK_KERNEL_ELL_INNER) {
+        rt::check_launch(spmvtk_k_spmv_ell_cm(m.n, m.band_count, m.ld, m.val.get(), m.col.get(),
+                                              x, y, st),
+                         "spmv ell-inner");
+      } else {
+        int splits = ell_splits(m.n, m.band_count);
+        DevArray<double> partial;
+        if (splits > 1) partial.reset(static_cast<std::size_t>(splits) * m.n, "ELL partials");
+        rt::check_launch(spmvtk_k_spmv_ell_cm_split(m.n, m.band_count, m.ld, m.val.get(),
+                                                    m.col.get(), x, y, splits, partial.get(), st),
+                         "spmv ell-outer");
+      }
+      return;
+    }
+    case SPMVTK_KERNEL_ELL_ROWMAJOR:
+      if (m.format != SPMVTK_FORMAT_ELL_ROWMAJOR)
+        throw Error(ErrorCode::InvalidArgument, "kernel requires a row-major ELL handle");
+      rt::check_launch(spmvtk_k_spmv_ell_rm(m.n, m.band_count, m.val.get(), m.col.get(), x, y, st),
+                       "spmv ell-row");
+      return;
+  }
+  throw Error(ErrorCode::InvalidArgument, "unknown kernel id");
+}
+
+std::int64_t device_array(const Matrix& m, spmvtk_array which, void** out) {
+  const DevArray<std::int32_t>* ia = nullptr;
+  switch (which) {
+    case SPMVTK_ARRAY_VALUES:
+      *out = m.val.get();
+      return static_cast<std::int64_t>(m.val.size());
+    case SPMVTK_ARRAY_POINTER: ia = &m.ptr; break;
+    case SPMVTK_ARRAY_ROW_IDX: ia = &m.row; break;
+    case SPMVTK_ARRAY_COL_IDX: ia = &m.col; break;
+    case SPMVTK_ARRAY_ROW_ENTRY_COUNT: ia = &m.count; break;
+  }
+  if (!ia || (ia->size() == 0 && !(which == SPMVTK_ARRAY_COL_IDX || which == SPMVTK_ARRAY_ROW_IDX)))
+    throw Error(ErrorCode::InvalidArgument, "array not present in this format");
+  *out = ia->get();
+  return static_cast<std::int64_t>(ia->size());
+}
+
+std::int64_t copy_array(const Matrix& m, spmvtk_array which, void* dst, std::int64_t capacity,
+                        int index_width, int index_base) {
+  if (which != SPMVTK_ARRAY_VALUES && index_width != 4 && index_width != 8)
+    throw Error(ErrorCode::InvalidArgument, "index_width must be 4 or 8");
+  // which arrays exist per format (formats.hpp of the reference)
+  bool present = false;
+  switch (m.format) {
+    case SPMVTK_FORMAT_CRS:
+      present = which == SPMVTK_ARRAY_VALUES || which == SPMVTK_ARRAY_POINTER ||
+                which == SPMVTK_ARRAY_COL_IDX;
+      break;
+    case SPMVTK_FORMAT_CCS:
+      present = which == SPMVTK_ARRAY_VALUES || which == SPMVTK_ARRAY_POINTER ||
+                which == SPMVTK_ARRAY_ROW_IDX;
+      break;
+    case SPMVTK_FORMAT_COO_ROW:
+    case SPMVTK_FORMAT_COO_COL:
+      present = which == SPMVTK_ARRAY_VALUES || which == SPMVTK_ARRAY_ROW_IDX ||
+                which == SPMVTK_ARRAY_COL_IDX;
+      break;
+    case SPMVTK_FORMAT_ELL:
+    case SPMVTK_FORMAT_ELL_ROWMAJOR:
+      present = which == SPMVTK_ARRAY_VALUES || which == SPMVTK_ARRAY_COL_IDX ||
+                which == SPMVTK_ARRAY_ROW_ENTRY_COUNT;
+      break;
+  }
+  if (!present) throw Error(ErrorCode::InvalidArgument, "array not present in this format");
+
+  const bool ell = m.format == SPMVTK_FORMAT_ELL || m.format == SPMVTK_FORMAT_ELL_ROWMAJOR;
+  const bool ell_cm = m.format == SPMVTK_FORMAT_ELL;
+  std::int64_t len = 0;
+  if (which == SPMVTK_ARRAY_VALUES || which == SPMVTK_ARRAY_COL_IDX)
+    len = ell ? m.n * static_cast<std::int64_t>(m.band_count) : m.nnz;
+  else if (which == SPMVTK_ARRAY_POINTER)
+    len = m.n + 1;
+  else if (which == SPMVTK_ARRAY_ROW_IDX)
+    len = m.nnz;
+  else
+    len = m.n;
+  if (!dst) return len;
+  if (capacity < len) throw Error(ErrorCode::InvalidArgument, "destination too small");
+  if (len == 0) return 0;
+
+  cudaStream_t st = rt::stream();
+  // gather the logical array into a contiguous device buffer (compacting
+  // the ELL leading-dimension padding), then convert width/base
+  const std::size_t esz = which == SPMVTK_ARRAY_VALUES ? 8 : 4;
+  if (which == SPMVTK_ARRAY_ROW_ENTRY_COUNT) index_base = 0;  // a count, not an index
+  void* src = nullptr;
+  device_array(m, which, &src);
+  DevArray<unsigned char> compact;
+  const void* contiguous = src;
+  if (ell_cm && (which == SPMVTK_ARRAY_VALUES || which == SPMVTK_ARRAY_COL_IDX) && m.ld != m.n) {
+    compact.reset(static_cast<std::size_t>(len) * esz, "ELL export");
+    rt::check(cudaMemcpy2DAsync(compact.get(), m.n * esz, src, m.ld * esz, m.n * esz,
+                                m.band_count, cudaMemcpyDeviceToDevice, st),
+              "ELL export");
+    contiguous = compact.get();
+  }
+  if (which == SPMVTK_ARRAY_VALUES || (index_width == 4 && index_base == 0)) {
+    rt::copy_to_host(dst, contiguous, static_cast<std::size_t>(len) * esz);
+    return len;
+  }
+  DevArray<std::int64_t> wide(static_cast<std::size_t>(len), "index export");
+  rt::check_launch(spmvtk_k_widen_index(static_cast<const std::int32_t*>(contiguous), wide.get(),
+                                        len, index_base, st),
+                   "index export");
+  if (index_width == 8) {
+    rt::copy_to_host(dst, wide.get(), static_cast<std::size_t>(len) * 8);
+  } else {
+    DevArray<std::int32_t> narrow(static_cast<std::size_t>(len), "index export");
+    rt::check_launch(spmvtk_k_narrow_index(wide.get(), narrow.get(), len, 0, st), "index export");
+    rt::copy_to_host(dst, narrow.get(), static_cast<std::size_t>(len) * 4);
+  }
+  return len;
+}
+
+}  // namespace spmvtk::dev

@@ -1,0 +1,73 @@
+// matrix.hpp -- the device-resident matrix handle behind spmvtk_matrix*.
+//
+// One handle type for every format (the reference keeps a
+// variant<Crs,Ccs,Coo,Ell> of host vectors, capi.cpp:23-25).  Arrays live in
+// HBM in the GPU layout: fp64 values, int32 0-based indices, ELL band-major
+// with a 32-aligned leading dimension.  Handles are immutable after
+// construction except for the cached row moments (guarded by a mutex), so
+// concurrent reads from several threads are safe, as in the reference
+// (SPEC.md:100-101).
+#pragma once
+
+#include <cstdint>
+#include <mutex>
+#include <optional>
+
+#include "runtime.hpp"
+#include "spmvtk/spmvtk.h"
+
+struct spmvtk_matrix {
+  spmvtk_format format = SPMVTK_FORMAT_CRS;
+  int ordering = -1;  // COO: 0 row-major, 1 column-major
+  int device = 0;
+  std::int64_t n = 0;
+  std::int64_t nnz = 0;  // stored entries; ELL: stored_nnz (real entries)
+
+  spmvtk::rt::DevArray<double> val;
+  spmvtk::rt::DevArray<std::int32_t> ptr;    // CRS row_ptr / CCS col_ptr
+  spmvtk::rt::DevArray<std::int32_t> row;    // COO / CCS row indices
+  spmvtk::rt::DevArray<std::int32_t> col;    // CRS / COO / ELL column indices
+  spmvtk::rt::DevArray<std::int32_t> count;  // ELL row_entry_count
+  std::int32_t band_count = 0;               // ELL
+  std::int64_t ld = 0;                       // ELL band-major leading dim
+
+  mutable std::mutex mu;
+  mutable std::optional<spmvtk::rt::Moments> moments;  // CRS row moments
+
+  std::uint64_t device_bytes() const {
+    return val.bytes() + ptr.bytes() + row.bytes() + col.bytes() + count.bytes();
+  }
+};
+
+namespace spmvtk::dev {
+
+using Matrix = spmvtk_matrix;
+
+// Exact row moments of a CRS handle (cached after the first GPU reduction).
+rt::Moments crs_moments(const Matrix& m);
+
+// CRS from caller arrays; see spmvtk_matrix_from_crs.
+Matrix* crs_from_arrays(std::int64_t n, std::int64_t nnz, const void* row_ptr,
+                        const void* col_idx, const double* values, int index_width,
+                        int index_base, bool on_device);
+
+// Reference ELL estimate (8+8 bytes per slot, convert.cpp:72-79).
+std::uint64_t reference_ell_estimate(const Matrix& crs);
+std::uint64_t device_bytes_for(const Matrix& crs, spmvtk_format to);
+
+// Conversions of a CRS handle (the guard applies to the ELL formats).
+Matrix* convert(const Matrix& crs, spmvtk_format to, std::uint64_t max_bytes);
+
+// y = A x on device vectors, async on the current stream.  Throws
+// InvalidArgument when the kernel does not match the handle's format (or
+// COO ordering), with the reference's messages (capi.cpp:230-252).
+void spmv_device(const Matrix& m, spmvtk_kernel kernel, const double* x, double* y);
+
+// One array to host memory in the requested index width / base.
+std::int64_t copy_array(const Matrix& m, spmvtk_array which, void* dst, std::int64_t capacity,
+                        int index_width, int index_base);
+std::int64_t device_array(const Matrix& m, spmvtk_array which, void** ptr);
+
+const char* kernel_label(spmvtk_kernel k);
+
+}  // namespace spmvtk::dev

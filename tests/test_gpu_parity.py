@@ -1,0 +1,431 @@
+"""Parity of the CUDA path with the oracle, through the C ABI (GPU).
+
+Transforms must be bit-exact against the reference (values memcmp, every
+index equal after widening to the reference's 1-based int64); SpMV within
+1e-12 max-norm relative of the reference (test_support.hpp:96-105; the
+tolerance of BASELINE.json north_star), and within 1e-10 of a dense mat-vec.
+"""
+import os
+import tempfile
+
+import numpy as np
+import pytest
+
+from oracle.oracle import dense_matvec, max_rel_error, random_crs
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-12
+
+
+def upload(sp, n, rp, ci, v):
+    return sp.Matrix.from_crs(n, np.asarray(rp, np.int64), np.asarray(ci, np.int64),
+                              np.asarray(v, np.float64), index_base=1)
+
+
+def ref_layout(m, sp, which):
+    return m.array(which, index_width=8, index_base=1)
+
+
+# ---------------------------------------------------------------- KATs
+def test_kat_transforms(gpu, kat):
+    sp = gpu
+    for c in kat["coo_row"]:
+        m = upload(sp, c["n"], c["row_ptr"], c["col_idx"], c["values"])
+        coo = m.convert(sp.Format.COO_ROW)
+        assert coo.format == sp.Format.COO_ROW
+        assert ref_layout(coo, sp, sp.Array.ROW_IDX).tolist() == c["row_idx"], c["ref"]
+        assert ref_layout(coo, sp, sp.Array.COL_IDX).tolist() == c["out_col_idx"]
+        assert coo.array(sp.Array.VALUES).tolist() == c["out_values"]
+    for c in kat["ccs"]:
+        m = upload(sp, c["n"], c["row_ptr"], c["col_idx"], c["values"])
+        ccs = m.convert(sp.Format.CCS)
+        assert ref_layout(ccs, sp, sp.Array.POINTER).tolist() == c["col_ptr"], c["ref"]
+        assert ref_layout(ccs, sp, sp.Array.ROW_IDX).tolist() == c["row_idx"]
+        assert ccs.array(sp.Array.VALUES).tolist() == c["out_values"]
+    for c in kat["coo_col"]:
+        m = upload(sp, c["n"], c["row_ptr"], c["col_idx"], c["values"])
+        coo = m.convert(sp.Format.COO_COL)
+        assert coo.format == sp.Format.COO_COL
+        assert ref_layout(coo, sp, sp.Array.COL_IDX).tolist() == c["out_col_idx"], c["ref"]
+        assert ref_layout(coo, sp, sp.Array.ROW_IDX).tolist() == c["row_idx"]
+        assert coo.array(sp.Array.VALUES).tolist() == c["out_values"]
+    for c in kat["ell"]:
+        m = upload(sp, c["n"], c["row_ptr"], c["col_idx"], c["values"])
+        ell = m.convert(sp.Format.ELL)
+        d = ell.describe()
+        assert d.band_count == c["band_count"] and d.nnz == c["stored_nnz"], c["ref"]
+        # counts are not indices: exported as-is whatever the index base
+        assert ref_layout(ell, sp, sp.Array.ROW_ENTRY_COUNT).tolist() == c["row_entry_count"]
+        assert ell.array(sp.Array.ROW_ENTRY_COUNT, 4, 0).tolist() == c["row_entry_count"]
+        if "out_values" in c:
+            assert ell.array(sp.Array.VALUES).tolist() == c["out_values"]
+            assert ref_layout(ell, sp, sp.Array.COL_IDX).tolist() == c["out_col_idx"]
+
+
+def test_kat_guard_and_estimates(gpu, kat):
+    sp = gpu
+    g = kat["ell_guard"]
+    n = g["n"]
+    rp = np.full(n + 1, g["heavy_row_entries"] + 1, np.int64)
+    rp[0] = 1
+    ci = np.arange(1, g["heavy_row_entries"] + 1)
+    m = upload(sp, n, rp, ci, np.ones(ci.shape[0]))
+    for fmt in (sp.Format.ELL, sp.Format.ELL_ROWMAJOR):
+        with pytest.raises(sp.SpmvtkError) as e:
+            m.convert(fmt, max_bytes=g["max_bytes"])
+        assert e.value.status == g["status"]
+        assert g["message_contains"] in e.value.message
+    assert m.info().ell_bytes == n * g["heavy_row_entries"] * 16
+    # unlimited: the conversion goes through on the GPU
+    ell = m.convert(sp.Format.ELL)
+    assert ell.describe().band_count == g["heavy_row_entries"]
+    c = kat["capi_guard"]
+    heavy = sp.Matrix.gen_skewed(*c["gen_skewed"])
+    with pytest.raises(sp.SpmvtkError) as e:
+        heavy.convert(sp.Format.ELL, c["max_bytes"])
+    assert e.value.status == sp.Status.ERR_MEMORY_LIMIT
+
+
+def test_kat_spmv(gpu, kat):
+    sp = gpu
+    for c in kat["spmv_crs"]:
+        m = upload(sp, c["n"], c["row_ptr"], c["col_idx"], c["values"])
+        y, _ = m.spmv(c["x"], sp.Kernel.CRS)
+        assert y.tolist() == c["y"], c["ref"]
+    c = kat["spmv_dim_mismatch"]
+    m = upload(sp, 2, [1, 1, 1], [], [])
+    with pytest.raises(sp.SpmvtkError) as e:
+        m.spmv(np.ones(c["x_len"]), sp.Kernel.CRS)
+    assert e.value.status == c["status"]
+    c = kat["ell_padding_spmv"]
+    m = upload(sp, c["n"], c["row_ptr"], c["col_idx"], c["values"])
+    for k, f in ((sp.Kernel.ELL_INNER, sp.Format.ELL), (sp.Kernel.ELL_OUTER, sp.Format.ELL),
+                 (sp.Kernel.ELL_ROWMAJOR, sp.Format.ELL_ROWMAJOR)):
+        y, _ = m.convert(f).spmv(c["x"], k)
+        assert y.tolist() == c["y"]
+    c = kat["ell_outer_idle_lanes"]
+    n = c["n"]
+    ident = upload(sp, n, np.arange(1, n + 2), np.arange(1, n + 1), np.ones(n))
+    y, _ = ident.convert(sp.Format.ELL).spmv(c["x"], sp.Kernel.ELL_OUTER, lanes=c["lanes"])
+    assert y.tolist() == c["y"]
+
+
+def test_kat_ordering_contract(gpu, kat):
+    sp = gpu
+    c = kat["coo_ordering"]
+    n = c["n"]
+    ident = upload(sp, n, np.arange(1, n + 2), np.arange(1, n + 1), np.ones(n))
+    coo_r = ident.convert(sp.Format.COO_ROW)
+    with pytest.raises(sp.SpmvtkError) as e:
+        coo_r.spmv(c["x"], sp.Kernel.COO_COL_OUTER, lanes=2)
+    assert e.value.status == c["wrong_kernel_status"]
+    assert "ordering" in e.value.message
+    y, _ = coo_r.spmv(c["x"], sp.Kernel.COO_ROW_OUTER, lanes=2)
+    assert y.tolist() == c["x"]
+    with pytest.raises(sp.SpmvtkError) as e:
+        coo_r.spmv(c["x"], sp.Kernel.ELL_INNER)
+    assert e.value.status == sp.Status.ERR_USAGE
+    with pytest.raises(sp.SpmvtkError) as e:
+        coo_r.spmv(c["x"], sp.Kernel.COO_ROW_OUTER, lanes=0)
+    assert e.value.status == sp.Status.ERR_USAGE
+
+
+def test_kat_stats(gpu, kat):
+    sp = gpu
+    for c in kat["stats"]:
+        counts = np.array(c["counts"], np.int64)
+        n = len(counts)
+        rp = np.concatenate([[1], 1 + np.cumsum(counts)])
+        ci = np.concatenate([np.arange(1, k + 1) for k in counts])
+        m = upload(sp, n, rp, ci, np.ones(ci.shape[0]))
+        s = m.row_stats()
+        if c.get("exact"):
+            assert s.d_mat == c["d_mat"], c["ref"]
+            if "mu" in c:
+                assert s.mu == c["mu"] and s.sigma == c["sigma"]
+        elif "d_mat" in c:
+            assert s.mu == c["mu"] and s.sigma == c["sigma"] and s.d_mat == c["d_mat"]
+        if c.get("d_mat_positive"):
+            assert s.d_mat > 0
+    c = kat["stats_empty"]
+    m = upload(sp, c["n"], c["row_ptr"], [], [])
+    with pytest.raises(sp.SpmvtkError) as e:
+        m.info()
+    assert e.value.status == c["status"]
+
+
+# ---------------------------------------------------- reference fixtures
+def _case(g, i):
+    p = f"m{i}_"
+    return int(g[p + "n"][0]), g[p + "row_ptr"], g[p + "col_idx"], g[p + "values"], g[p + "x"], p
+
+
+def test_transforms_bit_exact_vs_reference(gpu, golden):
+    sp = gpu
+    for i in range(int(golden["count"][0])):
+        n, rp, ci, v, x, p = _case(golden, i)
+        m = upload(sp, n, rp, ci, v)
+        ccs = m.convert(sp.Format.CCS)
+        np.testing.assert_array_equal(ref_layout(ccs, sp, sp.Array.POINTER), golden[p + "ccs_col_ptr"])
+        np.testing.assert_array_equal(ref_layout(ccs, sp, sp.Array.ROW_IDX), golden[p + "ccs_row_idx"])
+        assert ccs.array(sp.Array.VALUES).tobytes() == golden[p + "ccs_values"].tobytes()
+        for name, fmt in (("coo_row", sp.Format.COO_ROW), ("coo_col", sp.Format.COO_COL)):
+            coo = m.convert(fmt)
+            np.testing.assert_array_equal(ref_layout(coo, sp, sp.Array.ROW_IDX),
+                                          golden[p + name + "_row_idx"])
+            np.testing.assert_array_equal(ref_layout(coo, sp, sp.Array.COL_IDX),
+                                          golden[p + name + "_col_idx"])
+            assert coo.array(sp.Array.VALUES).tobytes() == golden[p + name + "_values"].tobytes()
+        ell = m.convert(sp.Format.ELL)
+        bc = int(golden[p + "ell_band_count"][0])
+        assert ell.describe().band_count == bc
+        assert ell.array(sp.Array.VALUES).tobytes() == golden[p + "ell_values"].tobytes()
+        np.testing.assert_array_equal(ref_layout(ell, sp, sp.Array.COL_IDX), golden[p + "ell_col_idx"])
+        np.testing.assert_array_equal(ell.array(sp.Array.ROW_ENTRY_COUNT, 8, 0),
+                                      golden[p + "ell_row_entry_count"])
+        # row-major ELL = transpose of the reference's band-major arrays
+        rm = m.convert(sp.Format.ELL_ROWMAJOR)
+        want_v = golden[p + "ell_values"].reshape(bc, n).T.reshape(-1) if bc else np.zeros(0)
+        want_c = golden[p + "ell_col_idx"].reshape(bc, n).T.reshape(-1) if bc else np.zeros(0)
+        assert rm.array(sp.Array.VALUES).tobytes() == np.ascontiguousarray(want_v).tobytes()
+        np.testing.assert_array_equal(ref_layout(rm, sp, sp.Array.COL_IDX), want_c)
+
+
+def test_spmv_all_kernels_vs_reference(gpu, golden):
+    sp = gpu
+    for i in range(int(golden["count"][0])):
+        n, rp, ci, v, x, p = _case(golden, i)
+        m = upload(sp, n, rp, ci, v)
+        dense = dense_matvec(n, rp, ci, v, x)
+        want = golden[p + "y_k0_l1"]
+        y, t = m.spmv(x, sp.Kernel.CRS)
+        assert max_rel_error(y, want) <= TOL and max_rel_error(y, dense) <= 1e-10
+        for k, fmt in ((sp.Kernel.COO_ROW_OUTER, sp.Format.COO_ROW),
+                       (sp.Kernel.COO_COL_OUTER, sp.Format.COO_COL),
+                       (sp.Kernel.ELL_INNER, sp.Format.ELL),
+                       (sp.Kernel.ELL_OUTER, sp.Format.ELL),
+                       (sp.Kernel.ELL_ROWMAJOR, sp.Format.ELL_ROWMAJOR)):
+            conv = m.convert(fmt)
+            for lanes in (1, 3):
+                y, _ = conv.spmv(x, k, lanes=lanes)
+                ref_y = golden[p + f"y_k{min(int(k), 4) if k != sp.Kernel.ELL_ROWMAJOR else 3}_l{lanes}"]
+                assert max_rel_error(y, ref_y) <= TOL, (i, k)
+                assert max_rel_error(y, dense) <= 1e-10
+
+
+def test_spmv_deterministic_where_reference_is(gpu):
+    """Repeated calls are bitwise identical for every kernel except the
+    column-ordered COO, whose fp64 reductions may add in any order (it stays
+    within the 1e-12 contract; spmv.cpp:105-109 is lane-dependent too)."""
+    sp = gpu
+    rng = np.random.default_rng(37)
+    for _ in range(5):
+        n, rp, ci, v = random_crs(rng, 500, 20000)
+        x = rng.uniform(-1, 1, n)
+        m = upload(sp, n, rp, ci, v)
+        for k, fmt in ((sp.Kernel.CRS, sp.Format.CRS), (sp.Kernel.COO_ROW_OUTER, sp.Format.COO_ROW),
+                       (sp.Kernel.ELL_INNER, sp.Format.ELL), (sp.Kernel.ELL_OUTER, sp.Format.ELL),
+                       (sp.Kernel.ELL_ROWMAJOR, sp.Format.ELL_ROWMAJOR)):
+            h = m if fmt == sp.Format.CRS else m.convert(fmt)
+            a, _ = h.spmv(x, k)
+            b, _ = h.spmv(x, k)
+            assert a.tobytes() == b.tobytes()
+
+
+def test_padding_neutrality(gpu):
+    """ELL padding slots (+0.0, own row) change nothing (test_spmv.cpp:172-190):
+    a matrix with one long row forces padding in every other row."""
+    sp = gpu
+    rng = np.random.default_rng(41)
+    n, rp, ci, v = random_crs(rng, 300, 3000)
+    x = rng.uniform(-1, 1, n)
+    m = upload(sp, n, rp, ci, v)
+    want, _ = m.spmv(x, sp.Kernel.CRS)
+    y, _ = m.convert(sp.Format.ELL).spmv(x, sp.Kernel.ELL_INNER)
+    assert max_rel_error(y, want) <= TOL
+
+
+def test_generators_byte_identical_to_reference(gpu, golden):
+    sp = gpu
+    gens = {
+        "banded_200_1": lambda: sp.Matrix.gen_banded(200, 1),
+        "banded_300_4": lambda: sp.Matrix.gen_banded(300, 4),
+        "skewed_500_2_10_250_99": lambda: sp.Matrix.gen_skewed(500, 2, 10, 250, 99),
+        "skewed_10000_1_1_5000_0": lambda: sp.Matrix.gen_skewed(10000, 1, 1, 5000, 0),
+        "cv_2000_8_1.5_7": lambda: sp.Matrix.gen_cv_target(2000, 8.0, 1.5, 7),
+        "cv_1000_5_0_3": lambda: sp.Matrix.gen_cv_target(1000, 5.0, 0.0, 3),
+    }
+    for key, make in gens.items():
+        m = make()
+        np.testing.assert_array_equal(ref_layout(m, sp, sp.Array.POINTER),
+                                      golden[f"gen_{key}_row_ptr"])
+        np.testing.assert_array_equal(ref_layout(m, sp, sp.Array.COL_IDX),
+                                      golden[f"gen_{key}_col_idx"])
+        assert m.array(sp.Array.VALUES).tobytes() == golden[f"gen_{key}_values"].tobytes()
+    with pytest.raises(sp.SpmvtkError) as e:
+        sp.Matrix.gen_banded(5, 5)
+    assert e.value.status == sp.Status.ERR_USAGE
+    with pytest.raises(sp.SpmvtkError) as e:
+        sp.Matrix.gen_cv_target(100, 90.0, 3.0, 1)
+    assert "feasible" in e.value.message
+
+
+def test_larger_random_parity_with_port(gpu, port):
+    """Bigger than the fixtures (long rows, many empty rows, unsorted columns)
+    against the C port, bit-exact transforms + 1e-12 SpMV."""
+    sp = gpu
+    rng = np.random.default_rng(7)
+    for it in range(4):
+        n = int(rng.integers(2000, 6000))
+        lens = rng.integers(0, 40, size=n)
+        lens[rng.integers(0, n, size=3)] = rng.integers(3000, 6000, size=3)  # long rows
+        lens[rng.random(n) < 0.2] = 0  # empty rows
+        rows = [np.sort(rng.choice(n, size=min(int(l), n), replace=False)) for l in lens]
+        for r in rows:
+            rng.shuffle(r)
+        ci = np.concatenate(rows).astype(np.int64) + 1
+        rp = np.concatenate([[1], 1 + np.cumsum([len(r) for r in rows])]).astype(np.int64)
+        v = rng.standard_normal(ci.shape[0])
+        x = rng.uniform(-1, 1, n)
+        m = upload(sp, n, rp, ci, v)
+        cp, ri, cv = port.crs_to_ccs(n, rp, ci, v)
+        ccs = m.convert(sp.Format.CCS)
+        np.testing.assert_array_equal(ref_layout(ccs, sp, sp.Array.POINTER), cp)
+        np.testing.assert_array_equal(ref_layout(ccs, sp, sp.Array.ROW_IDX), ri)
+        assert ccs.array(sp.Array.VALUES).tobytes() == cv.tobytes()
+        bc, ev, ec, cnt = port.crs_to_ell(n, rp, ci, v)
+        ell = m.convert(sp.Format.ELL)
+        assert ell.array(sp.Array.VALUES).tobytes() == ev.tobytes()
+        np.testing.assert_array_equal(ref_layout(ell, sp, sp.Array.COL_IDX), ec)
+        want = port.spmv_crs(n, rp, ci, v, x)
+        for k, f in ((sp.Kernel.CRS, None), (sp.Kernel.COO_ROW_OUTER, sp.Format.COO_ROW),
+                     (sp.Kernel.COO_COL_OUTER, sp.Format.COO_COL), (sp.Kernel.ELL_INNER, sp.Format.ELL),
+                     (sp.Kernel.ELL_OUTER, sp.Format.ELL),
+                     (sp.Kernel.ELL_ROWMAJOR, sp.Format.ELL_ROWMAJOR)):
+            h = m if f is None else m.convert(f)
+            y, _ = h.spmv(x, k)
+            assert max_rel_error(y, want) <= TOL, (it, k)
+
+
+def test_crs_long_rows_path(gpu, port):
+    """Rows above the vector kernel's 4096 limit take the block-per-row pass."""
+    sp = gpu
+    rng = np.random.default_rng(11)
+    n = 20000
+    lens = rng.integers(0, 8, size=n)
+    lens[[5, 77, 19999]] = [20000, 9000, 4097]
+    rows = [np.sort(rng.choice(n, size=int(l), replace=False)) for l in lens]
+    ci = np.concatenate(rows).astype(np.int64) + 1
+    rp = np.concatenate([[1], 1 + np.cumsum(lens)]).astype(np.int64)
+    v = rng.standard_normal(ci.shape[0])
+    x = rng.uniform(-1, 1, n)
+    m = upload(sp, n, rp, ci, v)
+    y, _ = m.spmv(x, sp.Kernel.CRS)
+    assert max_rel_error(y, port.spmv_crs(n, rp, ci, v, x)) <= TOL
+
+
+# -------------------------------------------- the reference's C API scenario
+def test_capi_end_to_end(gpu, kat):
+    """Mirror of test_capi.cpp:29-141 through our C ABI."""
+    sp = gpu
+    c = kat["capi_banded"]
+    banded = sp.Matrix.gen_banded(c["n"], c["half_width"])
+    info = banded.info()
+    assert info.n == c["n"] and info.nnz == c["nnz"] and info.max_row_entries == c["max_row_entries"]
+    assert info.d_mat > 0
+    with tempfile.TemporaryDirectory() as d:
+        path = os.path.join(d, "banded.mtx")
+        banded.write_matrix_market(path)
+        back = sp.Matrix.read_matrix_market(path)
+        info2 = back.info()
+        assert info2.nnz == info.nnz and info2.d_mat == info.d_mat
+        x = np.ones(c["n"])
+        y0, _ = banded.spmv(x, sp.Kernel.CRS)
+        for fmt, k in ((sp.Format.COO_ROW, sp.Kernel.COO_ROW_OUTER),
+                       (sp.Format.COO_COL, sp.Kernel.COO_COL_OUTER),
+                       (sp.Format.ELL, sp.Kernel.ELL_INNER), (sp.Format.ELL, sp.Kernel.ELL_OUTER)):
+            conv = banded.convert(fmt)
+            assert conv.format == fmt
+            y, _ = conv.spmv(x, k, lanes=3)
+            assert np.all(np.abs(y - y0) <= 1e-12 * np.abs(y0))
+            # non-CRS handles are written through their CRS reconstruction
+            p2 = os.path.join(d, f"conv{int(fmt)}.mtx")
+            conv.write_matrix_market(p2)
+            assert open(p2).read() == open(path).read()
+        b = sp.bench(banded, sp.Kernel.ELL_OUTER, 1, 3, 0)
+        assert b["t_crs"] > 0 and b["sp"] > 0 and b["t_trans"] > 0
+        assert b["r"] == pytest.approx(b["sp"] / b["tt"])
+        second = sp.Matrix.gen_banded(200, 2)
+        prof = sp.Profile.build([banded, second], ["a", "b"], sp.Kernel.ELL_INNER, 1, 1.0, 3, 0,
+                                "capi-test")
+        recs = prof.records()
+        assert len(recs) == 2 and recs[0]["matrix_id"] == "a"
+        assert not recs[0]["excluded"] and recs[0]["r"] > 0
+        ppath = os.path.join(d, "profile.json")
+        prof.write(ppath)
+        back_p = sp.Profile.read(ppath)
+        assert back_p.d_star == prof.d_star and back_p.kernel == sp.Kernel.ELL_INNER
+        dec, dm = sp.select(banded, back_p)
+        assert dm > 0
+        bad = os.path.join(d, "bad.json")
+        open(bad, "w").write('{"version": 1, "oops": true}')
+        with pytest.raises(sp.SpmvtkError) as e:
+            sp.Profile.read(bad)
+        assert e.value.status == sp.Status.ERR_DATA
+    assert sp.last_error() != ""
+
+
+def test_online_select_strict(gpu, kat, ref):
+    sp = gpu
+    c = kat["online_select"]
+    banded = sp.Matrix.gen_banded(*c["banded"])
+    skew = sp.Matrix.gen_skewed(*c["skewed"])
+    # profile with d_star = 0.1 through the JSON reader (schema v1)
+    with tempfile.TemporaryDirectory() as d:
+        path = os.path.join(d, "p.json")
+        open(path, "w").write('{"version": 1, "machine_label": "x", "kernel_variant": '
+                              '"ell-inner", "lanes": 1, "c": 1.0, "d_star": 0.1, "records": []}')
+        p = sp.Profile.read(path)
+        dec, dm = sp.select(banded, p)
+        assert dec == sp.Decision.USE_ELL
+        dec2, dm2 = sp.select(skew, p)
+        assert dm2 > 0.1 and dec2 == sp.Decision.USE_CRS
+        open(path, "w").write('{"version": 1, "machine_label": "x", "kernel_variant": '
+                              '"ell-inner", "lanes": 1, "c": 1.0, "d_star": %r, "records": []}' % dm)
+        p2 = sp.Profile.read(path)
+        assert sp.select(banded, p2)[0] == sp.Decision.USE_CRS  # strict
+    # GPU D_mat vs the reference Welford value
+    hb = ref.gen("banded", *c["banded"])
+    assert dm == pytest.approx(ref.row_stats(hb)[2], rel=1e-12)
+    ref.free(hb)
+
+
+def test_profile_excludes_guarded_matrix(gpu):
+    sp = gpu
+    ok = sp.Matrix.gen_banded(300, 1)
+    n = 10000
+    rp = np.full(n + 1, 5001, np.int64)
+    rp[0] = 1
+    wide = upload(sp, n, rp, np.arange(1, 5001), np.ones(5000))
+    p = sp.Profile.build([ok, wide], ["ok", "overflow"], sp.Kernel.ELL_OUTER, 1, 1.0, 3,
+                         100 << 20)
+    recs = p.records()
+    assert not recs[0]["excluded"] and recs[1]["excluded"]
+    assert "exceeds" in recs[1]["exclusion_reason"]
+    assert np.isnan(recs[1]["r"])
+    with pytest.raises(sp.SpmvtkError) as e:
+        sp.Profile.build([ok], ["ok"], sp.Kernel.CRS)
+    assert e.value.status == sp.Status.ERR_USAGE
+
+
+def test_validation_rejects_bad_arrays(gpu):
+    sp = gpu
+    with pytest.raises(sp.SpmvtkError) as e:
+        sp.Matrix.from_crs(2, np.array([0, 2, 1]), np.array([0, 1]), np.ones(2))
+    assert e.value.status == sp.Status.ERR_DATA
+    with pytest.raises(sp.SpmvtkError):
+        sp.Matrix.from_crs(2, np.array([0, 1, 2]), np.array([0, 5]), np.ones(2))
+    with pytest.raises(sp.SpmvtkError) as e:
+        sp.Matrix.from_crs(2, np.array([1, 1, 2]), np.array([0]), np.ones(1), index_base=0)
+    assert e.value.status == sp.Status.ERR_DATA

@@ -1,0 +1,121 @@
+"""The native library builds, loads and exports the whole C ABI (CPU only:
+no compute calls that need a device)."""
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+INC = os.path.join(ROOT, "include", "spmvtk")
+
+
+def declared_functions(header: str) -> set[str]:
+    text = open(os.path.join(INC, header)).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return set(re.findall(r"\b(spmvtk_[a-z0-9_]+)\s*\(", text))
+
+
+def exported_symbols(lib: str) -> set[str]:
+    out = subprocess.run(["nm", "-D", "--defined-only", lib], capture_output=True, text=True,
+                         check=True).stdout
+    return {line.split()[-1] for line in out.splitlines() if " T " in line}
+
+
+def test_library_exports_every_declared_symbol(sp):
+    syms = exported_symbols(sp.LIB_PATH)
+    for header in ("spmvtk.h", "spmvtk_kernels.h"):
+        missing = declared_functions(header) - syms
+        assert not missing, f"{header}: not exported: {sorted(missing)}"
+    # nothing but the C ABI leaks out of the shared object
+    assert all(s.startswith("spmvtk_") for s in syms), sorted(s for s in syms
+                                                               if not s.startswith("spmvtk_"))
+
+
+def test_reference_abi_is_complete(sp):
+    """All 23 entry points of the reference spmvtk.h:50-160 are present."""
+    ref23 = {
+        "spmvtk_last_error", "spmvtk_matrix_free", "spmvtk_profile_free",
+        "spmvtk_read_matrix_market", "spmvtk_write_matrix_market", "spmvtk_gen_banded",
+        "spmvtk_gen_skewed", "spmvtk_gen_cv_target", "spmvtk_matrix_get_format",
+        "spmvtk_matrix_get_info", "spmvtk_matrix_convert", "spmvtk_spmv", "spmvtk_bench",
+        "spmvtk_profile_build", "spmvtk_profile_write", "spmvtk_profile_read",
+        "spmvtk_profile_d_star", "spmvtk_profile_c", "spmvtk_profile_lanes",
+        "spmvtk_profile_kernel", "spmvtk_profile_record_count", "spmvtk_profile_record",
+        "spmvtk_select",
+    }
+    assert ref23 <= exported_symbols(sp.LIB_PATH)
+    assert ref23 <= set(sp.SIGNATURES)
+
+
+def test_sm100a_code_present(sp):
+    out = subprocess.run(["cuobjdump", "--list-elf", sp.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_enum_values_match_reference(sp):
+    # spmvtk.h:17-47 of the reference
+    assert [s.value for s in sp.Status] == [0, 1, 2, 3, 4]
+    assert [sp.Format.CRS, sp.Format.CCS, sp.Format.COO_ROW, sp.Format.COO_COL,
+            sp.Format.ELL] == [0, 1, 2, 3, 4]
+    assert [sp.Kernel.CRS, sp.Kernel.COO_ROW_OUTER, sp.Kernel.COO_COL_OUTER,
+            sp.Kernel.ELL_INNER, sp.Kernel.ELL_OUTER] == [0, 1, 2, 3, 4]
+    assert [sp.Decision.USE_ELL, sp.Decision.USE_CRS] == [0, 1]
+
+
+def test_host_side_autotune_arithmetic(sp, kat):
+    """Cost model / amortization / D* run on the host: checked against the KATs."""
+    for c in kat["compute_metrics"]:
+        if c.get("error"):
+            with pytest.raises(sp.SpmvtkError) as e:
+                sp.compute_metrics(*c["t"])
+            assert e.value.status == sp.Status.ERR_USAGE
+        else:
+            assert sp.compute_metrics(*c["t"]) == (c["sp"], c["tt"], c["r"]), c["ref"]
+    for c in kat["amortization"]:
+        assert sp.amortization_iterations(*c["t"]) == c["k"], c["ref"]
+    for c in kat["find_d_star"]:
+        assert sp.find_d_star([tuple(r) for r in c["records"]], c["c"]) == c["d_star"]
+
+
+def test_amortization_matches_linear_scan(sp, port):
+    rng = np.random.default_rng(67)
+    for _ in range(200):
+        t = (0.5 + rng.integers(0, 100) / 50.0, 0.1 + rng.integers(0, 100) / 50.0,
+             0.1 + rng.integers(0, 100) / 10.0)
+        assert sp.amortization_iterations(*t) == port.amortization(*t)
+
+
+def test_metric_identity(sp):
+    rng = np.random.default_rng(61)
+    for _ in range(200):
+        t = 1e-6 + rng.random(3)
+        s, tt, r = sp.compute_metrics(*t)
+        assert abs(r * t[1] * t[2] - t[0] ** 2) <= 1e-12 * t[0] ** 2
+
+
+def test_vector_generator_convention(sp):
+    """x ~ U(-1,1) with 2*((r>>11)*2^-53)-1 over mt19937_64 raw outputs
+    (test_support.hpp:76-81): deterministic per seed, in range."""
+    a = sp.gen_vector(1000, 5)
+    b = sp.gen_vector(1000, 5)
+    assert a.tobytes() == b.tobytes()
+    assert a.min() >= -1.0 and a.max() < 1.0
+    assert abs(a.mean()) < 0.1
+    # mt19937_64 seeded with 5489 (the default seed) first output is
+    # 14514284786278117030; (r >> 11) * 2^-53 * 2 - 1:
+    first = ((14514284786278117030 >> 11) * 2.0 ** -53) * 2.0 - 1.0
+    assert sp.gen_vector(1, 5489)[0] == first
+
+
+def test_no_silent_cpu_fallback_without_gpu(sp):
+    """Without a device every compute entry point fails loudly."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("device present")
+    with pytest.raises(sp.SpmvtkError) as e:
+        sp.Matrix.gen_banded(10, 1)
+    assert e.value.status in (sp.Status.ERR_DATA, sp.Status.ERR_MEMORY_LIMIT)
+    assert "CUDA" in e.value.message or "device" in e.value.message
