@@ -38,6 +38,21 @@ PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback
 
 
+def ncu_traffic(config: int, kernel: str):
+    """DRAM read+write bytes per launch of `kernel` on this config, from the
+    committed ncu launch list (profiles/traffic_*.json), or None."""
+    import glob
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "traffic_r*.json")), reverse=True):
+        try:
+            with open(path) as f:
+                v = json.load(f).get(f"config{config}", {}).get(kernel)
+            if v:
+                return float(v)
+        except Exception:
+            continue
+    return None
+
+
 def hbm_peak():
     try:
         with open(PEAKS_FILE) as f:
@@ -239,7 +254,12 @@ def impl_ours(args):
     st = m.row_stats()
     nz = st.max_row
 
-    # ---- transforms: one cold conversion each (wall clock, synchronised)
+    # ---- transforms.  t_trans = one conversion through the public API as the
+    # reference times it (wall clock around the call, allocation -- from the
+    # stream-ordered pool, grown once up front -- and the band-count
+    # reduction's host round trip included); kernel = median device time of
+    # the transform's kernels alone with outputs preallocated.
+    sp.reserve_device_memory(8 << 30)
     handles = {"crs": m}
     transforms = {}
     for name, fmt in (("coo-row", sp.Format.COO_ROW), ("ccs", sp.Format.CCS),
@@ -249,17 +269,11 @@ def impl_ours(args):
         t0 = time.perf_counter()
         h = m.convert(fmt)
         torch.cuda.synchronize()
-        cold = time.perf_counter() - t0
-        # warm repeat (pool already holds the memory) for the device-side cost
-        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ev0.record()
-        h2 = m.convert(fmt)
-        ev1.record()
-        torch.cuda.synchronize()
-        warm = ev0.elapsed_time(ev1) * 1e-3
-        h2.free()
-        transforms[name] = {"cold_ms": cold * 1e3, "warm_ms": warm * 1e3,
-                            "gbs_warm": transform_bytes(name, n, nnz, nz) / warm / 1e9}
+        t_trans = time.perf_counter() - t0
+        k = m.transform_kernel_seconds(fmt, 5)
+        transforms[name] = {"t_trans_ms": t_trans * 1e3, "kernel_ms": k * 1e3,
+                            "gbs_kernel": transform_bytes(name, n, nnz, nz) / k / 1e9,
+                            "bytes": transform_bytes(name, n, nnz, nz)}
         handles[name] = h
 
     x = torch.from_numpy(sp.gen_vector(n, args.seed + 1)).cuda()
@@ -297,11 +311,11 @@ def impl_ours(args):
                        "bytes": b, "frac": b / t / 1e9 / peak}
     t_crs = table["crs"]["ms"] * 1e-3
     for name, tr in transforms.items():
-        tr["tt_cold"] = tr["cold_ms"] * 1e-3 / t_crs
-        tr["tt_warm"] = tr["warm_ms"] * 1e-3 / t_crs
+        tr["tt"] = tr["t_trans_ms"] * 1e-3 / t_crs       # in CRS-SpMV units
+        tr["tt_kernel"] = tr["kernel_ms"] * 1e-3 / t_crs
     # AT model on GPU timings, ELL-inner variant (Eq. 1-3 as implemented)
     t_ell = table["ell-inner"]["ms"] * 1e-3
-    t_trans = transforms["ell"]["cold_ms"] * 1e-3
+    t_trans = transforms["ell"]["t_trans_ms"] * 1e-3
     sp_, tt_, r_ = sp.compute_metrics(t_crs, t_ell, t_trans)
 
     best = max(table, key=lambda k: table[k]["gbs"])
@@ -360,7 +374,8 @@ def impl_ours(args):
                    "gflops": 2 * nnz / t_step / 1e9,
                    "l2": "inputs larger than L2 (no flush)"},
         "roofline": {"bound": "hbm", "achieved": value, "peak": peak, "unit": "GB/s",
-                     "frac": value / peak, "traffic": None, "peak_kind": peak_kind,
+                     "frac": value / peak, "traffic": ncu_traffic(args.config, best),
+                     "peak_kind": peak_kind,
                      "kernel": best, "bytes_per_launch": bytes_step},
         "e2e": {"value": bytes_step / t_e2e / 1e9, "unit": "GB/s", "h2d_bytes_per_step": 8 * n,
                 "d2h_bytes_per_step": 8 * n, "ms_per_step": t_e2e * 1e3,

@@ -255,6 +255,16 @@ spmvtk_status spmvtk_gen_vector(int64_t n, uint64_t seed, double* out);
 spmvtk_status spmvtk_conversion_bytes(const spmvtk_matrix* m, spmvtk_format to,
                                       uint64_t* reference_estimate, uint64_t* device_bytes);
 
+/* Median device time (seconds) of the kernels of one CRS -> `to` conversion
+ * with outputs preallocated (allocation and host synchronisation excluded;
+ * spmvtk_bench's t_trans includes them, as the reference's does). */
+spmvtk_status spmvtk_transform_kernel_seconds(const spmvtk_matrix* m, spmvtk_format to,
+                                              int repeats, double* seconds);
+
+/* Grows the device memory pool by `bytes` once (allocate + free), so later
+ * stream-ordered allocations of handles are sub-allocations. */
+spmvtk_status spmvtk_reserve_device_memory(uint64_t bytes);
+
 /* Compute metrics / amortization / D* helpers (autotune.cpp:36-60, :130-158). */
 spmvtk_status spmvtk_compute_metrics(double t_crs, double t_ell, double t_trans,
                                      double* sp, double* tt, double* r);

@@ -114,6 +114,10 @@ int spmvtk_k_spmv_ell_rm(int64_t n, int32_t nz, const double* val,
                          const int32_t* col, const double* x, double* y,
                          void* stream);
 
+/* Tuning override for experiments ("crs_variant": -1 = heuristic, 0..9 pick
+ * a (lanes per row, rows per sub-warp) instance of the CRS kernel). */
+int spmvtk_k_tune(const char* key, int value);
+
 /* Forces every kernel of the library to be loaded (lazy module loading
  * would otherwise charge the first timed call). */
 int spmvtk_k_preload(void);

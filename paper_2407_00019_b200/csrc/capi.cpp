@@ -498,6 +498,24 @@ spmvtk_status spmvtk_conversion_bytes(const spmvtk_matrix* m, spmvtk_format to,
   });
 }
 
+spmvtk_status spmvtk_transform_kernel_seconds(const spmvtk_matrix* m, spmvtk_format to,
+                                              int repeats, double* seconds) {
+  return guarded([&] {
+    need(seconds);
+    const dev::Matrix& a = crs_of(m);
+    if (!valid_format(to)) throw Error(ErrorCode::InvalidArgument, "unknown target format");
+    *seconds = dev::transform_kernel_seconds(a, to, repeats);
+  });
+}
+
+spmvtk_status spmvtk_reserve_device_memory(uint64_t bytes) {
+  return guarded([&] {
+    rt::DevArray<unsigned char> block(static_cast<std::size_t>(bytes), "pool reservation");
+    block.release();
+    rt::sync();
+  });
+}
+
 spmvtk_status spmvtk_compute_metrics(double t_crs, double t_ell, double t_trans, double* sp,
                                      double* tt, double* r) {
   return guarded([&] {

@@ -306,6 +306,47 @@ __global__ void __launch_bounds__(256) k_crs_to_ell_cm(int64_t n, int32_t nz, in
   }
 }
 
+// Band-major, short bands (nz <= 32): the block's 64 rows are one
+// contiguous CRS range of at most 2048 entries, copied to shared memory with
+// fully coalesced loads, then written band by band.
+constexpr int kFlatRows = 64;
+constexpr int kFlatCap = kFlatRows * 32;
+
+__global__ void __launch_bounds__(256) k_crs_to_ell_cm_flat(int64_t n, int32_t nz, int64_t ld,
+                                                            const int32_t* __restrict__ irp,
+                                                            const int32_t* __restrict__ icol,
+                                                            const double* __restrict__ val,
+                                                            double* __restrict__ out_val,
+                                                            int32_t* __restrict__ out_col,
+                                                            int32_t* __restrict__ out_count) {
+  __shared__ int32_t s_ptr[kFlatRows + 1];
+  __shared__ double s_v[kFlatCap];
+  __shared__ int32_t s_c[kFlatCap];
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * kFlatRows;
+  for (int t = threadIdx.x; t <= kFlatRows; t += blockDim.x)
+    s_ptr[t] = __ldg(irp + min(r0 + t, n));
+  __syncthreads();
+  const int32_t e0 = s_ptr[0], cnt = s_ptr[kFlatRows] - e0;
+  for (int f = threadIdx.x; f < cnt; f += blockDim.x) {
+    s_v[f] = ld_stream(val + e0 + f);
+    s_c[f] = ld_stream(icol + e0 + f);
+  }
+  for (int t = threadIdx.x; t < kFlatRows; t += blockDim.x)
+    if (r0 + t < n) out_count[r0 + t] = s_ptr[t + 1] - s_ptr[t];
+  __syncthreads();
+  const int slots = nz * kFlatRows;
+  for (int f = threadIdx.x; f < slots; f += blockDim.x) {
+    const int k = f / kFlatRows, row = f % kFlatRows;
+    const int64_t i = r0 + row;
+    if (i >= ld) continue;
+    const int32_t a = s_ptr[row], len = s_ptr[row + 1] - a;
+    const bool real = k < len;
+    const int64_t slot = static_cast<int64_t>(k) * ld + i;
+    st_stream(out_val + slot, real ? s_v[a - e0 + k] : 0.0);
+    out_col[slot] = real ? s_c[a - e0 + k] : (i < n ? static_cast<int32_t>(i) : 0);
+  }
+}
+
 // Row-major ELL: the block's R rows own R*nz consecutive output slots; one
 // thread per slot, writes fully coalesced, reads row-contiguous.
 __global__ void __launch_bounds__(256) k_crs_to_ell_rm(int64_t n, int32_t nz, FastDiv div_nz,
@@ -407,7 +448,11 @@ int spmvtk_k_crs_to_ell_cm(int64_t n, int32_t nz, int64_t ld, const int32_t* irp
     k_crs_to_ell_cm<KC><<<blocks, 256, 0, s>>>(n, nz, ld, irp, icol, val, out_val, out_col,
                                                 out_count);
   };
-  if (nz <= 4) launch(std::integral_constant<int, 4>{});
+  if (nz <= 32) {
+    unsigned blocks = static_cast<unsigned>((ld + kFlatRows - 1) / kFlatRows);
+    k_crs_to_ell_cm_flat<<<blocks, 256, 0, s>>>(n, nz, ld, irp, icol, val, out_val, out_col,
+                                                out_count);
+  } else if (nz <= 4) launch(std::integral_constant<int, 4>{});
   else if (nz <= 8) launch(std::integral_constant<int, 8>{});
   else if (nz <= 16) launch(std::integral_constant<int, 16>{});
   else launch(std::integral_constant<int, 32>{});

@@ -8,6 +8,7 @@
 // /root/reference/proj/src/spmv.cpp; each kernel below names the one it
 // replaces.  Summation orders differ from the reference (fp64, FMA), which the
 // contract allows (max-norm relative 1e-12, BASELINE.json north_star).
+#include <string>
 #include <type_traits>
 
 #include "common.cuh"
@@ -49,10 +50,11 @@ __global__ void __launch_bounds__(256) k_spmv_vec(int64_t n, Rows rows,
                                                   const double* __restrict__ val,
                                                   const double* __restrict__ x,
                                                   double* __restrict__ y, int64_t long_limit,
-                                                  int32_t* long_rows) {
+                                                  int32_t* long_rows, bool hint) {
   const int lane = threadIdx.x & (W - 1);
   const unsigned mask = subwarp_mask(W);
   const int64_t nsub = (static_cast<int64_t>(gridDim.x) * blockDim.x) / W;
+  const uint64_t pf = policy_evict_first(), pl = policy_evict_last();
   for (int64_t r = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / W; r < n;
        r += nsub) {
     int64_t a, b;
@@ -69,13 +71,14 @@ __global__ void __launch_bounds__(256) k_spmv_vec(int64_t n, Rows rows,
       for (int j = 0; j < U; ++j) {
         const int64_t q = p + static_cast<int64_t>(j) * W;
         if (q < b) {
-          c[j] = ld_stream(col + q);
-          v[j] = ld_stream(val + q);
+          c[j] = hint ? ld_stream_hint(col + q, pf) : ld_stream(col + q);
+          v[j] = hint ? ld_stream_hint(val + q, pf) : ld_stream(val + q);
         }
       }
 #pragma unroll
       for (int j = 0; j < U; ++j)
-        if (p + static_cast<int64_t>(j) * W < b) acc = fma(v[j], ld_x(x + c[j]), acc);
+        if (p + static_cast<int64_t>(j) * W < b)
+          acc = fma(v[j], hint ? ld_x_hint(x + c[j], pl) : ld_x(x + c[j]), acc);
     }
 #pragma unroll
     for (int o = W / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(mask, acc, o, W);
@@ -83,7 +86,184 @@ __global__ void __launch_bounds__(256) k_spmv_vec(int64_t n, Rows rows,
   }
 }
 
-// block per long row (queue filled by k_spmv_vec)
+// ---- multi-row vector CRS -------------------------------------------------
+// A sub-warp of W lanes owns R consecutive rows at a time and issues the
+// loads of all R rows before consuming any (R x (entries/W) independent
+// col/val loads and x gathers in flight per lane -- the single-row vector
+// kernel was latency-bound).  The R partial sums are then reduced with a
+// transpose-reduction: R-1 + log2(W/R) shuffles leave lane l holding row
+// l / (W/R), instead of R*log2(W).
+template <int W, int R>
+__device__ __forceinline__ double transpose_reduce(double (&acc)[R], int lane, unsigned mask) {
+  static_assert(R <= W, "R rows need at least R lanes");
+  int off = W / 2;
+#pragma unroll
+  for (int s = R / 2; s >= 1; s /= 2, off /= 2) {
+    const bool upper = (lane & off) != 0;
+#pragma unroll
+    for (int k = 0; k < s; ++k) {
+      const double send = upper ? acc[k] : acc[k + s];
+      const double keep = upper ? acc[k + s] : acc[k];
+      acc[k] = keep + __shfl_xor_sync(mask, send, off, W);
+    }
+  }
+  double v = acc[0];
+#pragma unroll
+  for (; off >= 1; off /= 2) v += __shfl_xor_sync(mask, v, off, W);
+  return v;
+}
+
+template <int W, int R, typename Rows>
+__global__ void __launch_bounds__(256) k_spmv_multi(int64_t n, Rows rows,
+                                                    const int32_t* __restrict__ col,
+                                                    const double* __restrict__ val,
+                                                    const double* __restrict__ x,
+                                                    double* __restrict__ y, int64_t long_limit,
+                                                    int32_t* long_rows) {
+  const int lane = threadIdx.x & (W - 1);
+  const unsigned mask = subwarp_mask(W);
+  const int64_t nsub = (static_cast<int64_t>(gridDim.x) * blockDim.x) / W;
+  for (int64_t rb = ((static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / W) * R;
+       rb < n; rb += nsub * R) {
+    int64_t a[R], b[R];
+    int64_t maxlen = 0;
+    unsigned long_mask = 0;
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      if (rb + k < n) {
+        rows.get(rb + k, a[k], b[k]);
+      } else {
+        a[k] = b[k] = 0;
+      }
+      if (b[k] - a[k] > long_limit) {
+        if (lane == 0) long_rows[1 + atomicAdd(long_rows, 1)] = static_cast<int32_t>(rb + k);
+        b[k] = a[k];  // handled by the block-per-row pass
+        long_mask |= 1u << k;
+      }
+      maxlen = max(maxlen, b[k] - a[k]);
+    }
+    double acc[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k) acc[k] = 0.0;
+    for (int64_t off = lane; off < maxlen; off += W) {
+      int32_t c[R];
+      double v[R];
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        const int64_t p = a[k] + off;
+        if (p < b[k]) {
+          c[k] = ld_stream(col + p);
+          v[k] = ld_stream(val + p);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < R; ++k)
+        if (a[k] + off < b[k]) acc[k] = fma(v[k], ld_x(x + c[k]), acc[k]);
+    }
+    const double total = transpose_reduce<W, R>(acc, lane, mask);
+    constexpr int kLanesPerRow = W / R;
+    if ((lane & (kLanesPerRow - 1)) == 0) {
+      const int k = lane / kLanesPerRow;
+      if (rb + k < n && !((long_mask >> k) & 1u)) y[rb + k] = total;
+    }
+  }
+}
+
+// ---- tiled CRS ("stream" phase + per-row reduction from shared memory) ----
+// A block owns 256 consecutive rows.  Phase 1 streams the block's entries in
+// chunks of kTileC with one entry per thread (coalesced col/val loads, the x
+// gather, one multiply) into shared memory; phase 2 sums each row's products
+// out of shared memory, one thread per row for short segments, one warp per
+// segment for long ones.  ~8 warp instructions per 32 entries instead of ~90
+// for the sub-warp-per-row kernel, and the entry stream is perfectly balanced
+// inside a block whatever the row lengths.  Products are stored at a padded
+// index (p + p/16) so that rows 16 doubles apart do not share a bank.
+constexpr int kTileRows = 256;
+constexpr int kTileC = 4096;
+constexpr int kLongSeg = 48;
+
+__device__ __forceinline__ int tile_idx(int p) { return p + (p >> 4); }
+
+template <typename Rows>
+__global__ void __launch_bounds__(256) k_spmv_tile(int64_t n, Rows rows,
+                                                   const int32_t* __restrict__ col,
+                                                   const double* __restrict__ val,
+                                                   const double* __restrict__ x,
+                                                   double* __restrict__ y) {
+  __shared__ double s_prod[kTileC + kTileC / 16];
+  __shared__ int64_t s_ptr[kTileRows + 1];
+  __shared__ double s_extra[kTileRows];
+  __shared__ int s_list[kTileRows];
+  __shared__ int s_nlist;
+  const int t = threadIdx.x;
+  const int lane = t & 31, warp = t >> 5;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * kTileRows;
+  const int rows_here = static_cast<int>(min(static_cast<int64_t>(kTileRows), n - r0));
+  for (int k = t; k <= kTileRows; k += blockDim.x) {
+    int64_t a, b;
+    const int64_t r = r0 + min(k, rows_here);
+    if (k < rows_here) {
+      rows.get(r, a, b);
+    } else {
+      rows.get(r0 + rows_here - 1, a, b);
+      a = b;
+    }
+    s_ptr[k] = a;
+  }
+  s_extra[t] = 0.0;
+  __syncthreads();
+  const int64_t e0 = s_ptr[0], e1 = s_ptr[rows_here];
+  const int64_t my_a = s_ptr[t < rows_here ? t : rows_here];
+  const int64_t my_b = s_ptr[t < rows_here ? t + 1 : rows_here];
+  double acc = 0.0;
+  for (int64_t c0 = e0; c0 < e1; c0 += kTileC) {
+    const int len = static_cast<int>(min(static_cast<int64_t>(kTileC), e1 - c0));
+    // phase 1: products of the chunk, U = 4 entries per thread in flight
+    for (int base = 0; base < len; base += 4 * 256) {
+      int32_t c[4];
+      double v[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int q = base + j * 256 + t;
+        if (q < len) {
+          c[j] = ld_stream(col + c0 + q);
+          v[j] = ld_stream(val + c0 + q);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int q = base + j * 256 + t;
+        if (q < len) s_prod[tile_idx(q)] = v[j] * ld_x(x + c[j]);
+      }
+    }
+    if (t == 0) s_nlist = 0;
+    __syncthreads();
+    // phase 2a: short segments, one thread per row
+    const int lo = static_cast<int>(max(my_a, c0) - c0);
+    const int hi = static_cast<int>(min(my_b, c0 + len) - c0);
+    if (hi - lo > kLongSeg) {
+      s_list[atomicAdd(&s_nlist, 1)] = t;
+    } else {
+      for (int q = lo; q < hi; ++q) acc += s_prod[tile_idx(q)];
+    }
+    __syncthreads();
+    // phase 2b: long segments, one warp each
+    const int nl = s_nlist;
+    for (int i = warp; i < nl; i += blockDim.x >> 5) {
+      const int owner = s_list[i];
+      const int a = static_cast<int>(max(s_ptr[owner], c0) - c0);
+      const int b = static_cast<int>(min(s_ptr[owner + 1], c0 + len) - c0);
+      double s = 0.0;
+      for (int q = a + lane; q < b; q += 32) s += s_prod[tile_idx(q)];
+      s = warp_sum(s);
+      if (lane == 0) s_extra[owner] += s;
+    }
+    __syncthreads();
+  }
+  if (t < rows_here) y[r0 + t] = acc + s_extra[t];
+}
+
+// block per long row (queue filled by k_spmv_vec / k_spmv_multi)
 __global__ void __launch_bounds__(256) k_spmv_crs_long(const int32_t* __restrict__ irp,
                                                        const int32_t* __restrict__ col,
                                                        const double* __restrict__ val,
@@ -239,7 +419,7 @@ __global__ void __launch_bounds__(256) k_spmv_coo_col(int64_t nnz,
 // thread, fully coalesced (ld is a multiple of 32 so every band starts
 // 256-byte aligned).  Bands are walked in order with U loads in flight.
 // Every slot is multiplied, padding included (the ELL contract).
-template <int U>
+template <int U, bool H>
 __global__ void __launch_bounds__(256) k_spmv_ell_cm(int64_t n, int32_t k_begin, int32_t k_end,
                                                      int64_t ld, const double* __restrict__ val,
                                                      const int32_t* __restrict__ col,
@@ -252,26 +432,34 @@ __global__ void __launch_bounds__(256) k_spmv_ell_cm(int64_t n, int32_t k_begin,
   const double2* vp = reinterpret_cast<const double2*>(val + i);
   const int2* cp = reinterpret_cast<const int2*>(col + i);
   const int64_t step = ld >> 1;  // in double2 / int2 units
+  uint64_t pf = 0, pl = 0;
+  if (H) {
+    pf = policy_evict_first();
+    pl = policy_evict_last();
+  }
+  auto lv = [&](int64_t off) { return H ? ld_stream2_hint(vp + off, pf) : ld_stream2(vp + off); };
+  auto lc = [&](int64_t off) { return H ? ld_stream2_hint(cp + off, pf) : ld_stream2(cp + off); };
+  auto lx = [&](int32_t c) { return H ? ld_x_hint(x + c, pl) : ld_x(x + c); };
   int32_t k = k_begin;
   for (; k + U <= k_end; k += U) {
     double2 v[U];
     int2 c[U];
 #pragma unroll
     for (int j = 0; j < U; ++j) {
-      v[j] = ld_stream2(vp + static_cast<int64_t>(k + j) * step);
-      c[j] = ld_stream2(cp + static_cast<int64_t>(k + j) * step);
+      v[j] = lv(static_cast<int64_t>(k + j) * step);
+      c[j] = lc(static_cast<int64_t>(k + j) * step);
     }
 #pragma unroll
     for (int j = 0; j < U; ++j) {
-      a0 = fma(v[j].x, ld_x(x + c[j].x), a0);
-      a1 = fma(v[j].y, ld_x(x + c[j].y), a1);
+      a0 = fma(v[j].x, lx(c[j].x), a0);
+      a1 = fma(v[j].y, lx(c[j].y), a1);
     }
   }
   for (; k < k_end; ++k) {
-    const double2 v = ld_stream2(vp + static_cast<int64_t>(k) * step);
-    const int2 c = ld_stream2(cp + static_cast<int64_t>(k) * step);
-    a0 = fma(v.x, ld_x(x + c.x), a0);
-    a1 = fma(v.y, ld_x(x + c.y), a1);
+    const double2 v = lv(static_cast<int64_t>(k) * step);
+    const int2 c = lc(static_cast<int64_t>(k) * step);
+    a0 = fma(v.x, lx(c.x), a0);
+    a1 = fma(v.y, lx(c.y), a1);
   }
   // rows past n in the last pair are ld padding: their result is dropped
   y[i] = a0;
@@ -337,28 +525,60 @@ __global__ void k_reduce_partials(int64_t n, int32_t splits, const double* __res
   }
 }
 
+int g_l2_hint = 0;  // L2 evict_first (matrix) / evict_last (x) policies
+
 template <int W, int U, typename Rows>
 void launch_vec(int64_t n, Rows rows, const int32_t* col, const double* val, const double* x,
                 double* y, int64_t long_limit, int32_t* long_rows, cudaStream_t s) {
   const int64_t threads = n * W;
-  k_spmv_vec<W, U, Rows><<<grid_for(threads, 256, 8), 256, 0, s>>>(n, rows, col, val, x, y,
-                                                                   long_limit, long_rows);
+  k_spmv_vec<W, U, Rows><<<grid_for(threads, 256, 8), 256, 0, s>>>(
+      n, rows, col, val, x, y, long_limit, long_rows, g_l2_hint != 0);
 }
 
+template <int W, int R, typename Rows>
+void launch_multi(int64_t n, Rows rows, const int32_t* col, const double* val, const double* x,
+                  double* y, int64_t long_limit, int32_t* long_rows, cudaStream_t s) {
+  const int64_t threads = (n + R - 1) / R * W;
+  k_spmv_multi<W, R, Rows><<<grid_for(threads, 256, 8), 256, 0, s>>>(n, rows, col, val, x, y,
+                                                                     long_limit, long_rows);
+}
+
+int g_crs_variant = -1;  // tuning override (spmvtk_k_tune), -1 = heuristic
+
 template <typename Rows>
-void dispatch_vec(double mean, int64_t n, Rows rows, const int32_t* col, const double* val,
-                  const double* x, double* y, int64_t long_limit, int32_t* long_rows,
-                  cudaStream_t s) {
-  if (mean <= 3.0)
-    launch_vec<2, 2>(n, rows, col, val, x, y, long_limit, long_rows, s);
-  else if (mean <= 6.0)
-    launch_vec<4, 2>(n, rows, col, val, x, y, long_limit, long_rows, s);
-  else if (mean <= 12.0)
-    launch_vec<8, 2>(n, rows, col, val, x, y, long_limit, long_rows, s);
-  else if (mean <= 40.0)
-    launch_vec<16, 2>(n, rows, col, val, x, y, long_limit, long_rows, s);
-  else
-    launch_vec<32, 4>(n, rows, col, val, x, y, long_limit, long_rows, s);
+void dispatch_vec(double mean, int64_t max_row, int64_t n, Rows rows, const int32_t* col,
+                  const double* val, const double* x, double* y, int64_t long_limit,
+                  int32_t* long_rows, cudaStream_t s) {
+  int v = g_crs_variant;
+  if (v < 0) {
+    // measured on B200 (tools/tune_crs.py, profiles/r01_tune_crs.txt): few
+    // lanes per row (more rows in flight) win unless the rows are skewed
+    if (static_cast<double>(max_row) > 8.0 * mean + 8.0) v = 0;  // W=16
+    else if (mean <= 6.0) v = 12;                              // W=4
+    else if (mean <= 40.0) v = 11;                             // W=8
+    else v = 0;                                                // W=16
+  }
+  switch (v) {
+    case 11: launch_vec<8, 2>(n, rows, col, val, x, y, long_limit, long_rows, s); break;
+    case 12: launch_vec<4, 2>(n, rows, col, val, x, y, long_limit, long_rows, s); break;
+    case 13: launch_vec<32, 4>(n, rows, col, val, x, y, long_limit, long_rows, s); break;
+    case 14: launch_vec<32, 2>(n, rows, col, val, x, y, long_limit, long_rows, s); break;
+    case 0: launch_vec<16, 2>(n, rows, col, val, x, y, long_limit, long_rows, s); break;
+    case 1: launch_multi<4, 4>(n, rows, col, val, x, y, long_limit, long_rows, s); break;
+    case 2: launch_multi<8, 4>(n, rows, col, val, x, y, long_limit, long_rows, s); break;
+    case 3: launch_multi<16, 4>(n, rows, col, val, x, y, long_limit, long_rows, s); break;
+    case 4: launch_multi<32, 4>(n, rows, col, val, x, y, long_limit, long_rows, s); break;
+    case 5: launch_multi<8, 2>(n, rows, col, val, x, y, long_limit, long_rows, s); break;
+    case 6: launch_multi<8, 8>(n, rows, col, val, x, y, long_limit, long_rows, s); break;
+    case 7: launch_multi<16, 8>(n, rows, col, val, x, y, long_limit, long_rows, s); break;
+    case 8: launch_multi<4, 2>(n, rows, col, val, x, y, long_limit, long_rows, s); break;
+    case 9: launch_multi<16, 2>(n, rows, col, val, x, y, long_limit, long_rows, s); break;
+    case 10:
+      k_spmv_tile<Rows><<<static_cast<unsigned>((n + kTileRows - 1) / kTileRows), kTileRows, 0,
+                          s>>>(n, rows, col, val, x, y);
+      break;
+    default: launch_multi<8, 4>(n, rows, col, val, x, y, long_limit, long_rows, s); break;
+  }
 }
 
 }  // namespace
@@ -373,7 +593,7 @@ int spmvtk_k_spmv_crs(int64_t n, const int32_t* irp, const int32_t* icol, const 
   const int64_t long_limit = 4096;
   const bool use_long = long_rows != nullptr && max_row > long_limit;
   if (use_long) cudaMemsetAsync(long_rows, 0, sizeof(int32_t), s);
-  dispatch_vec(mean_row, n, CrsRows{irp}, icol, val, x, y,
+  dispatch_vec(mean_row, max_row, n, CrsRows{irp}, icol, val, x, y,
                use_long ? long_limit : INT64_MAX, long_rows, s);
   if (use_long) k_spmv_crs_long<<<kSMs * 4, 256, 0, s>>>(irp, icol, val, x, y, long_rows);
   SPMVTK_LAUNCH_RETURN();
@@ -415,7 +635,10 @@ int spmvtk_k_spmv_ell_cm(int64_t n, int32_t nz, int64_t ld, const double* val,
   }
   const int64_t pairs = (n + 1) / 2;
   const unsigned blocks = static_cast<unsigned>((pairs + 255) / 256);
-  k_spmv_ell_cm<4><<<blocks, 256, 0, s>>>(n, 0, nz, ld, val, col, x, y);
+  if (g_l2_hint)
+    k_spmv_ell_cm<4, true><<<blocks, 256, 0, s>>>(n, 0, nz, ld, val, col, x, y);
+  else
+    k_spmv_ell_cm<4, false><<<blocks, 256, 0, s>>>(n, 0, nz, ld, val, col, x, y);
   SPMVTK_LAUNCH_RETURN();
 }
 
@@ -437,9 +660,21 @@ int spmvtk_k_spmv_ell_rm(int64_t n, int32_t nz, const double* val, const int32_t
                          const double* x, double* y, void* stream) {
   cudaStream_t s = as_stream(stream);
   if (n <= 0) SPMVTK_LAUNCH_RETURN();
-  dispatch_vec(static_cast<double>(nz), n, EllRowMajorRows{nz}, col, val, x, y, INT64_MAX,
+  dispatch_vec(static_cast<double>(nz), nz, n, EllRowMajorRows{nz}, col, val, x, y, INT64_MAX,
                nullptr, s);
   SPMVTK_LAUNCH_RETURN();
+}
+
+int spmvtk_k_tune(const char* key, int value) {
+  if (key && std::string(key) == "crs_variant") {
+    g_crs_variant = value;
+    return 0;
+  }
+  if (key && std::string(key) == "l2_hint") {
+    g_l2_hint = value;
+    return 0;
+  }
+  return static_cast<int>(cudaErrorInvalidValue);
 }
 
 int spmvtk_k_preload(void) {
@@ -448,7 +683,8 @@ int spmvtk_k_preload(void) {
   cudaFuncGetAttributes(&a, k_spmv_crs_long);
   cudaFuncGetAttributes(&a, k_spmv_coo_row);
   cudaFuncGetAttributes(&a, k_spmv_coo_col);
-  cudaFuncGetAttributes(&a, k_spmv_ell_cm<4>);
+  cudaFuncGetAttributes(&a, k_spmv_ell_cm<4, false>);
+  cudaFuncGetAttributes(&a, k_spmv_ell_cm<4, true>);
   cudaFuncGetAttributes(&a, k_spmv_ell_cm_part<4>);
   cudaFuncGetAttributes(&a, k_reduce_partials);
   cudaFuncGetAttributes(&a, k_spmv_vec<2, 2, CrsRows>);
@@ -456,6 +692,14 @@ int spmvtk_k_preload(void) {
   cudaFuncGetAttributes(&a, k_spmv_vec<8, 2, CrsRows>);
   cudaFuncGetAttributes(&a, k_spmv_vec<16, 2, CrsRows>);
   cudaFuncGetAttributes(&a, k_spmv_vec<32, 4, CrsRows>);
+#define PRELOAD_MULTI(ROWS)                                 \
+  cudaFuncGetAttributes(&a, k_spmv_multi<4, 4, ROWS>);      \
+  cudaFuncGetAttributes(&a, k_spmv_multi<8, 4, ROWS>);      \
+  cudaFuncGetAttributes(&a, k_spmv_multi<16, 4, ROWS>);     \
+  cudaFuncGetAttributes(&a, k_spmv_multi<32, 4, ROWS>);
+  PRELOAD_MULTI(CrsRows)
+  PRELOAD_MULTI(EllRowMajorRows)
+#undef PRELOAD_MULTI
   cudaFuncGetAttributes(&a, k_spmv_vec<2, 2, EllRowMajorRows>);
   cudaFuncGetAttributes(&a, k_spmv_vec<4, 2, EllRowMajorRows>);
   cudaFuncGetAttributes(&a, k_spmv_vec<8, 2, EllRowMajorRows>);

@@ -267,6 +267,71 @@ Matrix* convert(const Matrix& a, spmvtk_format to, std::uint64_t max_bytes) {
   throw Error(ErrorCode::InvalidArgument, "unknown target format");
 }
 
+double transform_kernel_seconds(const Matrix& a, spmvtk_format to, int repeats) {
+  if (a.format != SPMVTK_FORMAT_CRS)
+    throw Error(ErrorCode::InvalidArgument, "operation requires a CRS handle");
+  if (repeats < 1) throw Error(ErrorCode::InvalidArgument, "repeats must be at least 1");
+  // outputs and scratch allocated once, outside the timed launches
+  std::unique_ptr<Matrix> out(convert(a, to, 0));
+  const std::int64_t n = a.n, nnz = a.nnz;
+  cudaStream_t st = rt::stream();
+  DevArray<std::int32_t> colptr;
+  DevArray<unsigned char> scratch;
+  if (to == SPMVTK_FORMAT_CCS || to == SPMVTK_FORMAT_COO_COL) {
+    colptr.reset(n + 1, "CCS col_ptr");
+    scratch.reset(spmvtk_k_ccs_scratch_bytes(n), "CCS scratch");
+  }
+  DevArray<unsigned long long> acc(3, "row statistics");
+  auto once = [&] {
+    switch (to) {
+      case SPMVTK_FORMAT_CRS:
+        cudaMemcpyAsync(out->ptr.get(), a.ptr.get(), a.ptr.bytes(), cudaMemcpyDeviceToDevice, st);
+        cudaMemcpyAsync(out->col.get(), a.col.get(), a.col.bytes(), cudaMemcpyDeviceToDevice, st);
+        cudaMemcpyAsync(out->val.get(), a.val.get(), a.val.bytes(), cudaMemcpyDeviceToDevice, st);
+        break;
+      case SPMVTK_FORMAT_COO_ROW:
+        cudaMemcpyAsync(out->col.get(), a.col.get(), a.col.bytes(), cudaMemcpyDeviceToDevice, st);
+        cudaMemcpyAsync(out->val.get(), a.val.get(), a.val.bytes(), cudaMemcpyDeviceToDevice, st);
+        rt::check_launch(spmvtk_k_expand_ptr(a.ptr.get(), n, nnz, out->row.get(), st), "expand");
+        break;
+      case SPMVTK_FORMAT_CCS:
+      case SPMVTK_FORMAT_COO_COL:
+        rt::check_launch(spmvtk_k_crs_to_ccs(n, nnz, a.ptr.get(), a.col.get(), a.val.get(),
+                                             colptr.get(), out->row.get(), out->val.get(),
+                                             scratch.get(), st),
+                         "CRS->CCS");
+        if (to == SPMVTK_FORMAT_COO_COL)
+          rt::check_launch(spmvtk_k_expand_ptr(colptr.get(), n, nnz, out->col.get(), st), "expand");
+        break;
+      case SPMVTK_FORMAT_ELL:
+        rt::check_launch(spmvtk_k_row_stats(a.ptr.get(), n, acc.get(), st), "row stats");
+        rt::check_launch(spmvtk_k_crs_to_ell_cm(n, out->band_count, out->ld, a.ptr.get(),
+                                                a.col.get(), a.val.get(), out->val.get(),
+                                                out->col.get(), out->count.get(), st),
+                         "CRS->ELL");
+        break;
+      case SPMVTK_FORMAT_ELL_ROWMAJOR:
+        rt::check_launch(spmvtk_k_row_stats(a.ptr.get(), n, acc.get(), st), "row stats");
+        rt::check_launch(spmvtk_k_crs_to_ell_rm(n, out->band_count, a.ptr.get(), a.col.get(),
+                                                a.val.get(), out->val.get(), out->col.get(),
+                                                out->count.get(), st),
+                         "CRS->ELL row-major");
+        break;
+    }
+  };
+  once();
+  rt::sync();
+  std::vector<double> samples;
+  rt::EventTimer timer;
+  for (int r = 0; r < repeats; ++r) {
+    timer.start();
+    once();
+    samples.push_back(timer.stop_seconds());
+  }
+  std::sort(samples.begin(), samples.end());
+  return samples[samples.size() / 2];
+}
+
 void spmv_device(const Matrix& m, spmvtk_kernel kernel, const double* x, double* y) {
   cudaStream_t st = rt::stream();
   switch (kernel) {

@@ -58,6 +58,10 @@ std::uint64_t device_bytes_for(const Matrix& crs, spmvtk_format to);
 // Conversions of a CRS handle (the guard applies to the ELL formats).
 Matrix* convert(const Matrix& crs, spmvtk_format to, std::uint64_t max_bytes);
 
+// Median device time of the transform's kernels alone (outputs and scratch
+// preallocated; the ELL variants include the band-count reduction).
+double transform_kernel_seconds(const Matrix& crs, spmvtk_format to, int repeats);
+
 // y = A x on device vectors, async on the current stream.  Throws
 // InvalidArgument when the kernel does not match the handle's format (or
 // COO ordering), with the reference's messages (capi.cpp:230-252).

@@ -173,10 +173,14 @@ SIGNATURES = {
     "spmvtk_host_crs_free": (None, [_P]),
     "spmvtk_matrix_from_host_crs": (C.c_int, [_P, _PP]),
     "spmvtk_conversion_bytes": (C.c_int, [_P, C.c_int, C.POINTER(_u64), C.POINTER(_u64)]),
+    "spmvtk_transform_kernel_seconds": (C.c_int, [_P, C.c_int, C.c_int, _pd]),
+    "spmvtk_reserve_device_memory": (C.c_int, [_u64]),
     "spmvtk_compute_metrics": (C.c_int, [_d, _d, _d, _pd, _pd, _pd]),
     "spmvtk_amortization_iterations": (C.c_int, [_d, _d, _d, C.POINTER(_i64)]),
     "spmvtk_find_d_star": (_d, [_pd, _pd, C.c_size_t, _d]),
     "spmvtk_version": (C.c_char_p, []),
+    # lower C ABI (device pointers); only the tuning knob is used from Python
+    "spmvtk_k_tune": (C.c_int, [C.c_char_p, C.c_int]),
 }
 
 _lib: C.CDLL | None = None
@@ -362,6 +366,15 @@ class Matrix:
 
     def write_matrix_market(self, path: str) -> None:
         _check(self._lib.spmvtk_write_matrix_market(self._h, path.encode()))
+
+    def transform_kernel_seconds(self, to: Format, repeats: int = 5) -> float:
+        s = C.c_double()
+        _check(self._lib.spmvtk_transform_kernel_seconds(self._h, int(to), repeats, C.byref(s)))
+        return s.value
+
+
+def reserve_device_memory(nbytes: int) -> None:
+    _check(load_library().spmvtk_reserve_device_memory(int(nbytes)))
 
 
 def bench(m: Matrix, variant: Kernel, lanes: int = 1, repeats: int = 9,

@@ -137,7 +137,9 @@ def test_kat_stats(gpu, kat):
         counts = np.array(c["counts"], np.int64)
         n = len(counts)
         rp = np.concatenate([[1], 1 + np.cumsum(counts)])
-        ci = np.concatenate([np.arange(1, k + 1) for k in counts])
+        # statistics are structure-only; column 1 everywhere keeps indices in
+        # range for any histogram (positions are not checked for distinctness)
+        ci = np.ones(int(counts.sum()), np.int64)
         m = upload(sp, n, rp, ci, np.ones(ci.shape[0]))
         s = m.row_stats()
         if c.get("exact"):
