@@ -238,7 +238,7 @@ def impl_ours(args):
     from paper_2407_00019_b200 import spmvtk as sp
 
     rank, world, local = dist_env()
-    if world > 1:
+    if world > 1 or args.force_dist:
         from paper_2407_00019_b200 import dist
         return dist.bench_main(args, rank, world, local)
 
@@ -400,6 +400,8 @@ def main():
     ap.add_argument("--param", type=int, default=None)
     ap.add_argument("--seed", type=int, default=2407)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--force-dist", action="store_true",
+                    help="use the row-block/NCCL path even on one rank (testing)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

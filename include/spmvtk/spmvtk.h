@@ -173,14 +173,25 @@ spmvtk_status spmvtk_matrix_from_crs(int64_t n, int64_t nnz, const void* row_ptr
                                      int index_width, int index_base, int on_device,
                                      spmvtk_matrix** out);
 
+/* Row-block shard for multi-GPU row partitioning: nrows local rows of a
+ * matrix with ncols columns; row_offset is the global index of local row 0
+ * (used for ELL padding columns).  Shards convert to CRS, COO-row and ELL
+ * (both layouts); SpMV takes x of length ncols and writes nrows entries. */
+spmvtk_status spmvtk_matrix_from_crs_block(int64_t nrows, int64_t ncols, int64_t row_offset,
+                                           int64_t nnz, const void* row_ptr, const void* col_idx,
+                                           const double* values, int index_width, int index_base,
+                                           int on_device, spmvtk_matrix** out);
+
 typedef struct spmvtk_matrix_desc {
   int32_t format;       /* spmvtk_format */
   int32_t ordering;     /* COO: 0 row-major, 1 column-major; else -1 */
-  int64_t n;
+  int64_t n;            /* rows */
   int64_t nnz;          /* stored entries (ELL: stored_nnz) */
   int64_t band_count;   /* ELL only */
   int64_t ld;           /* ELL band-major leading dimension on the device */
   uint64_t device_bytes;
+  int64_t ncols;        /* columns (== n unless a row-block shard) */
+  int64_t row_offset;   /* global index of row 0 (row-block shards) */
 } spmvtk_matrix_desc;
 
 spmvtk_status spmvtk_matrix_describe(const spmvtk_matrix* m, spmvtk_matrix_desc* out);

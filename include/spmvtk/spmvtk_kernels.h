@@ -65,17 +65,20 @@ int spmvtk_k_exclusive_scan(const int32_t* in, int32_t* out, int64_t n,
                             void* scratch, void* stream);
 
 /* CRS -> ELL (convert.cpp:81-115), band-major: slot(k,i) = k*ld + i, with
- * ld >= n (ld = n reproduces the reference array exactly).  Padding slots
- * get value +0.0 and column = own row.  out_count[i] = row length. */
+ * ld >= n a multiple of 32 (the rows [n, ld) are layout padding: value 0,
+ * column pad_base; exporting the first n rows of each band reproduces the
+ * reference array).  Padding slots get value +0.0 and column = own row
+ * (pad_base + i: pad_base is the global index of row 0 for a row-block
+ * shard, 0 otherwise).  out_count[i] = row length. */
 int spmvtk_k_crs_to_ell_cm(int64_t n, int32_t nz, int64_t ld, const int32_t* irp,
                            const int32_t* icol, const double* val,
                            double* out_val, int32_t* out_col,
-                           int32_t* out_count, void* stream);
+                           int32_t* out_count, int64_t pad_base, void* stream);
 /* Row-major ELL (no reference counterpart): slot(i,k) = i*nz + k. */
 int spmvtk_k_crs_to_ell_rm(int64_t n, int32_t nz, const int32_t* irp,
                            const int32_t* icol, const double* val,
                            double* out_val, int32_t* out_col,
-                           int32_t* out_count, void* stream);
+                           int32_t* out_count, int64_t pad_base, void* stream);
 
 /* ---- SpMV (y is overwritten; every row of y is written) ----------------*/
 

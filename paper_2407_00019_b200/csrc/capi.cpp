@@ -231,14 +231,15 @@ spmvtk_status spmvtk_spmv(const spmvtk_matrix* m, spmvtk_kernel kernel, const do
     if (!valid_kernel(kernel)) throw Error(ErrorCode::InvalidArgument, "unknown kernel id");
     if (kernel != SPMVTK_KERNEL_CRS && lanes < 1)
       throw Error(ErrorCode::InvalidArgument, "lane count must be at least 1");
-    if (len != m->n)
+    if (len != m->ncols)
       throw Error(ErrorCode::InvalidArgument, "vector length " + std::to_string(len) +
                                                   " does not match matrix dimension " +
-                                                  std::to_string(m->n));
+                                                  std::to_string(m->ncols));
     rt::init();
     const std::size_t n = static_cast<std::size_t>(m->n);
-    rt::DevArray<double> dx(std::max<std::size_t>(n, 1), "x"), dy(std::max<std::size_t>(n, 1), "y");
-    rt::copy_to_device(dx.get(), x, n * sizeof(double));
+    const std::size_t nc = static_cast<std::size_t>(m->ncols);
+    rt::DevArray<double> dx(std::max<std::size_t>(nc, 1), "x"), dy(std::max<std::size_t>(n, 1), "y");
+    rt::copy_to_device(dx.get(), x, nc * sizeof(double));
     rt::EventTimer timer;
     timer.start();
     dev::spmv_device(*m, kernel, dx.get(), dy.get());
@@ -371,6 +372,17 @@ spmvtk_status spmvtk_matrix_from_crs(int64_t n, int64_t nnz, const void* row_ptr
   });
 }
 
+spmvtk_status spmvtk_matrix_from_crs_block(int64_t nrows, int64_t ncols, int64_t row_offset,
+                                           int64_t nnz, const void* row_ptr, const void* col_idx,
+                                           const double* values, int index_width, int index_base,
+                                           int on_device, spmvtk_matrix** out) {
+  return guarded([&] {
+    need(out, "null output");
+    *out = dev::crs_block_from_arrays(nrows, ncols, row_offset, nnz, row_ptr, col_idx, values,
+                                      index_width, index_base, on_device != 0);
+  });
+}
+
 spmvtk_status spmvtk_matrix_describe(const spmvtk_matrix* m, spmvtk_matrix_desc* out) {
   return guarded([&] {
     need(m);
@@ -382,6 +394,8 @@ spmvtk_status spmvtk_matrix_describe(const spmvtk_matrix* m, spmvtk_matrix_desc*
     out->band_count = m->band_count;
     out->ld = m->ld;
     out->device_bytes = m->device_bytes();
+    out->ncols = m->ncols;
+    out->row_offset = m->row_offset;
   });
 }
 

@@ -266,7 +266,8 @@ __global__ void __launch_bounds__(256) k_crs_to_ell_cm(int64_t n, int32_t nz, in
                                                        const double* __restrict__ val,
                                                        double* __restrict__ out_val,
                                                        int32_t* __restrict__ out_col,
-                                                       int32_t* __restrict__ out_count) {
+                                                       int32_t* __restrict__ out_count,
+                                                       int64_t pad_base) {
   constexpr int R = 2048 / KC;
   __shared__ int32_t s_ptr[R + 1];
   __shared__ double s_v[R][KC + 1];
@@ -299,7 +300,7 @@ __global__ void __launch_bounds__(256) k_crs_to_ell_cm(int64_t n, int32_t nz, in
         const int64_t slot = static_cast<int64_t>(k) * ld + i;
         const bool real = k < len;
         st_stream(out_val + slot, real ? s_v[row][kk] : 0.0);
-        out_col[slot] = real ? s_c[row][kk] : (i < n ? static_cast<int32_t>(i) : 0);
+        out_col[slot] = real ? s_c[row][kk] : static_cast<int32_t>(pad_base + (i < n ? i : 0));
       }
     }
     __syncthreads();
@@ -318,7 +319,8 @@ __global__ void __launch_bounds__(256) k_crs_to_ell_cm_flat(int64_t n, int32_t n
                                                             const double* __restrict__ val,
                                                             double* __restrict__ out_val,
                                                             int32_t* __restrict__ out_col,
-                                                            int32_t* __restrict__ out_count) {
+                                                            int32_t* __restrict__ out_count,
+                                                            int64_t pad_base) {
   __shared__ int32_t s_ptr[kFlatRows + 1];
   __shared__ double s_v[kFlatCap];
   __shared__ int32_t s_c[kFlatCap];
@@ -343,7 +345,7 @@ __global__ void __launch_bounds__(256) k_crs_to_ell_cm_flat(int64_t n, int32_t n
     const bool real = k < len;
     const int64_t slot = static_cast<int64_t>(k) * ld + i;
     st_stream(out_val + slot, real ? s_v[a - e0 + k] : 0.0);
-    out_col[slot] = real ? s_c[a - e0 + k] : (i < n ? static_cast<int32_t>(i) : 0);
+    out_col[slot] = real ? s_c[a - e0 + k] : static_cast<int32_t>(pad_base + (i < n ? i : 0));
   }
 }
 
@@ -356,7 +358,8 @@ __global__ void __launch_bounds__(256) k_crs_to_ell_rm(int64_t n, int32_t nz, Fa
                                                        const double* __restrict__ val,
                                                        double* __restrict__ out_val,
                                                        int32_t* __restrict__ out_col,
-                                                       int32_t* __restrict__ out_count) {
+                                                       int32_t* __restrict__ out_count,
+                                                       int64_t pad_base) {
   extern __shared__ int32_t s_ptr[];
   const int64_t r0 = static_cast<int64_t>(blockIdx.x) * rows_per_block;
   const int rows = static_cast<int>(min(static_cast<int64_t>(rows_per_block), n - r0));
@@ -371,7 +374,7 @@ __global__ void __launch_bounds__(256) k_crs_to_ell_rm(int64_t n, int32_t nz, Fa
     const int32_t k = static_cast<int32_t>(f - row * static_cast<uint32_t>(nz));
     const int32_t a = s_ptr[row], len = s_ptr[row + 1] - a;
     double v = 0.0;
-    int32_t c = static_cast<int32_t>(r0 + row);
+    int32_t c = static_cast<int32_t>(pad_base + r0 + row);
     if (k < len) {
       v = ld_stream(val + a + k);
       c = ld_stream(icol + a + k);
@@ -437,7 +440,8 @@ int spmvtk_k_crs_to_ccs(int64_t n, int64_t nnz, const int32_t* irp, const int32_
 
 int spmvtk_k_crs_to_ell_cm(int64_t n, int32_t nz, int64_t ld, const int32_t* irp,
                            const int32_t* icol, const double* val, double* out_val,
-                           int32_t* out_col, int32_t* out_count, void* stream) {
+                           int32_t* out_col, int32_t* out_count, int64_t pad_base,
+                           void* stream) {
   cudaStream_t s = as_stream(stream);
   if (n <= 0) SPMVTK_LAUNCH_RETURN();
   if (ld < n || (ld & 31) != 0) return static_cast<int>(cudaErrorInvalidValue);
@@ -446,12 +450,12 @@ int spmvtk_k_crs_to_ell_cm(int64_t n, int32_t nz, int64_t ld, const int32_t* irp
     constexpr int R = 2048 / KC;  // multiple of 32, so blocks also cover [n, ld)
     unsigned blocks = static_cast<unsigned>((ld + R - 1) / R);
     k_crs_to_ell_cm<KC><<<blocks, 256, 0, s>>>(n, nz, ld, irp, icol, val, out_val, out_col,
-                                                out_count);
+                                                out_count, pad_base);
   };
   if (nz <= 32) {
     unsigned blocks = static_cast<unsigned>((ld + kFlatRows - 1) / kFlatRows);
     k_crs_to_ell_cm_flat<<<blocks, 256, 0, s>>>(n, nz, ld, irp, icol, val, out_val, out_col,
-                                                out_count);
+                                                out_count, pad_base);
   } else if (nz <= 4) launch(std::integral_constant<int, 4>{});
   else if (nz <= 8) launch(std::integral_constant<int, 8>{});
   else if (nz <= 16) launch(std::integral_constant<int, 16>{});
@@ -461,7 +465,7 @@ int spmvtk_k_crs_to_ell_cm(int64_t n, int32_t nz, int64_t ld, const int32_t* irp
 
 int spmvtk_k_crs_to_ell_rm(int64_t n, int32_t nz, const int32_t* irp, const int32_t* icol,
                            const double* val, double* out_val, int32_t* out_col,
-                           int32_t* out_count, void* stream) {
+                           int32_t* out_count, int64_t pad_base, void* stream) {
   cudaStream_t s = as_stream(stream);
   if (n <= 0) SPMVTK_LAUNCH_RETURN();
   // ~4096 slots per block, at least one row
@@ -471,7 +475,8 @@ int spmvtk_k_crs_to_ell_rm(int64_t n, int32_t nz, const int32_t* irp, const int3
   unsigned blocks = static_cast<unsigned>((n + rows - 1) / rows);
   size_t smem = static_cast<size_t>(rows + 1) * sizeof(int32_t);
   k_crs_to_ell_rm<<<blocks, 256, smem, s>>>(n, nz, FastDiv(static_cast<uint32_t>(nz > 0 ? nz : 1)),
-                                           rows, irp, icol, val, out_val, out_col, out_count);
+                                           rows, irp, icol, val, out_val, out_col, out_count,
+                                           pad_base);
   SPMVTK_LAUNCH_RETURN();
 }
 

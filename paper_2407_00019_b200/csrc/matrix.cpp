@@ -69,7 +69,16 @@ Matrix* new_matrix(spmvtk_format f, std::int64_t n, std::int64_t nnz) {
   m->format = f;
   m->n = n;
   m->nnz = nnz;
+  m->ncols = n;
   cudaGetDevice(&m->device);
+  return m;
+}
+
+// conversions inherit the shape of their source (row-block shards)
+Matrix* derived(const Matrix& src, spmvtk_format f, std::int64_t nnz) {
+  Matrix* m = new_matrix(f, src.n, nnz);
+  m->ncols = src.ncols;
+  m->row_offset = src.row_offset;
   return m;
 }
 
@@ -105,8 +114,19 @@ rt::Moments crs_moments(const Matrix& m) {
 Matrix* crs_from_arrays(std::int64_t n, std::int64_t nnz, const void* row_ptr,
                         const void* col_idx, const double* values, int index_width,
                         int index_base, bool on_device) {
+  return crs_block_from_arrays(n, n, 0, nnz, row_ptr, col_idx, values, index_width, index_base,
+                               on_device);
+}
+
+Matrix* crs_block_from_arrays(std::int64_t n, std::int64_t ncols, std::int64_t row_offset,
+                              std::int64_t nnz, const void* row_ptr, const void* col_idx,
+                              const double* values, int index_width, int index_base,
+                              bool on_device) {
   rt::init();
   require_int32_range(n, nnz);
+  require_int32_range(ncols, 0);
+  if (row_offset < 0 || row_offset > INT32_MAX)
+    throw Error(ErrorCode::InvalidArgument, "row offset out of range");
   if (nnz < 0) throw Error(ErrorCode::InvalidArgument, "negative nnz");
   if (index_width != 4 && index_width != 8)
     throw Error(ErrorCode::InvalidArgument, "index_width must be 4 or 8");
@@ -115,6 +135,8 @@ Matrix* crs_from_arrays(std::int64_t n, std::int64_t nnz, const void* row_ptr,
   if (!row_ptr || ((!col_idx || !values) && nnz > 0))
     throw Error(ErrorCode::InvalidArgument, "null array");
   std::unique_ptr<Matrix> m(new_matrix(SPMVTK_FORMAT_CRS, n, nnz));
+  m->ncols = ncols;
+  m->row_offset = row_offset;
   upload_index(m->ptr, row_ptr, n + 1, index_width, index_base, on_device, "row_ptr upload");
   upload_index(m->col, col_idx, nnz, index_width, index_base, on_device, "col_idx upload");
   m->val.reset(static_cast<std::size_t>(nnz), "values upload");
@@ -135,7 +157,7 @@ Matrix* crs_from_arrays(std::int64_t n, std::int64_t nnz, const void* row_ptr,
   rt::Moments mo = rt::row_moments(m->ptr.get(), n);
   if (!mo.monotone) throw Error(ErrorCode::Validation, "row_ptr not nondecreasing");
   m->moments = mo;
-  if (nnz && count_bad_indices(m->col.get(), nnz, n))
+  if (nnz && count_bad_indices(m->col.get(), nnz, ncols))
     throw Error(ErrorCode::Validation, "column index out of range");
   return m.release();
 }
@@ -172,7 +194,7 @@ Matrix* convert(const Matrix& a, spmvtk_format to, std::uint64_t max_bytes) {
   const std::int64_t n = a.n, nnz = a.nnz;
   switch (to) {
     case SPMVTK_FORMAT_CRS: {
-      std::unique_ptr<Matrix> m(new_matrix(SPMVTK_FORMAT_CRS, n, nnz));
+      std::unique_ptr<Matrix> m(derived(a, SPMVTK_FORMAT_CRS, nnz));
       m->ptr.reset(n + 1, "CRS copy");
       m->col.reset(nnz, "CRS copy");
       m->val.reset(nnz, "CRS copy");
@@ -186,7 +208,7 @@ Matrix* convert(const Matrix& a, spmvtk_format to, std::uint64_t max_bytes) {
     }
     case SPMVTK_FORMAT_COO_ROW: {
       // convert.cpp:11-22: copy values / col_idx, expand row_ptr
-      std::unique_ptr<Matrix> m(new_matrix(SPMVTK_FORMAT_COO_ROW, n, nnz));
+      std::unique_ptr<Matrix> m(derived(a, SPMVTK_FORMAT_COO_ROW, nnz));
       m->ordering = 0;
       m->row.reset(nnz, "COO row_idx");
       m->col.reset(nnz, "COO col_idx");
@@ -205,7 +227,11 @@ Matrix* convert(const Matrix& a, spmvtk_format to, std::uint64_t max_bytes) {
       // COO-col Phase II (convert.cpp:55-66) expands col_ptr into col_idx
       // and the CCS arrays become the COO arrays without a copy.
       const bool coo = to == SPMVTK_FORMAT_COO_COL;
-      std::unique_ptr<Matrix> m(new_matrix(to, n, nnz));
+      if (a.ncols != a.n)
+        throw Error(ErrorCode::InvalidArgument,
+                    "column-ordered formats need a square matrix (row-block shards convert to "
+                    "CRS, COO-row and ELL only)");
+      std::unique_ptr<Matrix> m(derived(a, to, nnz));
       m->row.reset(nnz, "CCS row_idx");
       m->val.reset(nnz, "CCS values");
       DevArray<std::int32_t> colptr(n + 1, "CCS col_ptr");
@@ -243,7 +269,7 @@ Matrix* convert(const Matrix& a, spmvtk_format to, std::uint64_t max_bytes) {
         throw Error(ErrorCode::InvalidArgument, "band count exceeds int32");
       const std::int32_t nz = static_cast<std::int32_t>(mo.max);
       const bool cm = to == SPMVTK_FORMAT_ELL;
-      std::unique_ptr<Matrix> m(new_matrix(to, n, nnz));
+      std::unique_ptr<Matrix> m(derived(a, to, nnz));
       m->band_count = nz;
       m->ld = cm ? round_up(n, 32) : n;
       const std::size_t slots =
@@ -255,11 +281,12 @@ Matrix* convert(const Matrix& a, spmvtk_format to, std::uint64_t max_bytes) {
       if (cm)
         rt::check_launch(spmvtk_k_crs_to_ell_cm(n, nz, m->ld, a.ptr.get(), a.col.get(),
                                                 a.val.get(), m->val.get(), m->col.get(),
-                                                m->count.get(), st),
+                                                m->count.get(), a.row_offset, st),
                          "CRS->ELL");
       else
         rt::check_launch(spmvtk_k_crs_to_ell_rm(n, nz, a.ptr.get(), a.col.get(), a.val.get(),
-                                                m->val.get(), m->col.get(), m->count.get(), st),
+                                                m->val.get(), m->col.get(), m->count.get(),
+                                                a.row_offset, st),
                          "CRS->ELL row-major");
       return m.release();
     }
@@ -307,14 +334,15 @@ double transform_kernel_seconds(const Matrix& a, spmvtk_format to, int repeats) 
         rt::check_launch(spmvtk_k_row_stats(a.ptr.get(), n, acc.get(), st), "row stats");
         rt::check_launch(spmvtk_k_crs_to_ell_cm(n, out->band_count, out->ld, a.ptr.get(),
                                                 a.col.get(), a.val.get(), out->val.get(),
-                                                out->col.get(), out->count.get(), st),
+                                                out->col.get(), out->count.get(), a.row_offset,
+                                                st),
                          "CRS->ELL");
         break;
       case SPMVTK_FORMAT_ELL_ROWMAJOR:
         rt::check_launch(spmvtk_k_row_stats(a.ptr.get(), n, acc.get(), st), "row stats");
         rt::check_launch(spmvtk_k_crs_to_ell_rm(n, out->band_count, a.ptr.get(), a.col.get(),
                                                 a.val.get(), out->val.get(), out->col.get(),
-                                                out->count.get(), st),
+                                                out->count.get(), a.row_offset, st),
                          "CRS->ELL row-major");
         break;
     }

@@ -20,8 +20,10 @@ struct spmvtk_matrix {
   spmvtk_format format = SPMVTK_FORMAT_CRS;
   int ordering = -1;  // COO: 0 row-major, 1 column-major
   int device = 0;
-  std::int64_t n = 0;
-  std::int64_t nnz = 0;  // stored entries; ELL: stored_nnz (real entries)
+  std::int64_t n = 0;     // rows
+  std::int64_t nnz = 0;   // stored entries; ELL: stored_nnz (real entries)
+  std::int64_t ncols = 0; // columns (== n except for row-block shards)
+  std::int64_t row_offset = 0;  // global index of row 0 (row-block shards)
 
   spmvtk::rt::DevArray<double> val;
   spmvtk::rt::DevArray<std::int32_t> ptr;    // CRS row_ptr / CCS col_ptr
@@ -50,6 +52,12 @@ rt::Moments crs_moments(const Matrix& m);
 Matrix* crs_from_arrays(std::int64_t n, std::int64_t nnz, const void* row_ptr,
                         const void* col_idx, const double* values, int index_width,
                         int index_base, bool on_device);
+// Row-block shard: nrows local rows holding global columns in [0, ncols);
+// row_offset = global index of local row 0 (multi-GPU row partitioning).
+Matrix* crs_block_from_arrays(std::int64_t nrows, std::int64_t ncols, std::int64_t row_offset,
+                              std::int64_t nnz, const void* row_ptr, const void* col_idx,
+                              const double* values, int index_width, int index_base,
+                              bool on_device);
 
 // Reference ELL estimate (8+8 bytes per slot, convert.cpp:72-79).
 std::uint64_t reference_ell_estimate(const Matrix& crs);

@@ -112,7 +112,7 @@ class RecordView(C.Structure):
 class MatrixDesc(C.Structure):
     _fields_ = [("format", C.c_int32), ("ordering", C.c_int32), ("n", C.c_int64),
                 ("nnz", C.c_int64), ("band_count", C.c_int64), ("ld", C.c_int64),
-                ("device_bytes", C.c_uint64)]
+                ("device_bytes", C.c_uint64), ("ncols", C.c_int64), ("row_offset", C.c_int64)]
 
 
 class RowStats(C.Structure):
@@ -159,6 +159,8 @@ SIGNATURES = {
     "spmvtk_get_stream": (_P, []),
     "spmvtk_synchronize": (C.c_int, []),
     "spmvtk_matrix_from_crs": (C.c_int, [_i64, _i64, _P, _P, _P, C.c_int, C.c_int, C.c_int, _PP]),
+    "spmvtk_matrix_from_crs_block": (C.c_int, [_i64, _i64, _i64, _i64, _P, _P, _P, C.c_int,
+                                               C.c_int, C.c_int, _PP]),
     "spmvtk_matrix_describe": (C.c_int, [_P, C.POINTER(MatrixDesc)]),
     "spmvtk_matrix_copy_array": (C.c_int, [_P, C.c_int, _P, _i64, C.c_int, C.c_int,
                                            C.POINTER(_i64)]),
@@ -276,6 +278,20 @@ class Matrix:
                          rp.dtype.itemsize, index_base, 0)
 
     @classmethod
+    def from_crs_block(cls, nrows: int, ncols: int, row_offset: int, row_ptr, col_idx, values,
+                       index_base: int = 0) -> "Matrix":
+        """Row-block shard (multi-GPU): local rows, global columns."""
+        rp = np.ascontiguousarray(row_ptr)
+        if rp.dtype not in (np.int32, np.int64):
+            rp = rp.astype(np.int64)
+        ci = np.ascontiguousarray(col_idx).astype(rp.dtype, copy=False)
+        v = np.ascontiguousarray(values, dtype=np.float64)
+        lib = load_library()
+        return cls._make(lib.spmvtk_matrix_from_crs_block, nrows, ncols, row_offset,
+                         int(v.shape[0]), _ptr(rp), _ptr(ci), _ptr(v), rp.dtype.itemsize,
+                         index_base, 0)
+
+    @classmethod
     def from_crs_device(cls, n: int, nnz: int, row_ptr_ptr: int, col_idx_ptr: int,
                         values_ptr: int, index_width: int = 4, index_base: int = 0) -> "Matrix":
         lib = load_library()
@@ -354,7 +370,8 @@ class Matrix:
     def spmv(self, x, kernel: Kernel = Kernel.CRS, lanes: int = 1,
              out: np.ndarray | None = None) -> tuple[np.ndarray, float]:
         xs = np.ascontiguousarray(x, dtype=np.float64)
-        y = out if out is not None else np.empty(xs.shape[0], dtype=np.float64)
+        # y has one entry per row (== len(x) except for row-block shards)
+        y = out if out is not None else np.empty(self.describe().n, dtype=np.float64)
         el = C.c_double()
         _check(self._lib.spmvtk_spmv(self._h, int(kernel), _ptr(xs), xs.shape[0], lanes,
                                      _ptr(y), C.byref(el)))

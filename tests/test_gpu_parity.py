@@ -431,3 +431,54 @@ def test_validation_rejects_bad_arrays(gpu):
     with pytest.raises(sp.SpmvtkError) as e:
         sp.Matrix.from_crs(2, np.array([1, 1, 2]), np.array([0]), np.ones(1), index_base=0)
     assert e.value.status == sp.Status.ERR_DATA
+
+
+def test_row_block_shards_single_gpu(gpu, port):
+    """Row-block shards (the multi-GPU layout) run on one GPU: per-shard
+    SpMV assembled == full SpMV (1e-12), and each shard's ELL equals the
+    reference ELL of its row block embedded in the n x n matrix (padding
+    column = global row index)."""
+    from paper_2407_00019_b200 import dist as D
+    sp = gpu
+    rng = np.random.default_rng(5)
+    n, rp, ci, v = random_crs(rng, 3000, 60000)
+    x = rng.uniform(-1, 1, n)
+    want = port.spmv_crs(n, rp, ci, v, x)
+    rp0, ci0 = rp - 1, ci - 1
+    kernels = ((sp.Kernel.CRS, None), (sp.Kernel.ELL_INNER, sp.Format.ELL),
+               (sp.Kernel.COO_ROW_OUTER, sp.Format.COO_ROW),
+               (sp.Kernel.ELL_ROWMAJOR, sp.Format.ELL_ROWMAJOR))
+    for world in (2, 3, 4):
+        parts = {k: [] for k, _ in kernels}
+        for r in range(world):
+            r0, lrp, lci, lv = D.shard_arrays(rp0, ci0, v, n, world, r)
+            rows = D.block_rows(n, world)
+            sh = sp.Matrix.from_crs_block(rows, n, r0, lrp, lci, lv)
+            d = sh.describe()
+            assert (d.n, d.ncols, d.row_offset) == (rows, n, r0)
+            for k, f in kernels:
+                h = sh if f is None else sh.convert(f)
+                y, _ = h.spmv(x, k)
+                assert y.shape[0] == rows
+                parts[k].append(y[: D.block_range(n, world, r)[1] - r0])
+            # ELL arrays of the shard vs the reference ELL of the embedded block
+            a, b = D.block_range(n, world, r)
+            erp = np.concatenate([np.full(a, rp[a]), rp[a:b + 1],
+                                  np.full(n - b, rp[b])]).astype(np.int64)
+            erp = erp - erp[0] + 1
+            sl = slice(rp[a] - 1, rp[b] - 1)
+            bc, ev, ec, cnt = port.crs_to_ell(n, erp, ci[sl], v[sl])
+            ell = sh.convert(sp.Format.ELL)
+            assert ell.describe().band_count == bc
+            got_v = ell.array(sp.Array.VALUES).reshape(bc, rows) if bc else np.zeros((0, rows))
+            got_c = ell.array(sp.Array.COL_IDX, 8, 1).reshape(bc, rows) if bc else None
+            want_v = ev.reshape(bc, n)[:, a:b] if bc else np.zeros((0, b - a))
+            assert got_v[:, : b - a].tobytes() == np.ascontiguousarray(want_v).tobytes()
+            if bc:
+                np.testing.assert_array_equal(got_c[:, : b - a], ec.reshape(bc, n)[:, a:b])
+        for k, _ in kernels:
+            assert max_rel_error(np.concatenate(parts[k]), want) <= TOL, (world, k)
+    with pytest.raises(sp.SpmvtkError) as e:
+        sp.Matrix.from_crs_block(2, 10, 0, np.array([0, 1, 2]), np.array([3, 9]),
+                                 np.ones(2)).convert(sp.Format.CCS)
+    assert e.value.status == sp.Status.ERR_USAGE
