@@ -162,6 +162,68 @@ Matrix* crs_block_from_arrays(std::int64_t n, std::int64_t ncols, std::int64_t r
   return m.release();
 }
 
+Matrix* coo_from_arrays(std::int64_t n, std::int64_t nnz, const void* rows, const void* cols,
+                        const double* values, int index_width, int index_base, int ordering) {
+  rt::init();
+  require_int32_range(n, nnz);
+  if (ordering != 0 && ordering != 1)
+    throw Error(ErrorCode::InvalidArgument, "COO ordering must be row- or column-major");
+  std::unique_ptr<Matrix> m(new_matrix(ordering == 0 ? SPMVTK_FORMAT_COO_ROW
+                                                     : SPMVTK_FORMAT_COO_COL,
+                                       n, nnz));
+  m->ordering = ordering;
+  upload_index(m->row, rows, nnz, index_width, index_base, false, "COO row upload");
+  upload_index(m->col, cols, nnz, index_width, index_base, false, "COO col upload");
+  m->val.reset(static_cast<std::size_t>(nnz), "COO values upload");
+  if (nnz) rt::copy_to_device(m->val.get(), values, nnz * sizeof(double));
+  if (nnz && (count_bad_indices(m->row.get(), nnz, n) || count_bad_indices(m->col.get(), nnz, n)))
+    throw Error(ErrorCode::Validation, "COO index out of range");
+  if (ordering == 0 && nnz > 1) {
+    DevArray<unsigned long long> bad(1, "validation");
+    rt::check_launch(spmvtk_k_count_descents(m->row.get(), nnz, bad.get(), s()), "validation");
+    unsigned long long h = 0;
+    rt::copy_to_host(&h, bad.get(), sizeof(h));
+    m->rows_sorted = h == 0;
+  }
+  return m.release();
+}
+
+Matrix* ell_from_arrays(std::int64_t n, std::int64_t band_count, const std::int64_t* col_1based,
+                        const double* values, const std::int64_t* row_entry_count,
+                        std::int64_t stored_nnz) {
+  rt::init();
+  require_int32_range(n, stored_nnz);
+  if (band_count < 0 || band_count > INT32_MAX)
+    throw Error(ErrorCode::InvalidArgument, "band count out of range");
+  std::unique_ptr<Matrix> m(new_matrix(SPMVTK_FORMAT_ELL, n, stored_nnz));
+  m->band_count = static_cast<std::int32_t>(band_count);
+  m->ld = round_up(n, 32);
+  const std::size_t slots = static_cast<std::size_t>(m->ld) * static_cast<std::size_t>(band_count);
+  m->val.reset(slots, "ELL values");
+  m->col.reset(slots, "ELL col_idx");
+  m->count.reset(n, "ELL row_entry_count");
+  cudaStream_t st = rt::stream();
+  if (slots) {
+    rt::check(cudaMemsetAsync(m->val.get(), 0, slots * sizeof(double), st), "ELL upload");
+    rt::check(cudaMemsetAsync(m->col.get(), 0, slots * sizeof(std::int32_t), st), "ELL upload");
+    DevArray<std::int32_t> compact;
+    upload_index(compact, col_1based, n * band_count, 8, 1, false, "ELL col upload");
+    DevArray<double> vcompact(static_cast<std::size_t>(n * band_count), "ELL value upload");
+    rt::copy_to_device(vcompact.get(), values, static_cast<std::size_t>(n * band_count) * 8);
+    rt::check(cudaMemcpy2DAsync(m->val.get(), m->ld * 8, vcompact.get(), n * 8, n * 8,
+                                band_count, cudaMemcpyDeviceToDevice, st),
+              "ELL upload");
+    rt::check(cudaMemcpy2DAsync(m->col.get(), m->ld * 4, compact.get(), n * 4, n * 4, band_count,
+                                cudaMemcpyDeviceToDevice, st),
+              "ELL upload");
+    if (count_bad_indices(m->col.get(), static_cast<std::int64_t>(slots), n))
+      throw Error(ErrorCode::Validation, "ELL column index out of range");
+  }
+  upload_index(m->count, row_entry_count, n, 8, 0, false, "ELL counts upload");
+  rt::sync();
+  return m.release();
+}
+
 std::uint64_t reference_ell_estimate(const Matrix& crs) {
   rt::Moments mo = crs_moments(crs);
   return static_cast<std::uint64_t>(crs.n) * mo.max * 16ull;
@@ -382,6 +444,14 @@ void spmv_device(const Matrix& m, spmvtk_kernel kernel, const double* x, double*
       if (m.ordering != 0)
         throw Error(ErrorCode::InvalidArgument,
                     "spmv_coo_row_outer requires the matching COO ordering");
+      if (!m.rows_sorted) {
+        // host-built COO tagged row-major whose rows are not sorted: the
+        // segmented kernel needs sorted rows, the reduction kernel does not
+        rt::check_launch(spmvtk_k_spmv_coo_col(m.n, m.nnz, m.row.get(), m.col.get(),
+                                               m.val.get(), x, y, st),
+                         "spmv coo-row (unsorted)");
+        return;
+      }
       rt::check_launch(spmvtk_k_spmv_coo_row(m.n, m.nnz, m.row.get(), m.col.get(), m.val.get(),
                                              x, y, st),
                        "spmv coo-row");

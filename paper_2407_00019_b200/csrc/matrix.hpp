@@ -19,6 +19,7 @@
 struct spmvtk_matrix {
   spmvtk_format format = SPMVTK_FORMAT_CRS;
   int ordering = -1;  // COO: 0 row-major, 1 column-major
+  bool rows_sorted = true;  // COO row-major tag verified (host-built COO may not be)
   int device = 0;
   std::int64_t n = 0;     // rows
   std::int64_t nnz = 0;   // stored entries; ELL: stored_nnz (real entries)
@@ -58,6 +59,17 @@ Matrix* crs_block_from_arrays(std::int64_t nrows, std::int64_t ncols, std::int64
                               std::int64_t nnz, const void* row_ptr, const void* col_idx,
                               const double* values, int index_width, int index_base,
                               bool on_device);
+
+// COO from caller arrays (ordering: 0 row-major, 1 column-major).  A
+// row-major tag is checked on the GPU; unsorted rows keep the tag but the
+// SpMV then uses the order-independent kernel.
+Matrix* coo_from_arrays(std::int64_t n, std::int64_t nnz, const void* rows, const void* cols,
+                        const double* values, int index_width, int index_base, int ordering);
+// Band-major ELL from reference-layout arrays (n*band_count values and
+// columns, row_entry_count[n]); re-pitched to the device leading dimension.
+Matrix* ell_from_arrays(std::int64_t n, std::int64_t band_count, const std::int64_t* col_1based,
+                        const double* values, const std::int64_t* row_entry_count,
+                        std::int64_t stored_nnz);
 
 // Reference ELL estimate (8+8 bytes per slot, convert.cpp:72-79).
 std::uint64_t reference_ell_estimate(const Matrix& crs);

@@ -1,0 +1,55 @@
+"""Drop-in evidence: the reference's OWN test programs, compiled unchanged
+from /root/reference/proj/tests against this repository's headers and
+libspmvtk.so (tests/dropin/Makefile, built by __graft_entry__.build()).
+
+* unit_tests_b200: the 7 doctest suites (test_formats/convert/spmv/stats/
+  autotune/ingest/capi.cpp) through tests/dropin/doctest.h.
+* acceptance_b200: acceptance.cpp; criteria 6-7 drive the reference CLI
+  (CLI11 is absent) and 8 needs SuiteSparse fixtures, so
+  1-5 and 9 are the ones that must pass.
+* unit_tests_ref (CPU): the same suites against the reference library,
+  proving the doctest stand-in reports them as the real doctest would.
+"""
+import os
+import re
+import subprocess
+
+import pytest
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+BUILD = os.path.join(HERE, "dropin", "_build")
+
+
+def _run(name, *args, timeout=900):
+    exe = os.path.join(BUILD, name)
+    if not os.path.exists(exe):
+        pytest.skip(f"{name} not built (needs /root/reference at build time)")
+    return subprocess.run([exe, *args], capture_output=True, text=True, timeout=timeout)
+
+
+def test_doctest_standin_passes_reference_suites_on_reference():
+    r = _run("unit_tests_ref")
+    assert r.returncode == 0, r.stdout[-3000:]
+    m = re.search(r"test cases: (\d+) \| (\d+) passed \| 0 failed", r.stdout)
+    assert m and int(m.group(1)) == 50, r.stdout[-2000:]
+
+
+@pytest.mark.gpu
+def test_reference_unit_suites_pass_on_b200_library(gpu):
+    r = _run("unit_tests_b200")
+    tail = r.stdout[-4000:]
+    assert r.returncode == 0, tail
+    m = re.search(r"test cases: (\d+) \| (\d+) passed \| 0 failed", r.stdout)
+    assert m and int(m.group(1)) == 50, tail
+
+
+@pytest.mark.gpu
+def test_reference_acceptance_on_b200_library(gpu, tmp_path):
+    r = _run("acceptance_b200", "/bin/false", str(tmp_path))
+    status = dict(re.findall(r"\[(PASS|FAIL|SKIP)\] criterion (\d+)", r.stdout)[::-1])
+    got = {}
+    for st, num in re.findall(r"\[(PASS|FAIL|SKIP)\] criterion (\d+)", r.stdout):
+        got[int(num)] = st
+    for c in (1, 2, 3, 4, 5, 9):
+        assert got.get(c) == "PASS", (c, r.stdout[-3000:])
+    del status
