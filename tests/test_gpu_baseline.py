@@ -1,0 +1,136 @@
+"""BASELINE.json workloads on the GPU (tests against the C oracle).
+
+* configs 1-3 at FULL size: every transform bit-exact, every SpMV within
+  1e-12 max-norm relative, D_mat as measured in SURVEY.md §0.15;
+* config 4 (power-law, n = 2^22): statistics, the ELL memory guard refusal
+  (≈160 GB in GPU layout), CRS/COO parity;
+* config 5 (D_mat sweep) at reduced n for oracle parity, and at full size
+  for D in {0, 1, 2}: size-independent properties (ELL and COO SpMV equal
+  CRS SpMV to 1e-12, band count = max row length, exported row counts = row
+  lengths, D_mat close to the target).
+"""
+import numpy as np
+import pytest
+
+from oracle.oracle import max_rel_error
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-12
+
+
+def host_arrays(sp, cfg, param, dparam=0.0, seed=2407):
+    h = sp.HostCrs(cfg, param, dparam, seed)
+    rp, ci, v = h.arrays(index_base=1)
+    return h, rp, ci, v
+
+
+def check_all(sp, port, h, n, rp, ci, v, x, ell=True):
+    m = h.upload()
+    assert m.describe().nnz == v.shape[0]
+    want = port.spmv_crs(n, rp, ci, v, x)
+    y, _ = m.spmv(x, sp.Kernel.CRS)
+    assert max_rel_error(y, want) <= TOL
+    # COO-row
+    r, c, vv = port.crs_to_coo_row(n, rp, ci, v)
+    coo = m.convert(sp.Format.COO_ROW)
+    assert np.array_equal(coo.array(sp.Array.ROW_IDX), r)
+    del r
+    assert max_rel_error(coo.spmv(x, sp.Kernel.COO_ROW_OUTER)[0], want) <= TOL
+    coo.free()
+    # CCS / COO-col
+    cp, ri, cv = port.crs_to_ccs(n, rp, ci, v)
+    ccs = m.convert(sp.Format.CCS)
+    assert np.array_equal(ccs.array(sp.Array.POINTER), cp)
+    assert np.array_equal(ccs.array(sp.Array.ROW_IDX), ri)
+    assert ccs.array(sp.Array.VALUES).tobytes() == cv.tobytes()
+    ccs.free()
+    del cp, ri, cv
+    cc = m.convert(sp.Format.COO_COL)
+    assert max_rel_error(cc.spmv(x, sp.Kernel.COO_COL_OUTER)[0], want) <= TOL
+    cc.free()
+    if ell:
+        bc, ev, ec, cnt = port.crs_to_ell(n, rp, ci, v)
+        e = m.convert(sp.Format.ELL)
+        assert e.describe().band_count == bc
+        assert e.array(sp.Array.VALUES).tobytes() == ev.tobytes()
+        assert np.array_equal(e.array(sp.Array.COL_IDX), ec)
+        assert np.array_equal(e.array(sp.Array.ROW_ENTRY_COUNT), cnt)
+        for k in (sp.Kernel.ELL_INNER, sp.Kernel.ELL_OUTER):
+            assert max_rel_error(e.spmv(x, k)[0], want) <= TOL
+        e.free()
+        del ev, ec
+        er = m.convert(sp.Format.ELL_ROWMAJOR)
+        assert max_rel_error(er.spmv(x, sp.Kernel.ELL_ROWMAJOR)[0], want) <= TOL
+        er.free()
+    return m
+
+
+@pytest.mark.parametrize("cfg,param,dmat", [(1, 256, 0.024980), (2, 1 << 20, None),
+                                            (3, 128, 0.072040)])
+def test_configs_1_to_3_full_size(gpu, port, cfg, param, dmat):
+    sp = gpu
+    h, rp, ci, v = host_arrays(sp, cfg, param)
+    n = h.n
+    x = sp.gen_vector(n, 7)
+    m = check_all(sp, port, h, n, rp, ci, v, x)
+    st = m.row_stats()
+    mu, sg, dm = port.row_stats(n, rp)
+    assert abs(st.d_mat - dm) <= 1e-12 * dm
+    if dmat is not None:
+        assert round(st.d_mat, 6) == dmat
+    if cfg == 3:
+        assert (n, h.nnz) == (2097152, 55742968)
+
+
+def test_config_4_power_law(gpu, port):
+    sp = gpu
+    h, rp, ci, v = host_arrays(sp, 4, 1 << 22)
+    n = h.n
+    m = h.upload()
+    st = m.row_stats()
+    assert st.max_row <= 4096 and 1.5 < st.d_mat < 2.2
+    mu, sg, dm = port.row_stats(n, rp)
+    assert abs(st.d_mat - dm) <= 1e-12 * dm
+    # ELL would be n * 4096 slots: the reference guard (2 GiB, the CLI
+    # default) refuses, as the reference does
+    with pytest.raises(sp.SpmvtkError) as e:
+        m.convert(sp.Format.ELL, max_bytes=2 << 30)
+    assert e.value.status == sp.Status.ERR_MEMORY_LIMIT
+    ref_est, dev_bytes = m.conversion_bytes(sp.Format.ELL)
+    assert ref_est == n * st.max_row * 16 and dev_bytes > 100e9
+    x = sp.gen_vector(n, 7)
+    want = port.spmv_crs(n, rp, ci, v, x)
+    assert max_rel_error(m.spmv(x, sp.Kernel.CRS)[0], want) <= TOL
+    coo = m.convert(sp.Format.COO_ROW)
+    assert max_rel_error(coo.spmv(x, sp.Kernel.COO_ROW_OUTER)[0], want) <= TOL
+
+
+@pytest.mark.parametrize("d", [0.0, 0.3, 1.0, 2.0])
+def test_config_5_reduced_parity(gpu, port, d):
+    sp = gpu
+    h, rp, ci, v = host_arrays(sp, 5, 1 << 15, d)
+    n = h.n
+    check_all(sp, port, h, n, rp, ci, v, sp.gen_vector(n, 3), ell=True)
+
+
+@pytest.mark.parametrize("d", [0.0, 1.0, 2.0])
+def test_config_5_full_size_properties(gpu, d):
+    sp = gpu
+    h = sp.HostCrs(5, 1 << 21, d)
+    n = h.n
+    m = h.upload()
+    st = m.row_stats()
+    assert abs(st.d_mat - d) <= 0.05 * max(d, 0.02) + 1e-12
+    assert abs(st.mu - 32.0) < 0.5
+    x = sp.gen_vector(n, 11)
+    y0, _ = m.spmv(x, sp.Kernel.CRS)
+    e = m.convert(sp.Format.ELL)
+    assert e.describe().band_count == st.max_row
+    cnt = e.array(sp.Array.ROW_ENTRY_COUNT)
+    rp = m.array(sp.Array.POINTER, 8, 0)
+    assert np.array_equal(cnt, np.diff(rp))
+    for k in (sp.Kernel.ELL_INNER, sp.Kernel.ELL_OUTER):
+        assert max_rel_error(e.spmv(x, k)[0], y0) <= TOL
+    e.free()
+    c = m.convert(sp.Format.COO_COL)
+    assert max_rel_error(c.spmv(x, sp.Kernel.COO_COL_OUTER)[0], y0) <= TOL
