@@ -49,15 +49,20 @@ int spmvtk_k_count_descents(const int32_t* key, int64_t len,
 int spmvtk_k_expand_ptr(const int32_t* ptr, int64_t n, int64_t nnz,
                         int32_t* out_idx, void* stream);
 
-/* CRS -> CCS Phase I (convert.cpp:24-53).  scratch must hold 2*(n+1) int32
- * plus spmvtk_k_scan_scratch_bytes(n+1) bytes (see below).  Row indices come
- * out ascending inside every column, exactly as the reference's cursor
- * scatter. */
-size_t spmvtk_k_ccs_scratch_bytes(int64_t n);
+/* CRS -> CCS Phase I (convert.cpp:24-53).  scratch: device buffer of
+ * spmvtk_k_ccs_scratch_bytes(n, nnz) bytes.  Row indices come out ascending
+ * inside every column, exactly as the reference's cursor scatter. */
+size_t spmvtk_k_ccs_scratch_bytes(int64_t n, int64_t nnz);
 int spmvtk_k_crs_to_ccs(int64_t n, int64_t nnz, const int32_t* irp,
                         const int32_t* icol, const double* val,
                         int32_t* col_ptr, int32_t* row_idx, double* out_val,
                         void* scratch, void* stream);
+/* Earlier formulation (column histogram + atomic cursors + per-column
+ * fix-up sort); same result, kept for comparison. */
+int spmvtk_k_crs_to_ccs_atomic(int64_t n, int64_t nnz, const int32_t* irp,
+                               const int32_t* icol, const double* val,
+                               int32_t* col_ptr, int32_t* row_idx, double* out_val,
+                               void* scratch, void* stream);
 
 /* Exclusive scan of n int32 counts into out[0..n] (out[n] = total). */
 size_t spmvtk_k_scan_scratch_bytes(int64_t n);

@@ -114,8 +114,7 @@ __global__ void __launch_bounds__(256) k_ccs_scatter(const int32_t* __restrict__
                                                      const double* __restrict__ val,
                                                      int64_t n, int rows_per_warp,
                                                      int32_t* cursor,
-                                                     int32_t* __restrict__ row_idx,
-                                                     double* __restrict__ out_val) {
+                                                     int4* __restrict__ rec) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t rb = warp * rows_per_warp;
@@ -136,12 +135,16 @@ __global__ void __launch_bounds__(256) k_ccs_scatter(const int32_t* __restrict__
     }
     int32_t row = resolve_segment(w, irp, re, lane, p, valid);
     if (valid) {
-      int32_t slot = atomicAdd(cursor + c, 1);
-      row_idx[slot] = row;
-      out_val[slot] = v;
+      // one 16-byte (row, value) record per entry: a single half-sector
+      // store instead of a 4-byte and an 8-byte store into two arrays (the
+      // random partial-sector writes dominated this kernel's DRAM traffic)
+      const int32_t slot = atomicAdd(cursor + c, 1);
+      rec[slot] = make_int4(row, 0, __double2loint(v), __double2hiint(v));
     }
   }
 }
+
+__device__ __forceinline__ double rec_val(const int4& r) { return __hiloint2double(r.w, r.z); }
 
 // Columns of length <= 32: one warp per column, bitonic sort in registers on
 // a packed key (row << 5 | source lane); values follow by shuffle.  Sorted
@@ -151,8 +154,9 @@ constexpr int kShortCol = 32;
 constexpr int kMediumCol = 4096;
 
 __global__ void __launch_bounds__(256) k_ccs_fix_short(const int32_t* __restrict__ col_ptr,
-                                                       int64_t n, int32_t* row_idx,
-                                                       double* vals, int32_t* queue,
+                                                       int64_t n, const int4* __restrict__ rec,
+                                                       int32_t* __restrict__ row_idx,
+                                                       double* __restrict__ vals, int32_t* queue,
                                                        int32_t* queue_len, bool packed_ok) {
   const int lane = threadIdx.x & 31;
   const int64_t warps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -160,16 +164,24 @@ __global__ void __launch_bounds__(256) k_ccs_fix_short(const int32_t* __restrict
        j += warps) {
     const int32_t a = __ldg(col_ptr + j), b = __ldg(col_ptr + j + 1);
     const int32_t len = b - a;
-    if (len <= 1) continue;
+    if (len <= 0) continue;
     if (len > kShortCol || !packed_ok) {
       if (lane == 0) queue[atomicAdd(queue_len, 1)] = static_cast<int32_t>(j);
       continue;
     }
-    int32_t r = lane < len ? row_idx[a + lane] : INT_MAX;
-    int32_t rn = __shfl_down_sync(kFull, r, 1);
-    bool desc = (lane + 1 < len) && rn < r;
-    if (!__any_sync(kFull, desc)) continue;
-    double v = lane < len ? vals[a + lane] : 0.0;
+    int4 rc = make_int4(INT_MAX, 0, 0, 0);
+    if (lane < len) rc = ld_stream4(rec + a + lane);
+    const int32_t r = rc.x;
+    const double v = rec_val(rc);
+    const int32_t rn = __shfl_down_sync(kFull, r, 1);
+    const bool desc = (lane + 1 < len) && rn < r;
+    if (!__any_sync(kFull, desc)) {
+      if (lane < len) {
+        row_idx[a + lane] = r;
+        vals[a + lane] = v;
+      }
+      continue;
+    }
     // rows < 2^26 so (row << 5 | lane) fits; padding lanes sort last
     uint32_t key = lane < len ? (static_cast<uint32_t>(r) << 5) | lane : 0xffffffffu;
 #pragma unroll
@@ -226,6 +238,7 @@ __device__ void block_bitonic(KeyPtr key, ValPtr val, int32_t len) {
 }
 
 __global__ void __launch_bounds__(512) k_ccs_fix_long(const int32_t* __restrict__ col_ptr,
+                                                      const int4* __restrict__ rec,
                                                       int32_t* row_idx, double* vals,
                                                       const int32_t* queue,
                                                       const int32_t* queue_len) {
@@ -237,8 +250,9 @@ __global__ void __launch_bounds__(512) k_ccs_fix_long(const int32_t* __restrict_
     const int32_t a = col_ptr[j], len = col_ptr[j + 1] - a;
     if (len <= kMediumCol) {
       for (int32_t t = threadIdx.x; t < len; t += blockDim.x) {
-        s_key[t] = row_idx[a + t];
-        s_val[t] = vals[a + t];
+        const int4 rc = rec[a + t];
+        s_key[t] = rc.x;
+        s_val[t] = rec_val(rc);
       }
       __syncthreads();
       block_bitonic(s_key, s_val, len);
@@ -247,10 +261,266 @@ __global__ void __launch_bounds__(512) k_ccs_fix_long(const int32_t* __restrict_
         vals[a + t] = s_val[t];
       }
     } else {
-      // very long column: same network directly in global memory (L2)
+      // very long column: unpack, then the same network in global memory (L2)
+      for (int32_t t = threadIdx.x; t < len; t += blockDim.x) {
+        const int4 rc = rec[a + t];
+        row_idx[a + t] = rc.x;
+        vals[a + t] = rec_val(rc);
+      }
+      __syncthreads();
       block_bitonic(row_idx + a, vals + a, len);
     }
     __syncthreads();
+  }
+}
+
+// ---- CRS -> CCS, bucketed (no global atomics) -------------------------------
+// Columns are grouped into NB buckets of CB = 2^shift consecutive columns
+// (~4k entries per bucket).  The CRS is split into kSlices row ranges of
+// equal entry counts (one per SM).
+//   1. k_bkt_count   slice-local bucket histograms in shared memory ->
+//                    T[b * kSlices + slice]
+//   2. exclusive scan of T (bucket-major) -> each (bucket, slice) owns a run
+//   3. k_bkt_scatter each slice re-reads its rows and appends 16-byte
+//                    records (col, row, value) to its runs with shared-memory
+//                    cursors: writes are kSlices x NB sequential streams that
+//                    fill whole sectors in L2
+//   4. k_bkt_sort    one CTA per bucket: counting sort by column in shared
+//                    memory, per-column sort by row (rows are distinct within
+//                    a column, so this restores the reference's order,
+//                    convert.cpp:43-51), col_ptr and the final row_idx /
+//                    values written fully coalesced.
+// Buckets too large for shared memory take a global-memory path.
+constexpr int kSlices = 3 * 148;  // 3 CTAs per SM (64 KB histograms)
+constexpr int kBktThreads = 512;
+constexpr int kBktItems = 12;
+constexpr int kBktCap = kBktThreads * kBktItems;  // records per bucket sorted in smem
+
+__global__ void k_slice_rows(const int32_t* __restrict__ irp, int64_t n, int32_t* slice_row) {
+  // slice s starts at the first row whose start >= s * nnz / kSlices
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s > kSlices) return;
+  const int64_t nnz = irp[n];
+  const int64_t target = nnz * s / kSlices;
+  int64_t lo = 0, hi = n;  // smallest r with irp[r] >= target
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (irp[mid] < target) lo = mid + 1;
+    else hi = mid;
+  }
+  slice_row[s] = static_cast<int32_t>(s == kSlices ? n : lo);
+}
+
+__global__ void __launch_bounds__(kBktThreads) k_bkt_count(const int32_t* __restrict__ irp,
+                                                           const int32_t* __restrict__ icol,
+                                                           const int32_t* __restrict__ slice_row,
+                                                           int shift, int nb, int32_t* T) {
+  extern __shared__ int32_t s_hist[];
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) s_hist[b] = 0;
+  __syncthreads();
+  const int32_t e0 = irp[slice_row[blockIdx.x]], e1 = irp[slice_row[blockIdx.x + 1]];
+  const int32_t step = static_cast<int32_t>(blockDim.x);
+  int32_t p = e0 + static_cast<int32_t>(threadIdx.x);
+  for (; p + 3 * step < e1; p += 4 * step) {  // 4 loads in flight per thread
+    const int32_t c0 = ld_stream(icol + p), c1 = ld_stream(icol + p + step);
+    const int32_t c2 = ld_stream(icol + p + 2 * step), c3 = ld_stream(icol + p + 3 * step);
+    atomicAdd(&s_hist[c0 >> shift], 1);
+    atomicAdd(&s_hist[c1 >> shift], 1);
+    atomicAdd(&s_hist[c2 >> shift], 1);
+    atomicAdd(&s_hist[c3 >> shift], 1);
+  }
+  for (; p < e1; p += step) atomicAdd(&s_hist[ld_stream(icol + p) >> shift], 1);
+  __syncthreads();
+  for (int b = threadIdx.x; b < nb; b += blockDim.x)
+    T[static_cast<int64_t>(b) * kSlices + blockIdx.x] = s_hist[b];
+}
+
+__global__ void __launch_bounds__(kBktThreads) k_bkt_scatter(
+    const int32_t* __restrict__ irp, const int32_t* __restrict__ icol,
+    const double* __restrict__ val, const int32_t* __restrict__ slice_row, int shift, int nb,
+    const int32_t* __restrict__ Toff, int4* __restrict__ rec) {
+  extern __shared__ int32_t s_cur[];
+  for (int b = threadIdx.x; b < nb; b += blockDim.x)
+    s_cur[b] = Toff[static_cast<int64_t>(b) * kSlices + blockIdx.x];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int64_t r_begin = slice_row[blockIdx.x], r_end = slice_row[blockIdx.x + 1];
+  constexpr int kRows = 64;  // rows per warp chunk
+  for (int64_t rb = r_begin + static_cast<int64_t>(warp) * kRows; rb < r_end;
+       rb += static_cast<int64_t>(nwarps) * kRows) {
+    const int64_t re = min(rb + kRows, r_end);
+    const int32_t e0 = __ldg(irp + rb), e1 = __ldg(irp + re);
+    SegWindow w;
+    w.r0 = rb;
+    w.load(irp, re, lane);
+    for (int32_t base = e0; base < e1; base += 32) {
+      const int32_t p = base + lane;
+      const bool valid = p < e1;
+      int32_t c = 0;
+      double v = 0.0;
+      if (valid) {
+        c = ld_stream(icol + p);
+        v = ld_stream(val + p);
+      }
+      const int32_t row = resolve_segment(w, irp, re, lane, p, valid);
+      if (valid) {
+        const int32_t slot = atomicAdd(&s_cur[c >> shift], 1);
+        rec[slot] = make_int4(c, row, __double2loint(v), __double2hiint(v));
+      }
+    }
+  }
+}
+
+// one CTA per bucket; dynamic smem: cnt[cb+1] | s_row[kBktCap] | s_val[kBktCap]
+__global__ void __launch_bounds__(kBktThreads) k_bkt_sort(
+    const int4* __restrict__ rec, const int32_t* __restrict__ Toff, int64_t n, int shift,
+    int nb, int32_t* __restrict__ col_ptr, int32_t* __restrict__ row_idx,
+    double* __restrict__ out_val, int32_t* big_queue, int32_t* big_len) {
+  extern __shared__ unsigned char s_raw[];
+  const int cb = 1 << shift;
+  int32_t* cnt = reinterpret_cast<int32_t*>(s_raw);  // cb + 1 entries
+  double* s_val = reinterpret_cast<double*>(s_raw + ((static_cast<size_t>(cb + 1) * 4 + 15) & ~15));
+  int32_t* s_row = reinterpret_cast<int32_t*>(s_val + kBktCap);
+  const int b = blockIdx.x;
+  const int32_t bs = Toff[static_cast<int64_t>(b) * kSlices];
+  const int32_t be = (b + 1 < nb) ? Toff[static_cast<int64_t>(b + 1) * kSlices]
+                                  : Toff[static_cast<int64_t>(nb) * kSlices];
+  const int64_t c0 = static_cast<int64_t>(b) << shift;
+  const int ncols = static_cast<int>(min(static_cast<int64_t>(cb), n - c0));
+  const int32_t len = be - bs;
+  const bool fits = len <= kBktCap;
+  for (int i = threadIdx.x; i <= cb; i += blockDim.x) cnt[i] = 0;
+  // records stay in registers between the count and the placement
+  int4 r[kBktItems];
+  if (fits) {
+#pragma unroll
+    for (int k = 0; k < kBktItems; ++k) {
+      const int32_t q = static_cast<int32_t>(threadIdx.x) + k * kBktThreads;
+      if (q < len) r[k] = ld_stream4(rec + bs + q);
+    }
+  }
+  __syncthreads();
+  if (fits) {
+#pragma unroll
+    for (int k = 0; k < kBktItems; ++k) {
+      const int32_t q = static_cast<int32_t>(threadIdx.x) + k * kBktThreads;
+      if (q < len) atomicAdd(&cnt[r[k].x - c0], 1);
+    }
+  } else {
+    for (int32_t q = threadIdx.x; q < len; q += blockDim.x)
+      atomicAdd(&cnt[__ldg(&rec[bs + q].x) - c0], 1);
+  }
+  __syncthreads();
+  // exclusive scan of cnt[0..cb) by warp 0 (cb <= 4096, a few passes)
+  if (threadIdx.x < 32) {
+    int32_t carry = 0;
+    for (int base = 0; base < cb; base += 32) {
+      const int i = base + threadIdx.x;
+      const int32_t v = cnt[i];
+      int32_t inc = v;
+      for (int d = 1; d < 32; d <<= 1) {
+        const int32_t t = __shfl_up_sync(kFull, inc, d);
+        if (threadIdx.x >= d) inc += t;
+      }
+      cnt[i] = carry + inc - v;
+      carry += __shfl_sync(kFull, inc, 31);
+    }
+    if (threadIdx.x == 0) cnt[cb] = carry;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < ncols; i += blockDim.x) col_ptr[c0 + i] = bs + cnt[i];
+  if (b == nb - 1 && threadIdx.x == 0) col_ptr[n] = be;
+  __syncthreads();  // cnt becomes a cursor array below
+  if (len > kBktCap) {
+    // oversized bucket: place into the final arrays with shared cursors,
+    // then sort every column of it in global memory (k_bkt_sort_big)
+    __syncthreads();
+    for (int32_t q = threadIdx.x; q < len; q += blockDim.x) {
+      const int4 r = rec[bs + q];
+      const int32_t slot = atomicAdd(&cnt[r.x - c0], 1);
+      row_idx[bs + slot] = r.y;
+      out_val[bs + slot] = rec_val(r);
+    }
+    if (threadIdx.x == 0) big_queue[atomicAdd(big_len, 1)] = b;
+    return;
+  }
+  // place by column (shared cursors; order inside a column arbitrary)
+#pragma unroll
+  for (int k = 0; k < kBktItems; ++k) {
+    const int32_t q = static_cast<int32_t>(threadIdx.x) + k * kBktThreads;
+    if (q < len) {
+      const int32_t slot = atomicAdd(&cnt[r[k].x - c0], 1);
+      s_row[slot] = r[k].y;
+      s_val[slot] = rec_val(r[k]);
+    }
+  }
+  __syncthreads();
+  // cnt[i] now holds the END of column i; column i spans [end(i-1), end(i)).
+  // One warp per column: register bitonic sort on (row << 5 | lane) for
+  // columns of <= 32 entries (already-sorted columns skip the network), a
+  // lane-0 insertion sort beyond; results go straight to the output arrays.
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int i = warp; i < ncols; i += blockDim.x >> 5) {
+    const int32_t a = i ? cnt[i - 1] : 0, e = cnt[i], cl = e - a;
+    if (cl <= 32 && n < (int64_t(1) << 27)) {  // (row << 5 | lane) must fit 32 bits
+      int32_t rr = lane < cl ? s_row[a + lane] : INT_MAX;
+      double v = lane < cl ? s_val[a + lane] : 0.0;
+      const int32_t rn = __shfl_down_sync(kFull, rr, 1);
+      if (__any_sync(kFull, lane + 1 < cl && rn < rr)) {
+        uint32_t key = lane < cl ? (static_cast<uint32_t>(rr) << 5) | lane : 0xffffffffu;
+#pragma unroll
+        for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+          for (int d = size >> 1; d > 0; d >>= 1) {
+            const uint32_t other = __shfl_xor_sync(kFull, key, d);
+            const bool up = (lane & size) == 0, lower = (lane & d) == 0;
+            key = (lower == up) ? min(key, other) : max(key, other);
+          }
+        }
+        v = __shfl_sync(kFull, v, static_cast<int>(key & 31u));
+        rr = static_cast<int32_t>(key >> 5);
+      }
+      if (lane < cl) {
+        row_idx[bs + a + lane] = rr;
+        st_stream(out_val + bs + a + lane, v);
+      }
+    } else {
+      if (lane == 0)
+        for (int32_t k = a + 1; k < e; ++k) {  // insertion sort on row
+          const int32_t key = s_row[k];
+          const double v = s_val[k];
+          int32_t j = k - 1;
+          while (j >= a && s_row[j] > key) {
+            s_row[j + 1] = s_row[j];
+            s_val[j + 1] = s_val[j];
+            --j;
+          }
+          s_row[j + 1] = key;
+          s_val[j + 1] = v;
+        }
+      __syncwarp();
+      for (int32_t q = a + lane; q < e; q += 32) {
+        row_idx[bs + q] = s_row[q];
+        st_stream(out_val + bs + q, s_val[q]);
+      }
+    }
+  }
+}
+
+// columns of oversized buckets: sort each column segment in place
+__global__ void __launch_bounds__(512) k_bkt_sort_big(const int32_t* __restrict__ col_ptr,
+                                                      int64_t n, int shift, int32_t* row_idx,
+                                                      double* vals, const int32_t* big_queue,
+                                                      const int32_t* big_len) {
+  const int32_t count = *big_len;
+  for (int32_t q = blockIdx.x; q < count; q += gridDim.x) {
+    const int64_t c0 = static_cast<int64_t>(big_queue[q]) << shift;
+    const int64_t c1 = min(c0 + (int64_t(1) << shift), n);
+    for (int64_t c = c0; c < c1; ++c) {
+      const int32_t a = col_ptr[c], len = col_ptr[c + 1] - a;
+      if (len > 1) block_bitonic(row_idx + a, vals + a, len);
+      __syncthreads();
+    }
   }
 }
 
@@ -399,21 +669,96 @@ int spmvtk_k_expand_ptr(const int32_t* ptr, int64_t n, int64_t nnz, int32_t* out
   SPMVTK_LAUNCH_RETURN();
 }
 
-size_t spmvtk_k_ccs_scratch_bytes(int64_t n) {
-  // count[n+1], cursor[n+1], queue[n], queue_len[1], scan tiles
-  size_t ints = static_cast<size_t>(n + 1) * 2 + static_cast<size_t>(n) + 4;
-  return ints * sizeof(int32_t) + spmvtk_k_scan_scratch_bytes(n + 1) + 256;
+namespace {
+struct BucketPlan {
+  int shift;
+  int nb;
+};
+BucketPlan bucket_plan(int64_t n, int64_t nnz) {
+  const double per_col = n > 0 ? static_cast<double>(nnz) / static_cast<double>(n) : 1.0;
+  int shift = 0;
+  while (shift < 12 && static_cast<double>(int64_t(1) << (shift + 1)) * per_col <= 4096.0) ++shift;
+  while (((n + (int64_t(1) << shift) - 1) >> shift) > 32768) ++shift;
+  return {shift, static_cast<int>((n + (int64_t(1) << shift) - 1) >> shift)};
+}
+size_t align256(size_t v) { return (v + 255) & ~static_cast<size_t>(255); }
+}  // namespace
+
+size_t spmvtk_k_ccs_scratch_bytes(int64_t n, int64_t nnz) {
+  const BucketPlan bp = bucket_plan(n, nnz);
+  const size_t t = static_cast<size_t>(bp.nb) * kSlices + 1;
+  const size_t bucketed = align256(static_cast<size_t>(nnz) * 16) + align256((kSlices + 1) * 4) +
+                          2 * align256(t * 4) + align256((static_cast<size_t>(bp.nb) + 1) * 4) +
+                          align256(spmvtk_k_scan_scratch_bytes(static_cast<int64_t>(t))) + 1024;
+  // the atomic-cursor variant needs count/cursor/queue over n columns
+  const size_t atomic = static_cast<size_t>(nnz) * 16 +
+                        (static_cast<size_t>(n + 1) * 3 + 4) * sizeof(int32_t) +
+                        spmvtk_k_scan_scratch_bytes(n + 1) + 1024;
+  return bucketed > atomic ? bucketed : atomic;
 }
 
 int spmvtk_k_crs_to_ccs(int64_t n, int64_t nnz, const int32_t* irp, const int32_t* icol,
                         const double* val, int32_t* col_ptr, int32_t* row_idx,
                         double* out_val, void* scratch, void* stream) {
   cudaStream_t s = as_stream(stream);
-  int32_t* count = static_cast<int32_t*>(scratch);
+  if (n <= 0) SPMVTK_LAUNCH_RETURN();
+  if (nnz == 0) {
+    cudaMemsetAsync(col_ptr, 0, static_cast<size_t>(n + 1) * sizeof(int32_t), s);
+    SPMVTK_LAUNCH_RETURN();
+  }
+  const BucketPlan bp = bucket_plan(n, nnz);
+  const int64_t tlen = static_cast<int64_t>(bp.nb) * kSlices;
+  uintptr_t cur = (reinterpret_cast<uintptr_t>(scratch) + 255) & ~static_cast<uintptr_t>(255);
+  auto take = [&](size_t bytes) {
+    void* p = reinterpret_cast<void*>(cur);
+    cur += align256(bytes);
+    return p;
+  };
+  int4* rec = static_cast<int4*>(take(static_cast<size_t>(nnz) * 16));
+  int32_t* slice_row = static_cast<int32_t*>(take((kSlices + 1) * 4));
+  int32_t* T = static_cast<int32_t*>(take(static_cast<size_t>(tlen + 1) * 4));
+  int32_t* Toff = static_cast<int32_t*>(take(static_cast<size_t>(tlen + 1) * 4));
+  int32_t* big = static_cast<int32_t*>(take((static_cast<size_t>(bp.nb) + 1) * 4));
+  int32_t* big_len = big + bp.nb;
+  void* scan_scratch = take(spmvtk_k_scan_scratch_bytes(tlen + 1));
+
+  const size_t hist_smem = static_cast<size_t>(bp.nb) * 4;
+  const int cb = 1 << bp.shift;
+  const size_t sort_smem = ((static_cast<size_t>(cb + 1) * 4 + 15) & ~static_cast<size_t>(15)) +
+                           static_cast<size_t>(kBktCap) * 12;
+  static bool attrs = false;
+  if (!attrs) {
+    cudaFuncSetAttribute(k_bkt_count, cudaFuncAttributeMaxDynamicSharedMemorySize, 32768 * 4);
+    cudaFuncSetAttribute(k_bkt_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, 32768 * 4);
+    cudaFuncSetAttribute(k_bkt_sort, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(((4097 * 4 + 15) & ~15) + kBktCap * 12));
+    attrs = true;
+  }
+  cudaMemsetAsync(big_len, 0, sizeof(int32_t), s);
+  k_slice_rows<<<(kSlices + 128) / 128, 128, 0, s>>>(irp, n, slice_row);
+  k_bkt_count<<<kSlices, kBktThreads, hist_smem, s>>>(irp, icol, slice_row, bp.shift, bp.nb, T);
+  int rc = spmvtk_k_exclusive_scan(T, Toff, tlen, scan_scratch, stream);
+  if (rc) return rc;
+  k_bkt_scatter<<<kSlices, kBktThreads, hist_smem, s>>>(irp, icol, val, slice_row, bp.shift,
+                                                         bp.nb, Toff, rec);
+  k_bkt_sort<<<bp.nb, kBktThreads, sort_smem, s>>>(rec, Toff, n, bp.shift, bp.nb, col_ptr,
+                                                    row_idx, out_val, big, big_len);
+  k_bkt_sort_big<<<kSMs, 512, 0, s>>>(col_ptr, n, bp.shift, row_idx, out_val, big, big_len);
+  SPMVTK_LAUNCH_RETURN();
+}
+
+// the previous, atomic-cursor formulation (kept for comparison / tuning)
+int spmvtk_k_crs_to_ccs_atomic(int64_t n, int64_t nnz, const int32_t* irp, const int32_t* icol,
+                               const double* val, int32_t* col_ptr, int32_t* row_idx,
+                               double* out_val, void* scratch, void* stream) {
+  cudaStream_t s = as_stream(stream);
+  uintptr_t base = (reinterpret_cast<uintptr_t>(scratch) + 255) & ~static_cast<uintptr_t>(255);
+  int4* rec = reinterpret_cast<int4*>(base);
+  int32_t* count = reinterpret_cast<int32_t*>(rec + nnz);
   int32_t* cursor = count + (n + 1);
   int32_t* queue = cursor + (n + 1);
   int32_t* queue_len = queue + n;
-  // keep the scan scratch 16-byte aligned
+  // keep the scan scratch aligned
   uintptr_t sp = reinterpret_cast<uintptr_t>(queue_len + 4);
   sp = (sp + 255) & ~static_cast<uintptr_t>(255);
   void* scan_scratch = reinterpret_cast<void*>(sp);
@@ -430,11 +775,11 @@ int spmvtk_k_crs_to_ccs(int64_t n, int64_t nnz, const int32_t* irp, const int32_
   int64_t warps = (n + rpw - 1) / rpw;
   int64_t blocks = (warps * 32 + 255) / 256;
   k_ccs_scatter<<<static_cast<unsigned>(blocks), 256, 0, s>>>(irp, icol, val, n, rpw, cursor,
-                                                             row_idx, out_val);
-  k_ccs_fix_short<<<grid_for(n * 32, 256, 16), 256, 0, s>>>(col_ptr, n, row_idx, out_val,
+                                                             rec);
+  k_ccs_fix_short<<<grid_for(n * 32, 256, 16), 256, 0, s>>>(col_ptr, n, rec, row_idx, out_val,
                                                             queue, queue_len,
                                                             n < (int64_t(1) << 26));
-  k_ccs_fix_long<<<kSMs * 2, 512, 0, s>>>(col_ptr, row_idx, out_val, queue, queue_len);
+  k_ccs_fix_long<<<kSMs * 2, 512, 0, s>>>(col_ptr, rec, row_idx, out_val, queue, queue_len);
   SPMVTK_LAUNCH_RETURN();
 }
 

@@ -297,7 +297,7 @@ Matrix* convert(const Matrix& a, spmvtk_format to, std::uint64_t max_bytes) {
       m->row.reset(nnz, "CCS row_idx");
       m->val.reset(nnz, "CCS values");
       DevArray<std::int32_t> colptr(n + 1, "CCS col_ptr");
-      DevArray<unsigned char> scratch(spmvtk_k_ccs_scratch_bytes(n), "CCS scratch");
+      DevArray<unsigned char> scratch(spmvtk_k_ccs_scratch_bytes(n, nnz), "CCS scratch");
       cudaStream_t st = rt::stream();
       rt::check_launch(spmvtk_k_crs_to_ccs(n, nnz, a.ptr.get(), a.col.get(), a.val.get(),
                                            colptr.get(), m->row.get(), m->val.get(),
@@ -368,7 +368,7 @@ double transform_kernel_seconds(const Matrix& a, spmvtk_format to, int repeats) 
   DevArray<unsigned char> scratch;
   if (to == SPMVTK_FORMAT_CCS || to == SPMVTK_FORMAT_COO_COL) {
     colptr.reset(n + 1, "CCS col_ptr");
-    scratch.reset(spmvtk_k_ccs_scratch_bytes(n), "CCS scratch");
+    scratch.reset(spmvtk_k_ccs_scratch_bytes(n, nnz), "CCS scratch");
   }
   DevArray<unsigned long long> acc(3, "row statistics");
   auto once = [&] {
