@@ -347,6 +347,39 @@ def impl_ours(args):
     assert np.allclose(yn, y.cpu().numpy(), rtol=1e-12, atol=0), "e2e result mismatch"
     del ych
 
+    # ---- the same kernels on config 3 (27-point stencil: x gathers are local,
+    # so SpMV meets the HBM roofline there; config 2's random columns make
+    # every kernel L2-sector-bound)
+    also = {}
+    if not args.no_also and args.config != 3:
+        m3 = sp.HostCrs(3, 128, 0.0, args.seed).upload()
+        d3 = m3.describe()
+        nz3 = m3.row_stats().max_row
+        x3 = torch.from_numpy(sp.gen_vector(d3.n, args.seed + 1)).cuda()
+        y3 = torch.empty(d3.n, dtype=torch.float64, device="cuda")
+        e3 = m3.convert(sp.Format.ELL)
+        c3 = m3.convert(sp.Format.COO_ROW)
+        tab3 = {}
+        for name, h3, k3 in (("crs", m3, sp.Kernel.CRS), ("ell-inner", e3, sp.Kernel.ELL_INNER),
+                             ("coo-row", c3, sp.Kernel.COO_ROW_OUTER)):
+            for _ in range(5):
+                h3.spmv_device(k3, x3.data_ptr(), y3.data_ptr())
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(200):
+                h3.spmv_device(k3, x3.data_ptr(), y3.data_ptr())
+            e1.record()
+            torch.cuda.synchronize()
+            t3 = e0.elapsed_time(e1) / 200 * 1e-3
+            b3 = spmv_bytes(name, d3.n, d3.nnz, nz3)
+            tab3[name] = {"gbs": b3 / t3 / 1e9, "gflops": 2 * d3.nnz / t3 / 1e9,
+                          "us": t3 * 1e6, "frac": b3 / t3 / 1e9 / peak}
+        also["config3"] = {"n": d3.n, "nnz": d3.nnz, "formats": tab3,
+                           "ell_transform_kernel_ms":
+                               m3.transform_kernel_seconds(sp.Format.ELL, 3) * 1e3}
+        for h3 in (e3, c3, m3):
+            h3.free()
+
     # ---- CPU baseline: the reference itself on this host (bounded sample)
     cpu = None
     if not args.no_cpu_baseline:
@@ -384,6 +417,7 @@ def impl_ours(args):
         "clocks": clk.summary(),
         "formats": table, "transforms": transforms,
         "at": {"variant": "ell-inner", "sp": sp_, "tt": tt_, "r": r_},
+        "also": also,
         "cpu_baseline": cpu,
     }
     print(json.dumps(line))
@@ -400,6 +434,7 @@ def main():
     ap.add_argument("--param", type=int, default=None)
     ap.add_argument("--seed", type=int, default=2407)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-also", action="store_true", help="skip the config-3 side table")
     ap.add_argument("--force-dist", action="store_true",
                     help="use the row-block/NCCL path even on one rank (testing)")
     args = ap.parse_args()

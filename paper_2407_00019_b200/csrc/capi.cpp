@@ -77,6 +77,51 @@ dev::Matrix* upload(const gen::HostCrs& h) {
                               h.base, false);
 }
 
+thread_local double t_scratch = 0.0;
+
+bool pinned(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+struct SideStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t ev[8] = {};
+  SideStream() {
+    rt::check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "side stream");
+    for (auto& e : ev) rt::check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+  }
+};
+
+double pipelined_spmv(const dev::Matrix& m, spmvtk_kernel kernel, const double* dx, double* dy,
+                      double* y_host) {
+  thread_local SideStream side;
+  constexpr int kChunks = 4;
+  const std::int64_t n = m.n;
+  std::int64_t step = (n + kChunks - 1) / kChunks;
+  step = (step + 63) / 64 * 64;
+  cudaStream_t st = rt::stream();
+  rt::EventTimer timer;
+  timer.start();
+  int k = 0;
+  for (std::int64_t r0 = 0; r0 < n; r0 += step, ++k) {
+    const std::int64_t r1 = std::min(n, r0 + step);
+    dev::spmv_device_rows(m, kernel, dx, dy, r0, r1);
+    rt::check(cudaEventRecord(side.ev[k], st), "event");
+    rt::check(cudaStreamWaitEvent(side.s, side.ev[k], 0), "event wait");
+    rt::check(cudaMemcpyAsync(y_host + r0, dy + r0, static_cast<std::size_t>(r1 - r0) * 8,
+                              cudaMemcpyDeviceToHost, side.s),
+              "D2H copy");
+  }
+  const double secs = timer.stop_seconds();
+  rt::check(cudaStreamSynchronize(side.s), "side stream synchronize");
+  return secs;
+}
+
 bool valid_format(int f) { return f >= SPMVTK_FORMAT_CRS && f <= SPMVTK_FORMAT_ELL_ROWMAJOR; }
 bool valid_kernel(int k) { return k >= SPMVTK_KERNEL_CRS && k <= SPMVTK_KERNEL_ELL_ROWMAJOR; }
 
@@ -240,6 +285,14 @@ spmvtk_status spmvtk_spmv(const spmvtk_matrix* m, spmvtk_kernel kernel, const do
     const std::size_t nc = static_cast<std::size_t>(m->ncols);
     rt::DevArray<double> dx(std::max<std::size_t>(nc, 1), "x"), dy(std::max<std::size_t>(n, 1), "y");
     rt::copy_to_device(dx.get(), x, nc * sizeof(double));
+    if (n >= 16384 && dev::spmv_row_splittable(*m, kernel) && pinned(y)) {
+      // pipelined: the D2H copy of each finished row block overlaps the
+      // SpMV of the next (x must be complete before any row: gathers are
+      // arbitrary), on a side stream ordered by events
+      *(elapsed_seconds ? elapsed_seconds : &t_scratch) =
+          pipelined_spmv(*m, kernel, dx.get(), dy.get(), y);
+      return;
+    }
     rt::EventTimer timer;
     timer.start();
     dev::spmv_device(*m, kernel, dx.get(), dy.get());

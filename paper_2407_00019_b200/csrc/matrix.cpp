@@ -422,6 +422,48 @@ double transform_kernel_seconds(const Matrix& a, spmvtk_format to, int repeats) 
   return samples[samples.size() / 2];
 }
 
+bool spmv_row_splittable(const Matrix& m, spmvtk_kernel kernel) {
+  return (kernel == SPMVTK_KERNEL_CRS && m.format == SPMVTK_FORMAT_CRS) ||
+         (kernel == SPMVTK_KERNEL_ELL_INNER && m.format == SPMVTK_FORMAT_ELL) ||
+         (kernel == SPMVTK_KERNEL_ELL_ROWMAJOR && m.format == SPMVTK_FORMAT_ELL_ROWMAJOR);
+}
+
+void spmv_device_rows(const Matrix& m, spmvtk_kernel kernel, const double* x, double* y,
+                      std::int64_t r0, std::int64_t r1) {
+  if (!spmv_row_splittable(m, kernel) || r0 < 0 || r1 > m.n || r0 > r1 || (r0 & 63))
+    throw Error(ErrorCode::InvalidArgument, "row-range SpMV not available for this kernel");
+  const std::int64_t rows = r1 - r0;
+  if (rows == 0) return;
+  cudaStream_t st = rt::stream();
+  switch (kernel) {
+    case SPMVTK_KERNEL_CRS: {
+      rt::Moments mo = crs_moments(m);
+      const double mean = m.n > 0 ? static_cast<double>(mo.sum) / static_cast<double>(m.n) : 0;
+      DevArray<std::int32_t> long_rows;
+      if (mo.max > 4096) long_rows.reset(rows + 1, "CRS long-row queue");
+      // row pointers stay absolute, so offsetting irp and y is enough
+      rt::check_launch(spmvtk_k_spmv_crs(rows, m.ptr.get() + r0, m.col.get(), m.val.get(), x,
+                                         y + r0, mean,
+                                         static_cast<std::int32_t>(std::min<std::uint64_t>(mo.max, INT32_MAX)),
+                                         long_rows.get(), st),
+                       "spmv crs");
+      return;
+    }
+    case SPMVTK_KERNEL_ELL_INNER:
+      rt::check_launch(spmvtk_k_spmv_ell_cm(rows, m.band_count, m.ld, m.val.get() + r0,
+                                            m.col.get() + r0, x, y + r0, st),
+                       "spmv ell-inner");
+      return;
+    default:
+      rt::check_launch(spmvtk_k_spmv_ell_rm(rows, m.band_count,
+                                            m.val.get() + r0 * static_cast<std::int64_t>(m.band_count),
+                                            m.col.get() + r0 * static_cast<std::int64_t>(m.band_count),
+                                            x, y + r0, st),
+                       "spmv ell-row");
+      return;
+  }
+}
+
 void spmv_device(const Matrix& m, spmvtk_kernel kernel, const double* x, double* y) {
   cudaStream_t st = rt::stream();
   switch (kernel) {

@@ -87,6 +87,15 @@ double transform_kernel_seconds(const Matrix& crs, spmvtk_format to, int repeats
 // COO ordering), with the reference's messages (capi.cpp:230-252).
 void spmv_device(const Matrix& m, spmvtk_kernel kernel, const double* x, double* y);
 
+// True when `kernel` on `m` can be launched on row sub-ranges (CRS, ELL
+// band-major inner, row-major ELL): rows are independent and y is written
+// once per row, so a host pipeline can copy finished row blocks back while
+// later ones compute.
+bool spmv_row_splittable(const Matrix& m, spmvtk_kernel kernel);
+// y[r0:r1) = A[r0:r1, :] x (r0 a multiple of 64).
+void spmv_device_rows(const Matrix& m, spmvtk_kernel kernel, const double* x, double* y,
+                      std::int64_t r0, std::int64_t r1);
+
 // One array to host memory in the requested index width / base.
 std::int64_t copy_array(const Matrix& m, spmvtk_array which, void* dst, std::int64_t capacity,
                         int index_width, int index_base);

@@ -433,6 +433,24 @@ def test_validation_rejects_bad_arrays(gpu):
     assert e.value.status == sp.Status.ERR_DATA
 
 
+def test_pipelined_host_spmv_matches_device(gpu):
+    """spmvtk_spmv with pinned host buffers takes the row-chunked pipeline
+    (D2H of finished rows overlaps the SpMV of the next); results must be
+    bitwise those of the pageable (single-shot) call and the device call."""
+    import torch
+    sp = gpu
+    m = sp.HostCrs(2, 1 << 16).upload()
+    n = m.describe().n
+    x = sp.gen_vector(n, 5)
+    xp = torch.from_numpy(x.copy()).pin_memory()
+    for h, k in ((m, sp.Kernel.CRS), (m.convert(sp.Format.ELL), sp.Kernel.ELL_INNER),
+                 (m.convert(sp.Format.ELL_ROWMAJOR), sp.Kernel.ELL_ROWMAJOR)):
+        yp = torch.empty(n, dtype=torch.float64).pin_memory()
+        h.spmv(xp.numpy(), k, 1, out=yp.numpy())
+        y_pageable, _ = h.spmv(x, k)
+        assert yp.numpy().tobytes() == y_pageable.tobytes(), k
+
+
 def test_row_block_shards_single_gpu(gpu, port):
     """Row-block shards (the multi-GPU layout) run on one GPU: per-shard
     SpMV assembled == full SpMV (1e-12), and each shard's ELL equals the
