@@ -95,6 +95,9 @@ int spmvtk_k_spmv_crs(int64_t n, const int32_t* irp, const int32_t* icol,
                       const double* val, const double* x, double* y,
                       double mean_row, int32_t max_row, int32_t* long_rows,
                       void* stream);
+/* Row length above which spmvtk_k_spmv_crs hands a row to the block-per-row
+ * pass (long_rows must then be non-NULL when max_row exceeds it). */
+int64_t spmvtk_k_crs_long_limit(double mean_row);
 /* spmv_coo_row_outer (spmv.cpp:79-101,111-115): row-sorted triplets,
  * deterministic segmented reduction, no atomics. */
 int spmvtk_k_spmv_coo_row(int64_t n, int64_t nnz, const int32_t* row,

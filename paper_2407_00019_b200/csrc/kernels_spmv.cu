@@ -263,6 +263,61 @@ __global__ void __launch_bounds__(256) k_spmv_tile(int64_t n, Rows rows,
   if (t < rows_here) y[r0 + t] = acc + s_extra[t];
 }
 
+// ---- vector CRS with 128-bit loads ----------------------------------------
+// Same sub-warp-per-row scheme, but each lane consumes aligned entry PAIRS
+// (one double2 value load + one int2 index load): half the load
+// instructions and L1 wavefronts per entry of the scalar kernel.  A row
+// starting at an odd position has its first entry taken by lane 0 alone.
+template <int W, int U>
+__global__ void __launch_bounds__(256) k_spmv_vec2(int64_t n, const int32_t* __restrict__ irp,
+                                                   const int32_t* __restrict__ col,
+                                                   const double* __restrict__ val,
+                                                   const double* __restrict__ x,
+                                                   double* __restrict__ y, int64_t long_limit,
+                                                   int32_t* long_rows) {
+  const int lane = threadIdx.x & (W - 1);
+  const unsigned mask = subwarp_mask(W);
+  const int64_t nsub = (static_cast<int64_t>(gridDim.x) * blockDim.x) / W;
+  for (int64_t r = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / W; r < n;
+       r += nsub) {
+    const int32_t a = __ldg(irp + r), b = __ldg(irp + r + 1);
+    if (b - a > long_limit) {
+      if (lane == 0) long_rows[1 + atomicAdd(long_rows, 1)] = static_cast<int32_t>(r);
+      continue;
+    }
+    double acc = 0.0;
+    int32_t a2 = a;
+    if ((a & 1) && a < b) {  // odd start: peel one entry
+      if (lane == 0) acc = ld_stream(val + a) * ld_x(x + ld_stream(col + a));
+      a2 = a + 1;
+    }
+    for (int32_t p = a2 + 2 * lane; p < b; p += 2 * W * U) {
+      double2 v[U];
+      int2 c[U];
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        const int32_t q = p + 2 * W * j;
+        if (q + 1 < b) {
+          v[j] = ld_stream2(reinterpret_cast<const double2*>(val + q));
+          c[j] = ld_stream2(reinterpret_cast<const int2*>(col + q));
+        } else if (q < b) {
+          v[j].x = ld_stream(val + q);
+          c[j].x = ld_stream(col + q);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        const int32_t q = p + 2 * W * j;
+        if (q < b) acc = fma(v[j].x, ld_x(x + c[j].x), acc);
+        if (q + 1 < b) acc = fma(v[j].y, ld_x(x + c[j].y), acc);
+      }
+    }
+#pragma unroll
+    for (int o = W / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(mask, acc, o, W);
+    if (lane == 0) y[r] = acc;
+  }
+}
+
 // block per long row (queue filled by k_spmv_vec / k_spmv_multi)
 __global__ void __launch_bounds__(256) k_spmv_crs_long(const int32_t* __restrict__ irp,
                                                        const int32_t* __restrict__ col,
@@ -553,12 +608,28 @@ void dispatch_vec(double mean, int64_t max_row, int64_t n, Rows rows, const int3
   if (v < 0) {
     // measured on B200 (tools/tune_crs.py, profiles/r01_tune_crs.txt): few
     // lanes per row (more rows in flight) win unless the rows are skewed
-    if (static_cast<double>(max_row) > 8.0 * mean + 8.0) v = 0;  // W=16
-    else if (mean <= 6.0) v = 12;                              // W=4
-    else if (mean <= 40.0) v = 11;                             // W=8
-    else v = 0;                                                // W=16
+    // (profiles/r01_tune_crs2.txt): 128-bit pair loads from 6 entries/row up
+    const bool crs = std::is_same_v<Rows, CrsRows>;
+    if (static_cast<double>(max_row) > 8.0 * mean + 8.0) v = crs ? 16 : 0;  // W=8 pairs
+    else if (mean <= 6.0) v = 12;                                         // W=4 scalar
+    else if (mean <= 30.0) v = crs ? 18 : 11;                             // W=4 pairs
+    else if (mean <= 64.0) v = crs ? 16 : 0;                              // W=8 pairs
+    else v = crs ? 17 : 13;                                               // W=16 pairs
   }
   switch (v) {
+    case 15: case 16: case 17: case 18: case 19:
+      if constexpr (std::is_same_v<Rows, CrsRows>) {
+        const int64_t W = v == 15 ? 4 : v == 16 ? 8 : v == 17 ? 16 : v == 18 ? 4 : 8;
+        const int blocks = grid_for(n * W, 256, 8);
+        if (v == 15) k_spmv_vec2<4, 2><<<blocks, 256, 0, s>>>(n, rows.irp, col, val, x, y, long_limit, long_rows);
+        if (v == 16) k_spmv_vec2<8, 1><<<blocks, 256, 0, s>>>(n, rows.irp, col, val, x, y, long_limit, long_rows);
+        if (v == 17) k_spmv_vec2<16, 1><<<blocks, 256, 0, s>>>(n, rows.irp, col, val, x, y, long_limit, long_rows);
+        if (v == 18) k_spmv_vec2<4, 1><<<blocks, 256, 0, s>>>(n, rows.irp, col, val, x, y, long_limit, long_rows);
+        if (v == 19) k_spmv_vec2<8, 2><<<blocks, 256, 0, s>>>(n, rows.irp, col, val, x, y, long_limit, long_rows);
+      } else {
+        launch_vec<8, 2>(n, rows, col, val, x, y, long_limit, long_rows, s);
+      }
+      break;
     case 11: launch_vec<8, 2>(n, rows, col, val, x, y, long_limit, long_rows, s); break;
     case 12: launch_vec<4, 2>(n, rows, col, val, x, y, long_limit, long_rows, s); break;
     case 13: launch_vec<32, 4>(n, rows, col, val, x, y, long_limit, long_rows, s); break;
@@ -590,7 +661,7 @@ int spmvtk_k_spmv_crs(int64_t n, const int32_t* irp, const int32_t* icol, const 
                       int32_t* long_rows, void* stream) {
   cudaStream_t s = as_stream(stream);
   if (n <= 0) SPMVTK_LAUNCH_RETURN();
-  const int64_t long_limit = 4096;
+  const int64_t long_limit = spmvtk_k_crs_long_limit(mean_row);
   const bool use_long = long_rows != nullptr && max_row > long_limit;
   if (use_long) cudaMemsetAsync(long_rows, 0, sizeof(int32_t), s);
   dispatch_vec(mean_row, max_row, n, CrsRows{irp}, icol, val, x, y,
@@ -663,6 +734,13 @@ int spmvtk_k_spmv_ell_rm(int64_t n, int32_t nz, const double* val, const int32_t
   dispatch_vec(static_cast<double>(nz), nz, n, EllRowMajorRows{nz}, col, val, x, y, INT64_MAX,
                nullptr, s);
   SPMVTK_LAUNCH_RETURN();
+}
+
+int64_t spmvtk_k_crs_long_limit(double mean_row) {
+  // rows this much longer than average would serialise one sub-warp: they go
+  // to the block-per-row pass (power-law rows, BASELINE config 4)
+  const int64_t m = static_cast<int64_t>(mean_row + 0.999);
+  return std::max<int64_t>(256, std::min<int64_t>(4096, 32 * m));
 }
 
 int spmvtk_k_tune(const char* key, int value) {

@@ -440,7 +440,8 @@ void spmv_device_rows(const Matrix& m, spmvtk_kernel kernel, const double* x, do
       rt::Moments mo = crs_moments(m);
       const double mean = m.n > 0 ? static_cast<double>(mo.sum) / static_cast<double>(m.n) : 0;
       DevArray<std::int32_t> long_rows;
-      if (mo.max > 4096) long_rows.reset(rows + 1, "CRS long-row queue");
+      if (static_cast<std::int64_t>(mo.max) > spmvtk_k_crs_long_limit(mean))
+        long_rows.reset(rows + 1, "CRS long-row queue");
       // row pointers stay absolute, so offsetting irp and y is enough
       rt::check_launch(spmvtk_k_spmv_crs(rows, m.ptr.get() + r0, m.col.get(), m.val.get(), x,
                                          y + r0, mean,
@@ -473,7 +474,8 @@ void spmv_device(const Matrix& m, spmvtk_kernel kernel, const double* x, double*
       rt::Moments mo = crs_moments(m);
       const double mean = m.n > 0 ? static_cast<double>(mo.sum) / static_cast<double>(m.n) : 0;
       DevArray<std::int32_t> long_rows;
-      if (mo.max > 4096) long_rows.reset(m.n + 1, "CRS long-row queue");
+      if (static_cast<std::int64_t>(mo.max) > spmvtk_k_crs_long_limit(mean))
+        long_rows.reset(m.n + 1, "CRS long-row queue");
       rt::check_launch(spmvtk_k_spmv_crs(m.n, m.ptr.get(), m.col.get(), m.val.get(), x, y, mean,
                                          static_cast<std::int32_t>(std::min<std::uint64_t>(mo.max, INT32_MAX)),
                                          long_rows.get(), st),
