@@ -182,6 +182,13 @@ spmvtk_status spmvtk_matrix_from_crs_block(int64_t nrows, int64_t ncols, int64_t
                                            const double* values, int index_width, int index_base,
                                            int on_device, spmvtk_matrix** out);
 
+/* Any handle -> new canonical CRS handle (columns ascending in each row),
+ * on the device: the inverse conversions coo_to_crs / ell_to_crs
+ * (convert.cpp:117-183), CCS -> CRS, and canonicalize for a CRS handle.
+ * Duplicate positions in COO / ELL input -> SPMVTK_ERR_DATA
+ * "duplicate (row, col) pair (r, c)". */
+spmvtk_status spmvtk_matrix_to_crs(const spmvtk_matrix* m, spmvtk_matrix** out);
+
 typedef struct spmvtk_matrix_desc {
   int32_t format;       /* spmvtk_format */
   int32_t ordering;     /* COO: 0 row-major, 1 column-major; else -1 */

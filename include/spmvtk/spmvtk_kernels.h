@@ -85,6 +85,29 @@ int spmvtk_k_crs_to_ell_rm(int64_t n, int32_t nz, const int32_t* irp,
                            double* out_val, int32_t* out_col,
                            int32_t* out_count, int64_t pad_base, void* stream);
 
+/* ---- inverse conversions -> canonical CRS (convert.cpp:117-183,
+ * formats.cpp:228-244).  dup (device uint64) receives the smallest
+ * duplicate position as (row << 32 | col), all-ones when there is none.
+ * scratch: spmvtk_k_canon_scratch_bytes(n) bytes. ------------------------*/
+size_t spmvtk_k_canon_scratch_bytes(int64_t nseg);
+/* Sorts key[ptr[s]..ptr[s+1]) (payload val) for every segment s; keys must
+ * be < key_bound. */
+int spmvtk_k_sort_segments(const int32_t* ptr, int64_t nseg, int64_t key_bound,
+                           int32_t* key, double* val, unsigned long long* dup,
+                           void* scratch, void* stream);
+/* ELL (slot(k,i) = k*stride_k + i*stride_i: band-major stride_k = ld,
+ * stride_i = 1; row-major stride_k = 1, stride_i = nz) -> canonical CRS;
+ * padding dropped by row_entry_count. */
+int spmvtk_k_ell_to_crs(int64_t n, int64_t ncols, int64_t stride_k, int64_t stride_i,
+                        const double* eval, const int32_t* ecol, const int32_t* cnt,
+                        int32_t* irp, int32_t* icol, double* val,
+                        unsigned long long* dup, void* scratch, void* stream);
+/* COO triplets in any order -> canonical CRS. */
+int spmvtk_k_coo_to_crs(int64_t n, int64_t ncols, int64_t nnz, const int32_t* row,
+                        const int32_t* col, const double* v, int32_t* irp,
+                        int32_t* icol, double* val, unsigned long long* dup,
+                        void* scratch, void* stream);
+
 /* ---- SpMV (y is overwritten; every row of y is written) ----------------*/
 
 /* spmv_crs (spmv.cpp:64-75).  max_row = longest row (from row stats); rows

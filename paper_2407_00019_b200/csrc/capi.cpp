@@ -211,8 +211,15 @@ spmvtk_status spmvtk_write_matrix_market(const spmvtk_matrix* m, const char* pat
     need(path);
     std::vector<std::int64_t> r, c;
     std::vector<double> v;
-    triplets(*m, r, c, v);
-    mm::write(m->n, std::move(r), std::move(c), std::move(v), m->format != SPMVTK_FORMAT_CRS, path);
+    if (m->format == SPMVTK_FORMAT_CRS) {
+      triplets(*m, r, c, v);
+    } else {
+      // non-CRS handles are written through their canonical CRS, rebuilt on
+      // the device (duplicates refused there, as coo_to_crs does)
+      std::unique_ptr<dev::Matrix> crs(dev::to_crs(*m));
+      triplets(*crs, r, c, v);
+    }
+    mm::write(m->n, std::move(r), std::move(c), std::move(v), false, path);
   });
 }
 
@@ -433,6 +440,14 @@ spmvtk_status spmvtk_matrix_from_crs_block(int64_t nrows, int64_t ncols, int64_t
     need(out, "null output");
     *out = dev::crs_block_from_arrays(nrows, ncols, row_offset, nnz, row_ptr, col_idx, values,
                                       index_width, index_base, on_device != 0);
+  });
+}
+
+spmvtk_status spmvtk_matrix_to_crs(const spmvtk_matrix* m, spmvtk_matrix** out) {
+  return guarded([&] {
+    need(m);
+    need(out, "null output");
+    *out = dev::to_crs(*m);
   });
 }
 

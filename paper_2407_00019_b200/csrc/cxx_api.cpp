@@ -80,6 +80,15 @@ EllMatrix down_ell(const dev::Matrix& h) {
   return e;
 }
 
+CrsMatrix down_crs(const dev::Matrix& h) {
+  CrsMatrix out;
+  out.n = h.n;
+  out.values = vals_of(h);
+  out.col_idx = idx_of(h, SPMVTK_ARRAY_COL_IDX);
+  out.row_ptr = idx_of(h, SPMVTK_ARRAY_POINTER);
+  return out;
+}
+
 void require_dim(index_t n, std::size_t len) {
   if (static_cast<index_t>(len) != n)
     throw Error(ErrorCode::InvalidArgument, "vector length " + std::to_string(len) +
@@ -323,6 +332,11 @@ CrsMatrix crs_from_dense(const DenseMatrix& d, double drop_tol) {
 }
 
 CrsMatrix canonicalize(const CrsMatrix& m) {
+  if (m.n > 0 && m.nnz() > 0) {  // per-row sort on the device
+    Handle h = up(m);
+    Handle c(dev::to_crs(*h));
+    return down_crs(*c);
+  }
   CrsMatrix out = m;
   std::vector<std::size_t> idx;
   for (index_t i = 1; i <= m.n; ++i) {
@@ -413,21 +427,23 @@ EllMatrix crs_to_ell(const CrsMatrix& m, std::uint64_t max_bytes) {
   return down_ell(*e);
 }
 
+// convert.cpp:158-164 -- on the device: row histogram, scan, cursor scatter,
+// per-row sort on the column, duplicate refusal
 CrsMatrix coo_to_crs(const CooMatrix& m) {
-  return canonical_from_triplets(m.n, m.row_idx, m.col_idx, m.values);
+  if (m.n <= 0) return canonical_from_triplets(m.n, m.row_idx, m.col_idx, m.values);
+  Handle h(dev::coo_from_arrays(m.n, m.nnz(), m.row_idx.data(), m.col_idx.data(),
+                                m.values.data(), 8, 1,
+                                m.ordering == CooOrdering::ColMajor ? 1 : 0));
+  Handle c(dev::to_crs(*h));
+  return down_crs(*c);
 }
 
+// convert.cpp:166-183 -- padding dropped by row_entry_count, on the device
 CrsMatrix ell_to_crs(const EllMatrix& m) {
-  std::vector<index_t> rows, cols;
-  std::vector<double> vals;
-  for (index_t i = 1; i <= m.n; ++i)
-    for (index_t k = 1; k <= m.row_entry_count[i - 1]; ++k) {
-      const std::size_t s = EllMatrix::slot(m.n, k, i);
-      rows.push_back(i);
-      cols.push_back(m.col_idx[s]);
-      vals.push_back(m.values[s]);
-    }
-  return canonical_from_triplets(m.n, std::move(rows), std::move(cols), std::move(vals));
+  if (m.n <= 0) return canonical_from_triplets(m.n, {}, {}, {});
+  Handle h = up(m);
+  Handle c(dev::to_crs(*h));
+  return down_crs(*c);
 }
 
 // ---------------------------------------------------------------- spmv

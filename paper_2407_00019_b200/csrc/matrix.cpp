@@ -356,6 +356,67 @@ Matrix* convert(const Matrix& a, spmvtk_format to, std::uint64_t max_bytes) {
   throw Error(ErrorCode::InvalidArgument, "unknown target format");
 }
 
+Matrix* to_crs(const Matrix& a) {
+  rt::init();
+  const std::int64_t n = a.n, nnz = a.nnz;
+  std::unique_ptr<Matrix> m(derived(a, SPMVTK_FORMAT_CRS, nnz));
+  m->ptr.reset(n + 1, "CRS row_ptr");
+  m->col.reset(nnz, "CRS col_idx");
+  m->val.reset(nnz, "CRS values");
+  cudaStream_t st = rt::stream();
+  DevArray<unsigned long long> dup(1, "duplicate flag");
+  DevArray<unsigned char> scratch(spmvtk_k_canon_scratch_bytes(n) +
+                                      spmvtk_k_ccs_scratch_bytes(a.ncols, nnz),
+                                  "canonical CRS scratch");
+  bool check_dup = true;
+  switch (a.format) {
+    case SPMVTK_FORMAT_CRS:
+      rt::check(cudaMemcpyAsync(m->ptr.get(), a.ptr.get(), a.ptr.bytes(), cudaMemcpyDeviceToDevice, st), "copy");
+      rt::check(cudaMemcpyAsync(m->col.get(), a.col.get(), a.col.bytes(), cudaMemcpyDeviceToDevice, st), "copy");
+      rt::check(cudaMemcpyAsync(m->val.get(), a.val.get(), a.val.bytes(), cudaMemcpyDeviceToDevice, st), "copy");
+      rt::check_launch(spmvtk_k_sort_segments(m->ptr.get(), n, a.ncols, m->col.get(), m->val.get(),
+                                              dup.get(), scratch.get(), st),
+                       "canonicalize");
+      check_dup = false;  // canonicalize() does not refuse (formats.cpp:228-244)
+      break;
+    case SPMVTK_FORMAT_CCS:
+      // the CCS of A is the CRS of A^T: transposing it back yields the CRS of
+      // A with rows visited in order, i.e. columns ascending in every row
+      rt::check_launch(spmvtk_k_crs_to_ccs(n, nnz, a.ptr.get(), a.row.get(), a.val.get(),
+                                           m->ptr.get(), m->col.get(), m->val.get(),
+                                           scratch.get(), st),
+                       "CCS->CRS");
+      check_dup = false;
+      break;
+    case SPMVTK_FORMAT_COO_ROW:
+    case SPMVTK_FORMAT_COO_COL:
+      rt::check_launch(spmvtk_k_coo_to_crs(n, a.ncols, nnz, a.row.get(), a.col.get(),
+                                           a.val.get(), m->ptr.get(), m->col.get(),
+                                           m->val.get(), dup.get(), scratch.get(), st),
+                       "COO->CRS");
+      break;
+    case SPMVTK_FORMAT_ELL:
+    case SPMVTK_FORMAT_ELL_ROWMAJOR: {
+      const bool cm = a.format == SPMVTK_FORMAT_ELL;
+      rt::check_launch(spmvtk_k_ell_to_crs(n, a.ncols, cm ? a.ld : 1, cm ? 1 : a.band_count,
+                                           a.val.get(), a.col.get(), a.count.get(),
+                                           m->ptr.get(), m->col.get(), m->val.get(), dup.get(),
+                                           scratch.get(), st),
+                       "ELL->CRS");
+      break;
+    }
+  }
+  if (check_dup) {
+    unsigned long long d = 0;
+    rt::copy_to_host(&d, dup.get(), sizeof(d));
+    if (d != ~0ull)
+      throw Error(ErrorCode::Validation,
+                  "duplicate (row, col) pair (" + std::to_string((d >> 32) + 1 + a.row_offset) +
+                      ", " + std::to_string((d & 0xffffffffull) + 1) + ")");
+  }
+  return m.release();
+}
+
 double transform_kernel_seconds(const Matrix& a, spmvtk_format to, int repeats) {
   if (a.format != SPMVTK_FORMAT_CRS)
     throw Error(ErrorCode::InvalidArgument, "operation requires a CRS handle");

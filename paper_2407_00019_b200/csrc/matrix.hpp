@@ -78,6 +78,11 @@ std::uint64_t device_bytes_for(const Matrix& crs, spmvtk_format to);
 // Conversions of a CRS handle (the guard applies to the ELL formats).
 Matrix* convert(const Matrix& crs, spmvtk_format to, std::uint64_t max_bytes);
 
+// Any handle -> canonical CRS on the device (columns ascending inside rows);
+// duplicate positions refused with the reference's message
+// (convert.cpp:119-154).  For a CRS handle this is canonicalize().
+Matrix* to_crs(const Matrix& m);
+
 // Median device time of the transform's kernels alone (outputs and scratch
 // preallocated; the ELL variants include the band-count reduction).
 double transform_kernel_seconds(const Matrix& crs, spmvtk_format to, int repeats);

@@ -161,6 +161,7 @@ SIGNATURES = {
     "spmvtk_matrix_from_crs": (C.c_int, [_i64, _i64, _P, _P, _P, C.c_int, C.c_int, C.c_int, _PP]),
     "spmvtk_matrix_from_crs_block": (C.c_int, [_i64, _i64, _i64, _i64, _P, _P, _P, C.c_int,
                                                C.c_int, C.c_int, _PP]),
+    "spmvtk_matrix_to_crs": (C.c_int, [_P, _PP]),
     "spmvtk_matrix_describe": (C.c_int, [_P, C.POINTER(MatrixDesc)]),
     "spmvtk_matrix_copy_array": (C.c_int, [_P, C.c_int, _P, _i64, C.c_int, C.c_int,
                                            C.POINTER(_i64)]),
@@ -366,6 +367,10 @@ class Matrix:
     # ---- operations ---------------------------------------------------
     def convert(self, to: Format, max_bytes: int = 0) -> "Matrix":
         return Matrix._make(self._lib.spmvtk_matrix_convert, self._h, int(to), max_bytes)
+
+    def to_crs(self) -> "Matrix":
+        """Canonical CRS rebuilt on the device (inverse conversions)."""
+        return Matrix._make(self._lib.spmvtk_matrix_to_crs, self._h)
 
     def spmv(self, x, kernel: Kernel = Kernel.CRS, lanes: int = 1,
              out: np.ndarray | None = None) -> tuple[np.ndarray, float]:

@@ -500,3 +500,33 @@ def test_row_block_shards_single_gpu(gpu, port):
         sp.Matrix.from_crs_block(2, 10, 0, np.array([0, 1, 2]), np.array([3, 9]),
                                  np.ones(2)).convert(sp.Format.CCS)
     assert e.value.status == sp.Status.ERR_USAGE
+
+
+def test_inverse_conversions_on_device(gpu, golden):
+    """coo_to_crs / ell_to_crs / CCS->CRS / canonicalize on the GPU give the
+    canonical CRS (test_convert.cpp:146-177, acceptance.cpp:90-115)."""
+    sp = gpu
+    for i in range(int(golden["count"][0])):
+        n, rp, ci, v, x, p = _case(golden, i)
+        m = upload(sp, n, rp, ci, v)
+        # canonical reference: sort columns inside each row
+        crp = np.asarray(rp, np.int64)
+        order = np.concatenate([np.argsort(ci[crp[r] - 1:crp[r + 1] - 1], kind="stable") +
+                                crp[r] - 1 for r in range(n)]).astype(np.int64) \
+            if v.size else np.zeros(0, np.int64)
+        want_c, want_v = ci[order], v[order]
+        for h in (m, m.convert(sp.Format.CCS), m.convert(sp.Format.COO_ROW),
+                  m.convert(sp.Format.COO_COL), m.convert(sp.Format.ELL),
+                  m.convert(sp.Format.ELL_ROWMAJOR)):
+            c = h.to_crs()
+            assert c.format == sp.Format.CRS
+            np.testing.assert_array_equal(c.array(sp.Array.POINTER), crp)
+            np.testing.assert_array_equal(c.array(sp.Array.COL_IDX), want_c)
+            assert c.array(sp.Array.VALUES).tobytes() == want_v.tobytes()
+    # duplicates are refused with the reference message
+    dup = sp.Matrix.from_crs(2, np.array([0, 2, 3]), np.array([1, 1, 0]), np.ones(3))
+    coo = dup.convert(sp.Format.COO_ROW)
+    with pytest.raises(sp.SpmvtkError) as e:
+        coo.to_crs()
+    assert e.value.status == sp.Status.ERR_DATA and "duplicate (row, col) pair (1, 2)" in \
+        e.value.message

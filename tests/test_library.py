@@ -28,9 +28,28 @@ def test_library_exports_every_declared_symbol(sp):
     for header in ("spmvtk.h", "spmvtk_kernels.h"):
         missing = declared_functions(header) - syms
         assert not missing, f"{header}: not exported: {sorted(missing)}"
-    # nothing but the C ABI leaks out of the shared object
-    assert all(s.startswith("spmvtk_") for s in syms), sorted(s for s in syms
-                                                               if not s.startswith("spmvtk_"))
+    # nothing but the C ABI and the reference's C++ entry points (namespace
+    # spmvtk, never the internal spmvtk::{dev,rt,at,gen,mm}) leaks out
+    internal = ("_ZN6spmvtk3dev", "_ZN6spmvtk2rt", "_ZN6spmvtk2at", "_ZN6spmvtk3gen",
+                "_ZN6spmvtk2mm")
+    leaked = [s for s in syms if not (s.startswith("spmvtk_") or s.startswith("_ZN6spmvtk"))
+              or s.startswith(internal)]
+    assert not leaked, sorted(leaked)
+
+
+def test_cxx_entry_points_exported(sp):
+    """The reference's C++ API (convert/spmv/stats/autotune/ingest.hpp) is
+    exported by libspmvtk.so for drop-in linking (tests/dropin/)."""
+    out = subprocess.run(["nm", "-DC", "--defined-only", sp.LIB_PATH], capture_output=True,
+                         text=True, check=True).stdout
+    for name in ("spmvtk::crs_to_ell(", "spmvtk::crs_to_ccs(", "spmvtk::crs_to_coo_row(",
+                 "spmvtk::crs_to_coo_col(", "spmvtk::spmv_crs(", "spmvtk::spmv_ell_inner(",
+                 "spmvtk::spmv_ell_outer(", "spmvtk::spmv_coo_row_outer(",
+                 "spmvtk::spmv_coo_col_outer(", "spmvtk::row_stats(", "spmvtk::compute_metrics(",
+                 "spmvtk::find_d_star(", "spmvtk::offline_profile(", "spmvtk::online_select(",
+                 "spmvtk::measure_spmv(", "spmvtk::measure_transformation(",
+                 "spmvtk::coo_to_crs(", "spmvtk::ell_to_crs(", "spmvtk::read_profile("):
+        assert name in out, name
 
 
 def test_reference_abi_is_complete(sp):
