@@ -726,14 +726,14 @@ int spmvtk_k_crs_to_ccs(int64_t n, int64_t nnz, const int32_t* irp, const int32_
   const int cb = 1 << bp.shift;
   const size_t sort_smem = ((static_cast<size_t>(cb + 1) * 4 + 15) & ~static_cast<size_t>(15)) +
                            static_cast<size_t>(kBktCap) * 12;
-  static bool attrs = false;
-  if (!attrs) {
+  static const bool attrs = [] {  // thread-safe one-time setup
     cudaFuncSetAttribute(k_bkt_count, cudaFuncAttributeMaxDynamicSharedMemorySize, 32768 * 4);
     cudaFuncSetAttribute(k_bkt_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, 32768 * 4);
     cudaFuncSetAttribute(k_bkt_sort, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(((4097 * 4 + 15) & ~15) + kBktCap * 12));
-    attrs = true;
-  }
+    return true;
+  }();
+  (void)attrs;
   cudaMemsetAsync(big_len, 0, sizeof(int32_t), s);
   k_slice_rows<<<(kSlices + 128) / 128, 128, 0, s>>>(irp, n, slice_row);
   k_bkt_count<<<kSlices, kBktThreads, hist_smem, s>>>(irp, icol, slice_row, bp.shift, bp.nb, T);

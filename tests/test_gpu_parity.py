@@ -433,6 +433,38 @@ def test_validation_rejects_bad_arrays(gpu):
     assert e.value.status == sp.Status.ERR_DATA
 
 
+def test_coo_row_kernels_both_variants(gpu, port):
+    """The 4-entries-per-lane COO-row kernel (default) and the scalar one agree
+    with the oracle on matrices with empty rows, long rows spanning many warp
+    chunks and row runs crossing lane / group boundaries."""
+    sp = gpu
+    lib = sp.load_library()
+    rng = np.random.default_rng(99)
+    try:
+        for it in range(6):
+            n = int(rng.integers(1, 5000))
+            lens = rng.integers(0, 12, size=n)
+            lens[rng.random(n) < 0.3] = 0
+            if it % 2:
+                lens[rng.integers(0, n, size=2)] = rng.integers(2000, 9000, size=2)
+            lens = np.minimum(lens, n)
+            rows = [np.sort(rng.choice(n, size=int(l), replace=False)) for l in lens]
+            ci = (np.concatenate(rows) if rows else np.zeros(0)).astype(np.int64) + 1
+            rp = np.concatenate([[1], 1 + np.cumsum(lens)]).astype(np.int64)
+            v = rng.standard_normal(ci.shape[0])
+            x = rng.uniform(-1, 1, n)
+            want = port.spmv_crs(n, rp, ci, v, x)
+            coo = upload(sp, n, rp, ci, v).convert(sp.Format.COO_ROW)
+            ys = []
+            for variant in (1, 0):
+                lib.spmvtk_k_tune(b"coo_variant", variant)
+                y, _ = coo.spmv(x, sp.Kernel.COO_ROW_OUTER)
+                assert max_rel_error(y, want) <= TOL, (it, variant)
+                ys.append(y)
+    finally:
+        lib.spmvtk_k_tune(b"coo_variant", 1)
+
+
 def test_pipelined_host_spmv_matches_device(gpu):
     """spmvtk_spmv with pinned host buffers takes the row-chunked pipeline
     (D2H of finished rows overlaps the SpMV of the next); results must be
