@@ -268,8 +268,8 @@ __global__ void __launch_bounds__(256) k_spmv_tile(int64_t n, Rows rows,
 // (one double2 value load + one int2 index load): half the load
 // instructions and L1 wavefronts per entry of the scalar kernel.  A row
 // starting at an odd position has its first entry taken by lane 0 alone.
-template <int W, int U>
-__global__ void __launch_bounds__(256) k_spmv_vec2(int64_t n, const int32_t* __restrict__ irp,
+template <int W, int U, typename Rows>
+__global__ void __launch_bounds__(256) k_spmv_vec2(int64_t n, Rows rows,
                                                    const int32_t* __restrict__ col,
                                                    const double* __restrict__ val,
                                                    const double* __restrict__ x,
@@ -280,23 +280,24 @@ __global__ void __launch_bounds__(256) k_spmv_vec2(int64_t n, const int32_t* __r
   const int64_t nsub = (static_cast<int64_t>(gridDim.x) * blockDim.x) / W;
   for (int64_t r = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / W; r < n;
        r += nsub) {
-    const int32_t a = __ldg(irp + r), b = __ldg(irp + r + 1);
+    int64_t a, b;
+    rows.get(r, a, b);
     if (b - a > long_limit) {
       if (lane == 0) long_rows[1 + atomicAdd(long_rows, 1)] = static_cast<int32_t>(r);
       continue;
     }
     double acc = 0.0;
-    int32_t a2 = a;
+    int64_t a2 = a;
     if ((a & 1) && a < b) {  // odd start: peel one entry
       if (lane == 0) acc = ld_stream(val + a) * ld_x(x + ld_stream(col + a));
       a2 = a + 1;
     }
-    for (int32_t p = a2 + 2 * lane; p < b; p += 2 * W * U) {
+    for (int64_t p = a2 + 2 * lane; p < b; p += 2 * W * U) {
       double2 v[U];
       int2 c[U];
 #pragma unroll
       for (int j = 0; j < U; ++j) {
-        const int32_t q = p + 2 * W * j;
+        const int64_t q = p + 2 * W * j;
         if (q + 1 < b) {
           v[j] = ld_stream2(reinterpret_cast<const double2*>(val + q));
           c[j] = ld_stream2(reinterpret_cast<const int2*>(col + q));
@@ -307,7 +308,7 @@ __global__ void __launch_bounds__(256) k_spmv_vec2(int64_t n, const int32_t* __r
       }
 #pragma unroll
       for (int j = 0; j < U; ++j) {
-        const int32_t q = p + 2 * W * j;
+        const int64_t q = p + 2 * W * j;
         if (q < b) acc = fma(v[j].x, ld_x(x + c[j].x), acc);
         if (q + 1 < b) acc = fma(v[j].y, ld_x(x + c[j].y), acc);
       }
@@ -704,6 +705,7 @@ __global__ void k_reduce_partials(int64_t n, int32_t splits, const double* __res
 
 int g_l2_hint = 0;  // L2 evict_first (matrix) / evict_last (x) policies
 int g_coo_variant = 1;  // 1: 4 entries per lane (k_spmv_coo_row4), 0: scalar
+int g_rm_variant = -1;  // row-major ELL variant override (tuning)
 
 template <int W, int U, typename Rows>
 void launch_vec(int64_t n, Rows rows, const int32_t* col, const double* val, const double* x,
@@ -732,27 +734,29 @@ void dispatch_vec(double mean, int64_t max_row, int64_t n, Rows rows, const int3
     // measured on B200 (tools/tune_crs.py, profiles/r01_tune_crs.txt): few
     // lanes per row (more rows in flight) win unless the rows are skewed
     // (profiles/r01_tune_crs2.txt): 128-bit pair loads from 6 entries/row up
-    const bool crs = std::is_same_v<Rows, CrsRows>;
-    if (static_cast<double>(max_row) > 8.0 * mean + 8.0) v = crs ? 16 : 0;  // W=8 pairs
-    else if (mean <= 6.0) v = 12;                                         // W=4 scalar
-    else if (mean <= 30.0) v = crs ? 18 : 11;                             // W=4 pairs
-    else if (mean <= 64.0) v = crs ? 16 : 0;                              // W=8 pairs
-    else v = crs ? 17 : 13;                                               // W=16 pairs
+    if (static_cast<double>(max_row) > 8.0 * mean + 8.0) v = 16;  // W=8 pairs
+    else if (mean <= 6.0) v = 12;                               // W=4 scalar
+    else if (mean <= 30.0) v = 18;                              // W=4 pairs
+    else if (mean <= 64.0) v = 16;                              // W=8 pairs
+    else v = 17;                                                // W=16 pairs
+    if constexpr (!std::is_same_v<Rows, CrsRows>) {
+      // row-major ELL: with an odd band count every other row starts at an
+      // odd slot, so pair loads lose to 4 scalar lanes (profiles/r01_tune_rm.txt)
+      if (max_row % 2 == 1 && max_row <= 40) v = 12;
+      if (g_rm_variant >= 0) v = g_rm_variant;
+    }
   }
   switch (v) {
-    case 15: case 16: case 17: case 18: case 19:
-      if constexpr (std::is_same_v<Rows, CrsRows>) {
-        const int64_t W = v == 15 ? 4 : v == 16 ? 8 : v == 17 ? 16 : v == 18 ? 4 : 8;
-        const int blocks = grid_for(n * W, 256, 8);
-        if (v == 15) k_spmv_vec2<4, 2><<<blocks, 256, 0, s>>>(n, rows.irp, col, val, x, y, long_limit, long_rows);
-        if (v == 16) k_spmv_vec2<8, 1><<<blocks, 256, 0, s>>>(n, rows.irp, col, val, x, y, long_limit, long_rows);
-        if (v == 17) k_spmv_vec2<16, 1><<<blocks, 256, 0, s>>>(n, rows.irp, col, val, x, y, long_limit, long_rows);
-        if (v == 18) k_spmv_vec2<4, 1><<<blocks, 256, 0, s>>>(n, rows.irp, col, val, x, y, long_limit, long_rows);
-        if (v == 19) k_spmv_vec2<8, 2><<<blocks, 256, 0, s>>>(n, rows.irp, col, val, x, y, long_limit, long_rows);
-      } else {
-        launch_vec<8, 2>(n, rows, col, val, x, y, long_limit, long_rows, s);
-      }
+    case 15: case 16: case 17: case 18: case 19: {
+      const int64_t W = v == 15 ? 4 : v == 16 ? 8 : v == 17 ? 16 : v == 18 ? 4 : 8;
+      const int blocks = grid_for(n * W, 256, 8);
+      if (v == 15) k_spmv_vec2<4, 2, Rows><<<blocks, 256, 0, s>>>(n, rows, col, val, x, y, long_limit, long_rows);
+      if (v == 16) k_spmv_vec2<8, 1, Rows><<<blocks, 256, 0, s>>>(n, rows, col, val, x, y, long_limit, long_rows);
+      if (v == 17) k_spmv_vec2<16, 1, Rows><<<blocks, 256, 0, s>>>(n, rows, col, val, x, y, long_limit, long_rows);
+      if (v == 18) k_spmv_vec2<4, 1, Rows><<<blocks, 256, 0, s>>>(n, rows, col, val, x, y, long_limit, long_rows);
+      if (v == 19) k_spmv_vec2<8, 2, Rows><<<blocks, 256, 0, s>>>(n, rows, col, val, x, y, long_limit, long_rows);
       break;
+    }
     case 11: launch_vec<8, 2>(n, rows, col, val, x, y, long_limit, long_rows, s); break;
     case 12: launch_vec<4, 2>(n, rows, col, val, x, y, long_limit, long_rows, s); break;
     case 13: launch_vec<32, 4>(n, rows, col, val, x, y, long_limit, long_rows, s); break;
@@ -884,6 +888,10 @@ int spmvtk_k_tune(const char* key, int value) {
   }
   if (key && std::string(key) == "coo_variant") {
     g_coo_variant = value;
+    return 0;
+  }
+  if (key && std::string(key) == "rm_variant") {
+    g_rm_variant = value;
     return 0;
   }
   return static_cast<int>(cudaErrorInvalidValue);
