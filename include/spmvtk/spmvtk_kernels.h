@@ -151,6 +151,9 @@ int spmvtk_k_spmv_ell_rm(int64_t n, int32_t nz, const double* val,
 /* Tuning override for experiments ("crs_variant": -1 = heuristic, 0..9 pick
  * a (lanes per row, rows per sub-warp) instance of the CRS kernel). */
 int spmvtk_k_tune(const char* key, int value);
+/* Transform tuning knobs ("ccs_slices", "ccs_threads"); spmvtk_k_tune
+ * forwards keys it does not know here. */
+int spmvtk_k_tune_convert(const char* key, int value);
 
 /* Forces every kernel of the library to be loaded (lazy module loading
  * would otherwise charge the first timed call). */

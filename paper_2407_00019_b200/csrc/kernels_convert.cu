@@ -13,6 +13,8 @@
 // construction.  Pointer expansion is warp-cooperative over a window of 32
 // row starts held one per lane, so every lane does useful work regardless of
 // the row-length distribution.
+#include <algorithm>
+#include <string>
 #include <type_traits>
 
 #include "common.cuh"
@@ -66,6 +68,36 @@ __device__ __forceinline__ int32_t resolve_segment(SegWindow& w, const int32_t* 
     w.load(ptr, r_end, lane);
   }
   return seg;
+}
+
+// resolve_segment for U positions per lane at once: the U binary searches
+// are independent shuffle chains, so their latencies overlap.
+template <int U>
+__device__ __forceinline__ void resolve_segments(SegWindow& w, const int32_t* ptr,
+                                                 int64_t r_end, int lane, const int32_t (&p)[U],
+                                                 int32_t (&seg)[U], uint32_t need) {
+  for (;;) {
+    int lo[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) lo[u] = 0;
+#pragma unroll
+    for (int step = 16; step >= 1; step >>= 1) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int32_t v = __shfl_sync(kFull, w.s, lo[u] + step - 1);
+        if (v <= p[u]) lo[u] += step;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (((need >> u) & 1u) && p[u] < w.end) {
+        seg[u] = static_cast<int32_t>(w.r0 + lo[u]);
+        need &= ~(1u << u);
+      }
+    if (!__any_sync(kFull, need != 0)) break;
+    w.r0 += 32;
+    w.load(ptr, r_end, lane);
+  }
 }
 
 // ---- pointer expansion ---------------------------------------------------
@@ -291,30 +323,48 @@ __global__ void __launch_bounds__(512) k_ccs_fix_long(const int32_t* __restrict_
 //                    convert.cpp:43-51), col_ptr and the final row_idx /
 //                    values written fully coalesced.
 // Buckets too large for shared memory take a global-memory path.
-constexpr int kSlices = 3 * 148;  // 3 CTAs per SM (64 KB histograms)
-constexpr int kBktThreads = 512;
-constexpr int kBktItems = 12;
-constexpr int kBktCap = kBktThreads * kBktItems;  // records per bucket sorted in smem
+constexpr int kSlices = 3 * 148;  // max slices (3 CTAs per SM, 64 KB histograms)
+int g_ccs_slices = 148;           // tuning: slices actually used (one per SM)
+int g_ccs_threads = 1024;         // tuning: threads of the count/scatter CTAs
+constexpr int kBktItems = 12;  // records per sort thread (bucket capacity = threads * 12)
+int g_ccs_sort_threads = 512;  // tuning: 256 or 512 (bucket target = threads * 8 entries)
 
-__global__ void k_slice_rows(const int32_t* __restrict__ irp, int64_t n, int32_t* slice_row) {
-  // slice s starts at the first row whose start >= s * nnz / kSlices
-  const int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s > kSlices) return;
-  const int64_t nnz = irp[n];
-  const int64_t target = nnz * s / kSlices;
-  int64_t lo = 0, hi = n;  // smallest r with irp[r] >= target
-  while (lo < hi) {
-    const int64_t mid = (lo + hi) >> 1;
-    if (irp[mid] < target) lo = mid + 1;
-    else hi = mid;
-  }
-  slice_row[s] = static_cast<int32_t>(s == kSlices ? n : lo);
+// Two-pass or single-pass partition is decided on the device from the
+// number of non-empty (fine bucket, slice) runs counted by k_bkt_count: few
+// runs (banded matrices) keep their write streams L2-resident in one pass;
+// many runs (scattered columns) go through the coarse pass + refine.
+constexpr int32_t kTwoPassRuns = 1 << 17;
+__device__ __forceinline__ bool two_pass(const int32_t* runs) {
+  return runs != nullptr && *runs > kTwoPassRuns;
 }
 
-__global__ void __launch_bounds__(kBktThreads) k_bkt_count(const int32_t* __restrict__ irp,
+__global__ void k_slice_rows(const int32_t* __restrict__ irp, int64_t n, int ns,
+                             int32_t* slice_row) {
+  // slice s starts at the first row whose start >= s * nnz / ns: one warp
+  // per slice, 32-way search (a handful of dependent loads, not log2(n))
+  const int s = static_cast<int>((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (s > ns) return;
+  const int64_t nnz = irp[n];
+  const int64_t target = nnz * s / ns;
+  int64_t lo = -1, hi = n;  // irp[lo] < target <= irp[hi] (irp[-1] = -inf)
+  while (hi - lo > 1) {
+    const int64_t probe = lo + 1 + ((hi - lo - 1) * lane) / 32;
+    const unsigned m = __ballot_sync(kFull, __ldg(irp + probe) < target);
+    const int64_t nlo = m ? __shfl_sync(kFull, probe, 31 - __clz(m)) : lo;
+    const int64_t nhi = ~m ? __shfl_sync(kFull, probe, __ffs(~m) - 1) : hi;
+    lo = nlo;
+    hi = nhi;
+  }
+  if (lane == 0) slice_row[s] = static_cast<int32_t>(s == ns ? n : hi);
+}
+
+__global__ void __launch_bounds__(1024) k_bkt_count(const int32_t* __restrict__ irp,
                                                            const int32_t* __restrict__ icol,
                                                            const int32_t* __restrict__ slice_row,
-                                                           int shift, int nb, int32_t* T) {
+                                                           int shift, int nb, int32_t* T,
+                                                           int fshift, int32_t* Tc,
+                                                           int32_t* runs) {
   extern __shared__ int32_t s_hist[];
   for (int b = threadIdx.x; b < nb; b += blockDim.x) s_hist[b] = 0;
   __syncthreads();
@@ -331,60 +381,308 @@ __global__ void __launch_bounds__(kBktThreads) k_bkt_count(const int32_t* __rest
   }
   for (; p < e1; p += step) atomicAdd(&s_hist[ld_stream(icol + p) >> shift], 1);
   __syncthreads();
-  for (int b = threadIdx.x; b < nb; b += blockDim.x)
-    T[static_cast<int64_t>(b) * kSlices + blockIdx.x] = s_hist[b];
-}
-
-__global__ void __launch_bounds__(kBktThreads) k_bkt_scatter(
-    const int32_t* __restrict__ irp, const int32_t* __restrict__ icol,
-    const double* __restrict__ val, const int32_t* __restrict__ slice_row, int shift, int nb,
-    const int32_t* __restrict__ Toff, int4* __restrict__ rec) {
-  extern __shared__ int32_t s_cur[];
-  for (int b = threadIdx.x; b < nb; b += blockDim.x)
-    s_cur[b] = Toff[static_cast<int64_t>(b) * kSlices + blockIdx.x];
-  __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-  const int64_t r_begin = slice_row[blockIdx.x], r_end = slice_row[blockIdx.x + 1];
-  constexpr int kRows = 64;  // rows per warp chunk
-  for (int64_t rb = r_begin + static_cast<int64_t>(warp) * kRows; rb < r_end;
-       rb += static_cast<int64_t>(nwarps) * kRows) {
-    const int64_t re = min(rb + kRows, r_end);
-    const int32_t e0 = __ldg(irp + rb), e1 = __ldg(irp + re);
-    SegWindow w;
-    w.r0 = rb;
-    w.load(irp, re, lane);
-    for (int32_t base = e0; base < e1; base += 32) {
-      const int32_t p = base + lane;
-      const bool valid = p < e1;
-      int32_t c = 0;
-      double v = 0.0;
-      if (valid) {
-        c = ld_stream(icol + p);
-        v = ld_stream(val + p);
+  int32_t nz = 0;
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+    T[static_cast<int64_t>(b) * gridDim.x + blockIdx.x] = s_hist[b];
+    nz += s_hist[b] != 0;
+  }
+  if (runs) {
+    nz = __reduce_add_sync(kFull, static_cast<unsigned>(nz));
+    if ((threadIdx.x & 31) == 0 && nz) atomicAdd(runs, nz);
+  }
+  if (Tc) {  // coarse buckets of 2^fshift fine buckets (two-pass partition)
+    const int F = 1 << fshift, nc = (nb + F - 1) >> fshift;
+    for (int c = threadIdx.x; c < nc; c += blockDim.x) {
+      int32_t sum = 0;
+      for (int f = 0; f < F; ++f) {
+        const int b = c * F + ((f + c) & (F - 1));  // rotated: spreads the banks
+        if (b < nb) sum += s_hist[b];
       }
-      const int32_t row = resolve_segment(w, irp, re, lane, p, valid);
-      if (valid) {
-        const int32_t slot = atomicAdd(&s_cur[c >> shift], 1);
-        rec[slot] = make_int4(c, row, __double2loint(v), __double2hiint(v));
-      }
+      Tc[static_cast<int64_t>(c) * gridDim.x + blockIdx.x] = sum;
     }
   }
 }
 
-// one CTA per bucket; dynamic smem: cnt[cb+1] | s_row[kBktCap] | s_val[kBktCap]
+__global__ void __launch_bounds__(1024) k_bkt_scatter(
+    const int32_t* __restrict__ irp, const int32_t* __restrict__ icol,
+    const double* __restrict__ val, const int32_t* __restrict__ slice_row, int shift, int nb,
+    const int32_t* __restrict__ Toff, int4* __restrict__ rec, const int32_t* runs, bool as_two) {
+  if (runs && two_pass(runs) != as_two) return;
+  extern __shared__ int32_t s_cur[];
+  for (int b = threadIdx.x; b < nb; b += blockDim.x)
+    s_cur[b] = Toff[static_cast<int64_t>(b) * gridDim.x + blockIdx.x];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int64_t r_begin = slice_row[blockIdx.x], r_end = slice_row[blockIdx.x + 1];
+  // every warp takes an equal share of the slice's ENTRIES (skewed rows
+  // would unbalance a split by rows) ...
+  const int32_t E0 = __ldg(irp + r_begin), E1 = __ldg(irp + r_end);
+  const int64_t tot = E1 - E0;
+  const int32_t p0 = E0 + static_cast<int32_t>(tot * warp / nwarps);
+  const int32_t p1 = E0 + static_cast<int32_t>(tot * (warp + 1) / nwarps);
+  if (p0 >= p1) return;
+  // ... and finds the row holding its first entry by a 32-way search
+  int64_t lo = r_begin, hi = r_end;  // irp[lo] <= p0 < irp[hi]
+  while (hi - lo > 1) {
+    const int64_t probe = lo + 1 + ((hi - lo - 1) * lane) / 32;
+    const unsigned m = __ballot_sync(kFull, __ldg(irp + probe) <= p0);
+    const int64_t nlo = m ? __shfl_sync(kFull, probe, 31 - __clz(m)) : lo;
+    const int64_t nhi = ~m ? __shfl_sync(kFull, probe, __ffs(~m) - 1) : hi;
+    lo = nlo;
+    hi = nhi;
+  }
+  SegWindow w;
+  w.r0 = lo;
+  w.load(irp, r_end, lane);
+  constexpr int kU = 4;  // 32-entry batches per lane per step
+  int32_t c[kU];
+  double v[kU];
+#pragma unroll
+  for (int u = 0; u < kU; ++u) {
+    const int32_t p = p0 + u * 32 + lane;
+    c[u] = p < p1 ? ld_stream(icol + p) : 0;
+    v[u] = p < p1 ? ld_stream(val + p) : 0.0;
+  }
+  for (int32_t base = p0; base < p1; base += 32 * kU) {
+    int32_t cn[kU];
+    double vn[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {  // next step's loads fly during this one
+      const int32_t p = base + 32 * kU + u * 32 + lane;
+      cn[u] = p < p1 ? ld_stream(icol + p) : 0;
+      vn[u] = p < p1 ? ld_stream(val + p) : 0.0;
+    }
+    int32_t pp[kU], row[kU];
+    uint32_t need = 0;
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      pp[u] = base + u * 32 + lane;
+      row[u] = 0;
+      if (pp[u] < p1) need |= 1u << u;
+    }
+    resolve_segments<kU>(w, irp, r_end, lane, pp, row, need);
+    int32_t slot[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u)  // independent shared atomics, back to back
+      slot[u] = pp[u] < p1 ? atomicAdd(&s_cur[c[u] >> shift], 1) : 0;
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (pp[u] < p1)
+        rec[slot[u]] = make_int4(c[u], row[u], __double2loint(v[u]), __double2hiint(v[u]));
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      c[u] = cn[u];
+      v[u] = vn[u];
+    }
+  }
+}
+
+// Staged variant for at most kStageMaxB buckets (the coarse pass, or a
+// single pass over few buckets): the 32 warps advance in lock step, 128
+// entries each per step; the step's 4096 records are counting-sorted by
+// bucket in shared memory and written out run by run, so consecutive lanes
+// store consecutive addresses instead of 32 scattered 16-byte records.
+constexpr int kStageThreads = 1024;
+constexpr int kStageU = 4;
+constexpr int kStageTile = kStageThreads * kStageU;
+constexpr int kStageMaxB = 1024;
+
+__global__ void __launch_bounds__(kStageThreads) k_bkt_scatter_staged(
+    const int32_t* __restrict__ irp, const int32_t* __restrict__ icol,
+    const double* __restrict__ val, const int32_t* __restrict__ slice_row, int shift, int nb,
+    const int32_t* __restrict__ Toff, int4* __restrict__ rec, const int32_t* runs, bool as_two) {
+  if (runs && two_pass(runs) != as_two) return;
+  extern __shared__ int4 s_rec[];  // kStageTile records
+  __shared__ int32_t s_cur[kStageMaxB], s_cnt[kStageMaxB], s_off[kStageMaxB];
+  __shared__ int32_t s_wsum[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int nwarps = kStageThreads / 32;
+  if (tid < nb) {
+    s_cur[tid] = Toff[static_cast<int64_t>(tid) * gridDim.x + blockIdx.x];
+    s_cnt[tid] = 0;
+  }
+  const int64_t r_begin = slice_row[blockIdx.x], r_end = slice_row[blockIdx.x + 1];
+  const int32_t E0 = __ldg(irp + r_begin), E1 = __ldg(irp + r_end);
+  const int64_t tot = E1 - E0;
+  const int32_t p0 = E0 + static_cast<int32_t>(tot * warp / nwarps);
+  const int32_t p1 = E0 + static_cast<int32_t>(tot * (warp + 1) / nwarps);
+  const int steps = static_cast<int>(((tot + nwarps - 1) / nwarps + 32 * kStageU - 1) /
+                                     (32 * kStageU));
+  int64_t lo = r_begin, hi = r_end;  // row holding p0: irp[lo] <= p0 < irp[hi]
+  if (p0 < p1) {
+    while (hi - lo > 1) {
+      const int64_t probe = lo + 1 + ((hi - lo - 1) * lane) / 32;
+      const unsigned m = __ballot_sync(kFull, __ldg(irp + probe) <= p0);
+      const int64_t nlo = m ? __shfl_sync(kFull, probe, 31 - __clz(m)) : lo;
+      const int64_t nhi = ~m ? __shfl_sync(kFull, probe, __ffs(~m) - 1) : hi;
+      lo = nlo;
+      hi = nhi;
+    }
+  }
+  SegWindow w;
+  w.r0 = lo;
+  w.load(irp, r_end, lane);
+  int32_t c[kStageU];
+  double v[kStageU];
+#pragma unroll
+  for (int u = 0; u < kStageU; ++u) {
+    const int32_t p = p0 + u * 32 + lane;
+    c[u] = p < p1 ? ld_stream(icol + p) : 0;
+    v[u] = p < p1 ? ld_stream(val + p) : 0.0;
+  }
+  __syncthreads();
+  for (int st = 0; st < steps; ++st) {
+    const int32_t base = p0 + st * 32 * kStageU;
+    int32_t pp[kStageU], row[kStageU], rk[kStageU], cn[kStageU];
+    double vn[kStageU];
+    uint32_t need = 0;
+#pragma unroll
+    for (int u = 0; u < kStageU; ++u) {  // the next step's loads fly across the barriers
+      const int32_t p = base + 32 * kStageU + u * 32 + lane;
+      cn[u] = p < p1 ? ld_stream(icol + p) : 0;
+      vn[u] = p < p1 ? ld_stream(val + p) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kStageU; ++u) {
+      pp[u] = base + u * 32 + lane;
+      row[u] = 0;
+      if (pp[u] < p1) need |= 1u << u;
+    }
+    resolve_segments<kStageU>(w, irp, r_end, lane, pp, row, need);
+#pragma unroll
+    for (int u = 0; u < kStageU; ++u)
+      rk[u] = pp[u] < p1 ? atomicAdd(&s_cnt[c[u] >> shift], 1) : 0;
+    __syncthreads();
+    // exclusive scan of the step's bucket counts (thread t owns bucket t)
+    const int32_t x = tid < nb ? s_cnt[tid] : 0;
+    int32_t inc = x;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int32_t t = __shfl_up_sync(kFull, inc, d);
+      if (lane >= d) inc += t;
+    }
+    if (lane == 31) s_wsum[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+      const int32_t wv = s_wsum[lane];
+      int32_t wi = wv;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int32_t t = __shfl_up_sync(kFull, wi, d);
+        if (lane >= d) wi += t;
+      }
+      s_wsum[lane] = wi - wv;
+    }
+    __syncthreads();
+    if (tid < nb) s_off[tid] = s_wsum[warp] + inc - x;
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < kStageU; ++u)
+      if (pp[u] < p1)
+        s_rec[s_off[c[u] >> shift] + rk[u]] =
+            make_int4(c[u], row[u], __double2loint(v[u]), __double2hiint(v[u]));
+    __syncthreads();
+    const int32_t count = s_off[nb - 1] + s_cnt[nb - 1];
+    for (int32_t i = tid; i < count; i += kStageThreads) {
+      const int4 r = s_rec[i];
+      const int b = r.x >> shift;
+      rec[s_cur[b] + i - s_off[b]] = r;
+    }
+    __syncthreads();
+    if (tid < nb) {
+      s_cur[tid] += s_cnt[tid];
+      s_cnt[tid] = 0;
+    }
+#pragma unroll
+    for (int u = 0; u < kStageU; ++u) {
+      c[u] = cn[u];
+      v[u] = vn[u];
+    }
+    __syncthreads();
+  }
+}
+
+// Two-pass partition, second pass: the coarse-partitioned records are cut
+// into chunks of kRefineItems; a chunk's fine buckets form a window (its
+// records lie in a contiguous range of coarse buckets); the chunk claims a
+// run per fine bucket with one global atomic (fcur) and appends its records
+// there with shared cursors, so every run is a contiguous write.
+constexpr int kRefineThreads = 512;
+constexpr int kRefinePer = 8;
+constexpr int kRefineItems = kRefineThreads * kRefinePer;
+constexpr int kRefineWin = 4096;
+
+__global__ void __launch_bounds__(kRefineThreads) k_bkt_refine(
+    const int4* __restrict__ rec, int64_t nnz, int shift, int fshift,
+    const int32_t* __restrict__ Toff, int ns, int32_t* __restrict__ fcur,
+    int4* __restrict__ rec2, const int32_t* runs) {
+  if (!two_pass(runs)) return;
+  __shared__ int32_t s_cnt[kRefineWin];
+  const int64_t q0 = static_cast<int64_t>(blockIdx.x) * kRefineItems;
+  const int32_t len = static_cast<int32_t>(min(static_cast<int64_t>(kRefineItems), nnz - q0));
+  int4 r[kRefinePer];
+#pragma unroll
+  for (int k = 0; k < kRefinePer; ++k) {
+    const int32_t q = static_cast<int32_t>(threadIdx.x) + k * kRefineThreads;
+    if (q < len) r[k] = ld_stream4(rec + q0 + q);
+  }
+  const int32_t b_lo = ((__ldg(&rec[q0].x) >> shift) >> fshift) << fshift;
+  const int32_t b_hi = (((__ldg(&rec[q0 + len - 1].x) >> shift) >> fshift) + 1) << fshift;
+  const int32_t win = b_hi - b_lo;
+  if (win > kRefineWin) {  // many tiny coarse buckets: global cursors
+#pragma unroll
+    for (int k = 0; k < kRefinePer; ++k) {
+      const int32_t q = static_cast<int32_t>(threadIdx.x) + k * kRefineThreads;
+      if (q < len) {
+        const int32_t b = r[k].x >> shift;
+        rec2[Toff[static_cast<int64_t>(b) * ns] + atomicAdd(&fcur[b], 1)] = r[k];
+      }
+    }
+    return;
+  }
+  for (int i = threadIdx.x; i < win; i += blockDim.x) s_cnt[i] = 0;
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < kRefinePer; ++k) {
+    const int32_t q = static_cast<int32_t>(threadIdx.x) + k * kRefineThreads;
+    if (q < len) atomicAdd(&s_cnt[(r[k].x >> shift) - b_lo], 1);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < win; i += blockDim.x) {
+    const int32_t c = s_cnt[i];
+    if (c) {
+      const int64_t b = b_lo + i;
+      s_cnt[i] = Toff[b * ns] + atomicAdd(&fcur[b], c);
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < kRefinePer; ++k) {
+    const int32_t q = static_cast<int32_t>(threadIdx.x) + k * kRefineThreads;
+    if (q < len) rec2[atomicAdd(&s_cnt[(r[k].x >> shift) - b_lo], 1)] = r[k];
+  }
+}
+
+// one CTA per bucket; dynamic smem: cnt[cb+1] | s_val | s_row | s_col (kBktCap each)
+constexpr int32_t kRankMax = 256;  // longer columns take the block network
+template <int kBktThreads>
 __global__ void __launch_bounds__(kBktThreads) k_bkt_sort(
-    const int4* __restrict__ rec, const int32_t* __restrict__ Toff, int64_t n, int shift,
-    int nb, int32_t* __restrict__ col_ptr, int32_t* __restrict__ row_idx,
+    const int4* rec1, const int4* rec2, const int32_t* runs,
+    const int32_t* __restrict__ Toff, int64_t n, int shift,
+    int nb, int ns, int32_t* __restrict__ col_ptr, int32_t* __restrict__ row_idx,
     double* __restrict__ out_val, int32_t* big_queue, int32_t* big_len) {
+  constexpr int kBktCap = kBktThreads * kBktItems;
+  const int4* __restrict__ rec = two_pass(runs) ? rec2 : rec1;
   extern __shared__ unsigned char s_raw[];
   const int cb = 1 << shift;
   int32_t* cnt = reinterpret_cast<int32_t*>(s_raw);  // cb + 1 entries
   double* s_val = reinterpret_cast<double*>(s_raw + ((static_cast<size_t>(cb + 1) * 4 + 15) & ~15));
   int32_t* s_row = reinterpret_cast<int32_t*>(s_val + kBktCap);
+  uint16_t* s_col = reinterpret_cast<uint16_t*>(s_row + kBktCap);
   const int b = blockIdx.x;
-  const int32_t bs = Toff[static_cast<int64_t>(b) * kSlices];
-  const int32_t be = (b + 1 < nb) ? Toff[static_cast<int64_t>(b + 1) * kSlices]
-                                  : Toff[static_cast<int64_t>(nb) * kSlices];
+  const int32_t bs = Toff[static_cast<int64_t>(b) * ns];
+  const int32_t be = (b + 1 < nb) ? Toff[static_cast<int64_t>(b + 1) * ns]
+                                  : Toff[static_cast<int64_t>(nb) * ns];
   const int64_t c0 = static_cast<int64_t>(b) << shift;
   const int ncols = static_cast<int>(min(static_cast<int64_t>(cb), n - c0));
   const int32_t len = be - bs;
@@ -411,21 +709,49 @@ __global__ void __launch_bounds__(kBktThreads) k_bkt_sort(
       atomicAdd(&cnt[__ldg(&rec[bs + q].x) - c0], 1);
   }
   __syncthreads();
-  // exclusive scan of cnt[0..cb) by warp 0 (cb <= 4096, a few passes)
-  if (threadIdx.x < 32) {
-    int32_t carry = 0;
-    for (int base = 0; base < cb; base += 32) {
-      const int i = base + threadIdx.x;
-      const int32_t v = cnt[i];
-      int32_t inc = v;
-      for (int d = 1; d < 32; d <<= 1) {
-        const int32_t t = __shfl_up_sync(kFull, inc, d);
-        if (threadIdx.x >= d) inc += t;
+  // block exclusive scan of cnt[0..cb) (cb a power of two <= 4096): each
+  // thread owns cb/512 consecutive counters
+  {
+    __shared__ int32_t s_warp[kBktThreads / 32];
+    const int per = cb > kBktThreads ? cb / kBktThreads : 1;
+    const int i0 = static_cast<int>(threadIdx.x) * per;
+    constexpr int kPer = 4096 / kBktThreads;
+    int32_t loc[kPer];
+    int32_t sum = 0;
+#pragma unroll
+    for (int k = 0; k < kPer; ++k)
+      if (k < per && i0 + k < cb) {
+        loc[k] = cnt[i0 + k];
+        sum += loc[k];
       }
-      cnt[i] = carry + inc - v;
-      carry += __shfl_sync(kFull, inc, 31);
+    int32_t inc = sum;
+    const int ln = threadIdx.x & 31, wp = threadIdx.x >> 5;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int32_t t = __shfl_up_sync(kFull, inc, d);
+      if (ln >= d) inc += t;
     }
-    if (threadIdx.x == 0) cnt[cb] = carry;
+    if (ln == 31) s_warp[wp] = inc;
+    __syncthreads();
+    if (wp == 0) {
+      const int32_t wv = ln < kBktThreads / 32 ? s_warp[ln] : 0;
+      int32_t wi = wv;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int32_t t = __shfl_up_sync(kFull, wi, d);
+        if (ln >= d) wi += t;
+      }
+      if (ln < kBktThreads / 32) s_warp[ln] = wi - wv;
+      if (ln == kBktThreads / 32 - 1) cnt[cb] = wi;
+    }
+    __syncthreads();
+    int32_t run = s_warp[wp] + inc - sum;
+#pragma unroll
+    for (int k = 0; k < kPer; ++k)
+      if (k < per && i0 + k < cb) {
+        cnt[i0 + k] = run;
+        run += loc[k];
+      }
   }
   __syncthreads();
   for (int i = threadIdx.x; i < ncols; i += blockDim.x) col_ptr[c0 + i] = bs + cnt[i];
@@ -449,61 +775,47 @@ __global__ void __launch_bounds__(kBktThreads) k_bkt_sort(
   for (int k = 0; k < kBktItems; ++k) {
     const int32_t q = static_cast<int32_t>(threadIdx.x) + k * kBktThreads;
     if (q < len) {
-      const int32_t slot = atomicAdd(&cnt[r[k].x - c0], 1);
+      const int32_t col = r[k].x - static_cast<int32_t>(c0);
+      const int32_t slot = atomicAdd(&cnt[col], 1);
       s_row[slot] = r[k].y;
       s_val[slot] = rec_val(r[k]);
+      s_col[slot] = static_cast<uint16_t>(col);
     }
   }
+  __shared__ int s_long;
+  if (threadIdx.x == 0) s_long = 0;
   __syncthreads();
   // cnt[i] now holds the END of column i; column i spans [end(i-1), end(i)).
-  // One warp per column: register bitonic sort on (row << 5 | lane) for
-  // columns of <= 32 entries (already-sorted columns skip the network), a
-  // lane-0 insertion sort beyond; results go straight to the output arrays.
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int i = warp; i < ncols; i += blockDim.x >> 5) {
-    const int32_t a = i ? cnt[i - 1] : 0, e = cnt[i], cl = e - a;
-    if (cl <= 32 && n < (int64_t(1) << 27)) {  // (row << 5 | lane) must fit 32 bits
-      int32_t rr = lane < cl ? s_row[a + lane] : INT_MAX;
-      double v = lane < cl ? s_val[a + lane] : 0.0;
-      const int32_t rn = __shfl_down_sync(kFull, rr, 1);
-      if (__any_sync(kFull, lane + 1 < cl && rn < rr)) {
-        uint32_t key = lane < cl ? (static_cast<uint32_t>(rr) << 5) | lane : 0xffffffffu;
-#pragma unroll
-        for (int size = 2; size <= 32; size <<= 1) {
-#pragma unroll
-          for (int d = size >> 1; d > 0; d >>= 1) {
-            const uint32_t other = __shfl_xor_sync(kFull, key, d);
-            const bool up = (lane & size) == 0, lower = (lane & d) == 0;
-            key = (lower == up) ? min(key, other) : max(key, other);
-          }
-        }
-        v = __shfl_sync(kFull, v, static_cast<int>(key & 31u));
-        rr = static_cast<int32_t>(key >> 5);
-      }
-      if (lane < cl) {
-        row_idx[bs + a + lane] = rr;
-        st_stream(out_val + bs + a + lane, v);
-      }
-    } else {
-      if (lane == 0)
-        for (int32_t k = a + 1; k < e; ++k) {  // insertion sort on row
-          const int32_t key = s_row[k];
-          const double v = s_val[k];
-          int32_t j = k - 1;
-          while (j >= a && s_row[j] > key) {
-            s_row[j + 1] = s_row[j];
-            s_val[j + 1] = s_val[j];
-            --j;
-          }
-          s_row[j + 1] = key;
-          s_val[j + 1] = v;
-        }
-      __syncwarp();
-      for (int32_t q = a + lane; q < e; q += 32) {
-        row_idx[bs + q] = s_row[q];
-        st_stream(out_val + bs + q, s_val[q]);
-      }
+  // Rows are distinct inside a column, so an entry's final position is its
+  // rank by row there: one thread per slot counts the smaller rows (lanes of
+  // a warp mostly share a column -> broadcast reads) and writes it out.
+  // (Measured: staging the permutation for coalesced writes, or ranking 4
+  // slots per thread, were both slower.)
+  for (int32_t q = threadIdx.x; q < len; q += blockDim.x) {
+    const int col = s_col[q];
+    const int32_t a = col ? cnt[col - 1] : 0, e = cnt[col];
+    if (e - a > kRankMax) {
+      s_long = 1;
+      continue;
     }
+    const int32_t row = s_row[q];
+    int32_t rank = 0;
+    for (int32_t j = a; j < e; ++j) rank += s_row[j] < row;
+    row_idx[bs + a + rank] = row;
+    st_stream(out_val + bs + a + rank, s_val[q]);
+  }
+  __syncthreads();
+  if (!s_long) return;
+  // long columns: block bitonic network in shared memory, then copy out
+  for (int i = 0; i < ncols; ++i) {
+    const int32_t a = i ? cnt[i - 1] : 0, e = cnt[i];
+    if (e - a <= kRankMax) continue;
+    block_bitonic(s_row + a, s_val + a, e - a);
+    for (int32_t q = a + threadIdx.x; q < e; q += blockDim.x) {
+      row_idx[bs + q] = s_row[q];
+      st_stream(out_val + bs + q, s_val[q]);
+    }
+    __syncthreads();
   }
 }
 
@@ -591,17 +903,19 @@ __global__ void __launch_bounds__(256) k_crs_to_ell_cm_flat(int64_t n, int32_t n
                                                             int32_t* __restrict__ out_col,
                                                             int32_t* __restrict__ out_count,
                                                             int64_t pad_base) {
+  // staged entry f lives at f + f/32: rows of exactly 16 or 32 entries read
+  // in the write phase (one row per lane) would otherwise all hit one bank
   __shared__ int32_t s_ptr[kFlatRows + 1];
-  __shared__ double s_v[kFlatCap];
-  __shared__ int32_t s_c[kFlatCap];
+  __shared__ double s_v[kFlatCap + kFlatCap / 32];
+  __shared__ int32_t s_c[kFlatCap + kFlatCap / 32];
   const int64_t r0 = static_cast<int64_t>(blockIdx.x) * kFlatRows;
   for (int t = threadIdx.x; t <= kFlatRows; t += blockDim.x)
     s_ptr[t] = __ldg(irp + min(r0 + t, n));
   __syncthreads();
   const int32_t e0 = s_ptr[0], cnt = s_ptr[kFlatRows] - e0;
   for (int f = threadIdx.x; f < cnt; f += blockDim.x) {
-    s_v[f] = ld_stream(val + e0 + f);
-    s_c[f] = ld_stream(icol + e0 + f);
+    s_v[f + (f >> 5)] = ld_stream(val + e0 + f);
+    s_c[f + (f >> 5)] = ld_stream(icol + e0 + f);
   }
   for (int t = threadIdx.x; t < kFlatRows; t += blockDim.x)
     if (r0 + t < n) out_count[r0 + t] = s_ptr[t + 1] - s_ptr[t];
@@ -614,8 +928,9 @@ __global__ void __launch_bounds__(256) k_crs_to_ell_cm_flat(int64_t n, int32_t n
     const int32_t a = s_ptr[row], len = s_ptr[row + 1] - a;
     const bool real = k < len;
     const int64_t slot = static_cast<int64_t>(k) * ld + i;
-    st_stream(out_val + slot, real ? s_v[a - e0 + k] : 0.0);
-    out_col[slot] = real ? s_c[a - e0 + k] : static_cast<int32_t>(pad_base + (i < n ? i : 0));
+    const int fs = a - e0 + k;
+    st_stream(out_val + slot, real ? s_v[fs + (fs >> 5)] : 0.0);
+    out_col[slot] = real ? s_c[fs + (fs >> 5)] : static_cast<int32_t>(pad_base + (i < n ? i : 0));
   }
 }
 
@@ -673,22 +988,52 @@ namespace {
 struct BucketPlan {
   int shift;
   int nb;
+  int fshift;  // coarse bucket = 2^fshift fine buckets; 0 = single pass
+  int nc;      // coarse buckets
 };
+int g_ccs_coarse = 9;  // tuning: log2 of the coarse bucket count target (0 = one pass)
 BucketPlan bucket_plan(int64_t n, int64_t nnz) {
   const double per_col = n > 0 ? static_cast<double>(nnz) / static_cast<double>(n) : 1.0;
   int shift = 0;
-  while (shift < 12 && static_cast<double>(int64_t(1) << (shift + 1)) * per_col <= 4096.0) ++shift;
+  const double target = 8.0 * g_ccs_sort_threads;
+  while (shift < 12 && static_cast<double>(int64_t(1) << (shift + 1)) * per_col <= target) ++shift;
   while (((n + (int64_t(1) << shift) - 1) >> shift) > 32768) ++shift;
-  return {shift, static_cast<int>((n + (int64_t(1) << shift) - 1) >> shift)};
+  const int nb = static_cast<int>((n + (int64_t(1) << shift) - 1) >> shift);
+  int fshift = 0;
+  if (g_ccs_coarse > 0)
+    while ((nb >> fshift) > (1 << g_ccs_coarse)) ++fshift;
+  return {shift, nb, fshift, (nb + (1 << fshift) - 1) >> fshift};
 }
 size_t align256(size_t v) { return (v + 255) & ~static_cast<size_t>(255); }
 }  // namespace
 
+int spmvtk_k_tune_convert(const char* key, int value) {
+  if (key && std::string(key) == "ccs_slices") {
+    g_ccs_slices = value;
+    return 0;
+  }
+  if (key && std::string(key) == "ccs_threads") {
+    g_ccs_threads = value;
+    return 0;
+  }
+  if (key && std::string(key) == "ccs_sort_threads") {
+    g_ccs_sort_threads = value == 256 ? 256 : 512;
+    return 0;
+  }
+  if (key && std::string(key) == "ccs_coarse") {
+    g_ccs_coarse = value;
+    return 0;
+  }
+  return static_cast<int>(cudaErrorInvalidValue);
+}
+
 size_t spmvtk_k_ccs_scratch_bytes(int64_t n, int64_t nnz) {
   const BucketPlan bp = bucket_plan(n, nnz);
   const size_t t = static_cast<size_t>(bp.nb) * kSlices + 1;
-  const size_t bucketed = align256(static_cast<size_t>(nnz) * 16) + align256((kSlices + 1) * 4) +
-                          2 * align256(t * 4) + align256((static_cast<size_t>(bp.nb) + 1) * 4) +
+  const size_t tc = static_cast<size_t>(bp.nc) * kSlices + 1;
+  const size_t bucketed = 2 * align256(static_cast<size_t>(nnz) * 16) + 256 +
+                          align256((kSlices + 1) * 4) + 2 * align256(t * 4) +
+                          2 * align256(tc * 4) + 2 * align256((static_cast<size_t>(bp.nb) + 1) * 4) +
                           align256(spmvtk_k_scan_scratch_bytes(static_cast<int64_t>(t))) + 1024;
   // the atomic-cursor variant needs count/cursor/queue over n columns
   const size_t atomic = static_cast<size_t>(nnz) * 16 +
@@ -707,7 +1052,9 @@ int spmvtk_k_crs_to_ccs(int64_t n, int64_t nnz, const int32_t* irp, const int32_
     SPMVTK_LAUNCH_RETURN();
   }
   const BucketPlan bp = bucket_plan(n, nnz);
-  const int64_t tlen = static_cast<int64_t>(bp.nb) * kSlices;
+  const int ns = std::max(1, std::min(g_ccs_slices, kSlices));
+  const int nt = g_ccs_threads == 1024 ? 1024 : 512;
+  const int64_t tlen = static_cast<int64_t>(bp.nb) * ns;
   uintptr_t cur = (reinterpret_cast<uintptr_t>(scratch) + 255) & ~static_cast<uintptr_t>(255);
   auto take = [&](size_t bytes) {
     void* p = reinterpret_cast<void*>(cur);
@@ -721,28 +1068,67 @@ int spmvtk_k_crs_to_ccs(int64_t n, int64_t nnz, const int32_t* irp, const int32_
   int32_t* big = static_cast<int32_t*>(take((static_cast<size_t>(bp.nb) + 1) * 4));
   int32_t* big_len = big + bp.nb;
   void* scan_scratch = take(spmvtk_k_scan_scratch_bytes(tlen + 1));
+  const bool two = bp.fshift > 0;
+  const int64_t tclen = static_cast<int64_t>(bp.nc) * ns;
+  int4* rec2 = two ? static_cast<int4*>(take(static_cast<size_t>(nnz) * 16)) : rec;
+  int32_t* Tc = two ? static_cast<int32_t*>(take(static_cast<size_t>(tclen + 1) * 4)) : nullptr;
+  int32_t* Tcoff = two ? static_cast<int32_t*>(take(static_cast<size_t>(tclen + 1) * 4)) : nullptr;
+  int32_t* fcur = two ? static_cast<int32_t*>(take(static_cast<size_t>(bp.nb) * 4)) : nullptr;
+  int32_t* runs = two ? static_cast<int32_t*>(take(4)) : nullptr;
 
   const size_t hist_smem = static_cast<size_t>(bp.nb) * 4;
   const int cb = 1 << bp.shift;
   const size_t sort_smem = ((static_cast<size_t>(cb + 1) * 4 + 15) & ~static_cast<size_t>(15)) +
-                           static_cast<size_t>(kBktCap) * 12;
+                           static_cast<size_t>(g_ccs_sort_threads) * kBktItems * 14;
   static const bool attrs = [] {  // thread-safe one-time setup
     cudaFuncSetAttribute(k_bkt_count, cudaFuncAttributeMaxDynamicSharedMemorySize, 32768 * 4);
     cudaFuncSetAttribute(k_bkt_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, 32768 * 4);
-    cudaFuncSetAttribute(k_bkt_sort, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(((4097 * 4 + 15) & ~15) + kBktCap * 12));
+    cudaFuncSetAttribute(k_bkt_scatter_staged, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kStageTile * static_cast<int>(sizeof(int4)));
+    cudaFuncSetAttribute(k_bkt_sort<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(((4097 * 4 + 15) & ~15) + 512 * kBktItems * 14));
+    cudaFuncSetAttribute(k_bkt_sort<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(((4097 * 4 + 15) & ~15) + 256 * kBktItems * 14));
     return true;
   }();
   (void)attrs;
   cudaMemsetAsync(big_len, 0, sizeof(int32_t), s);
-  k_slice_rows<<<(kSlices + 128) / 128, 128, 0, s>>>(irp, n, slice_row);
-  k_bkt_count<<<kSlices, kBktThreads, hist_smem, s>>>(irp, icol, slice_row, bp.shift, bp.nb, T);
+  if (two) cudaMemsetAsync(runs, 0, sizeof(int32_t), s);
+  k_slice_rows<<<(ns + 1 + 3) / 4, 128, 0, s>>>(irp, n, ns, slice_row);
+  k_bkt_count<<<ns, nt, hist_smem, s>>>(irp, icol, slice_row, bp.shift, bp.nb, T, bp.fshift,
+                                        Tc, runs);
   int rc = spmvtk_k_exclusive_scan(T, Toff, tlen, scan_scratch, stream);
   if (rc) return rc;
-  k_bkt_scatter<<<kSlices, kBktThreads, hist_smem, s>>>(irp, icol, val, slice_row, bp.shift,
-                                                         bp.nb, Toff, rec);
-  k_bkt_sort<<<bp.nb, kBktThreads, sort_smem, s>>>(rec, Toff, n, bp.shift, bp.nb, col_ptr,
-                                                    row_idx, out_val, big, big_len);
+  if (two) {
+    // both alternatives are launched; each returns at once unless the run
+    // count (device-side, no host sync) selects it
+    rc = spmvtk_k_exclusive_scan(Tc, Tcoff, tclen, scan_scratch, stream);
+    if (rc) return rc;
+    cudaMemsetAsync(fcur, 0, static_cast<size_t>(bp.nb) * 4, s);
+    if (bp.nc <= kStageMaxB)
+      k_bkt_scatter_staged<<<ns, kStageThreads, kStageTile * sizeof(int4), s>>>(
+          irp, icol, val, slice_row, bp.shift + bp.fshift, bp.nc, Tcoff, rec, runs, true);
+    else
+      k_bkt_scatter<<<ns, nt, static_cast<size_t>(bp.nc) * 4, s>>>(
+          irp, icol, val, slice_row, bp.shift + bp.fshift, bp.nc, Tcoff, rec, runs, true);
+    k_bkt_refine<<<static_cast<unsigned>((nnz + kRefineItems - 1) / kRefineItems),
+                   kRefineThreads, 0, s>>>(rec, nnz, bp.shift, bp.fshift, Toff, ns, fcur, rec2,
+                                           runs);
+    k_bkt_scatter<<<ns, nt, hist_smem, s>>>(irp, icol, val, slice_row, bp.shift, bp.nb, Toff,
+                                            rec, runs, false);
+  } else if (bp.nb <= kStageMaxB && g_ccs_coarse > 0) {
+    k_bkt_scatter_staged<<<ns, kStageThreads, kStageTile * sizeof(int4), s>>>(
+        irp, icol, val, slice_row, bp.shift, bp.nb, Toff, rec, nullptr, false);
+  } else {
+    k_bkt_scatter<<<ns, nt, hist_smem, s>>>(irp, icol, val, slice_row, bp.shift, bp.nb, Toff,
+                                            rec, nullptr, false);
+  }
+  if (g_ccs_sort_threads == 256)
+    k_bkt_sort<256><<<bp.nb, 256, sort_smem, s>>>(rec, rec2, runs, Toff, n, bp.shift, bp.nb, ns,
+                                                  col_ptr, row_idx, out_val, big, big_len);
+  else
+    k_bkt_sort<512><<<bp.nb, 512, sort_smem, s>>>(rec, rec2, runs, Toff, n, bp.shift, bp.nb, ns,
+                                                  col_ptr, row_idx, out_val, big, big_len);
   k_bkt_sort_big<<<kSMs, 512, 0, s>>>(col_ptr, n, bp.shift, row_idx, out_val, big, big_len);
   SPMVTK_LAUNCH_RETURN();
 }

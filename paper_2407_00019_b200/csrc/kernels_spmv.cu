@@ -894,7 +894,7 @@ int spmvtk_k_tune(const char* key, int value) {
     g_rm_variant = value;
     return 0;
   }
-  return static_cast<int>(cudaErrorInvalidValue);
+  return spmvtk_k_tune_convert(key, value);
 }
 
 int spmvtk_k_preload(void) {

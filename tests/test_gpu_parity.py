@@ -310,6 +310,45 @@ def test_larger_random_parity_with_port(gpu, port):
             assert max_rel_error(y, want) <= TOL, (it, k)
 
 
+def _crs_from_pairs(n, r, c, rng):
+    key = np.unique(r.astype(np.int64) * n + c.astype(np.int64))
+    rows, cols = key // n, key % n
+    rp = np.concatenate([[0], np.cumsum(np.bincount(rows, minlength=n))]).astype(np.int64) + 1
+    return rp, cols.astype(np.int64) + 1, rng.standard_normal(key.shape[0])
+
+
+def test_ccs_partition_paths(gpu, port):
+    """CRS->CCS through each partition path against the C port, bit-exact:
+    scattered columns (many runs -> coarse pass + refine) with a 1000-entry
+    column (block network inside a bucket) and two dense columns (oversized
+    bucket path); a banded matrix (few runs -> single pass)."""
+    sp = gpu
+    rng = np.random.default_rng(21)
+    n = 300_000
+    r = np.repeat(np.arange(n), rng.integers(4, 20, size=n))
+    c = rng.integers(0, n, size=r.shape[0])
+    dense = rng.random(n) < 0.5
+    extra_r = np.concatenate([np.nonzero(dense)[0], np.nonzero(dense)[0],
+                              rng.choice(n, 1000, replace=False)])
+    extra_c = np.concatenate([np.full(dense.sum(), 5), np.full(dense.sum(), 77777),
+                              np.full(1000, 123456)])
+    cases = [(n, *_crs_from_pairs(n, np.concatenate([r, extra_r]),
+                                  np.concatenate([c, extra_c]), rng))]
+    nb = 200_000
+    rb = np.repeat(np.arange(nb), 24)
+    cb = np.clip(rb + rng.integers(-500, 500, size=rb.shape[0]), 0, nb - 1)
+    cases.append((nb, *_crs_from_pairs(nb, rb, cb, rng)))
+    for nn, rp, ci, v in cases:
+        m = upload(sp, nn, rp, ci, v)
+        cp, ri, cv = port.crs_to_ccs(nn, rp, ci, v)
+        ccs = m.convert(sp.Format.CCS)
+        np.testing.assert_array_equal(ref_layout(ccs, sp, sp.Array.POINTER), cp)
+        np.testing.assert_array_equal(ref_layout(ccs, sp, sp.Array.ROW_IDX), ri)
+        assert ccs.array(sp.Array.VALUES).tobytes() == cv.tobytes()
+        ccs.free()
+        m.free()
+
+
 def test_crs_long_rows_path(gpu, port):
     """Rows above the vector kernel's 4096 limit take the block-per-row pass."""
     sp = gpu

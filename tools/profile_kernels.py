@@ -21,6 +21,7 @@ ap.add_argument("--dparam", type=float, default=0.0)
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--only", default="")
 ap.add_argument("--transforms", action="store_true")
+ap.add_argument("--formats", default="", help="comma list of formats to convert to")
 a = ap.parse_args()
 param = a.param or {1: 256, 2: 1 << 20, 3: 128, 4: 1 << 22, 5: 1 << 21}[a.config]
 only = set(a.only.split(",")) if a.only else None
@@ -30,7 +31,10 @@ n = m.describe().n
 fmts = {"coo-row": sp.Format.COO_ROW, "coo-col": sp.Format.COO_COL, "ell": sp.Format.ELL,
         "ell-row": sp.Format.ELL_ROWMAJOR, "ccs": sp.Format.CCS}
 hs = {"crs": m}
+fonly = set(a.formats.split(",")) if a.formats else None
 for name, f in fmts.items():
+    if fonly and name not in fonly:
+        continue
     for _ in range(a.reps if a.transforms else 1):
         hs[name] = m.convert(f)
 x = torch.ones(n, dtype=torch.float64, device="cuda")
@@ -39,7 +43,7 @@ ks = {"crs": ("crs", sp.Kernel.CRS), "coo-row": ("coo-row", sp.Kernel.COO_ROW_OU
       "coo-col": ("coo-col", sp.Kernel.COO_COL_OUTER), "ell-inner": ("ell", sp.Kernel.ELL_INNER),
       "ell-outer": ("ell", sp.Kernel.ELL_OUTER), "ell-row": ("ell-row", sp.Kernel.ELL_ROWMAJOR)}
 for name, (h, k) in ks.items():
-    if only and name not in only:
+    if (only and name not in only) or h not in hs:
         continue
     for _ in range(a.reps):
         hs[h].spmv_device(k, x.data_ptr(), y.data_ptr())

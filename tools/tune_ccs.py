@@ -1,0 +1,23 @@
+"""Times the bucketed CRS->CCS kernels for several (coarse, sort threads)
+settings.  coarse = log2 of the coarse bucket target of the two-pass
+partition (0 = single pass)."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch  # noqa: E402
+
+from paper_2407_00019_b200 import spmvtk as sp  # noqa: E402
+
+lib = sp.load_library()
+sp.set_stream(torch.cuda.current_stream().cuda_stream)
+SETTINGS = [(0, 512), (9, 512)]
+for cfg, param in ((2, 1 << 20), (3, 128), (4, 1 << 22), (5, 1 << 21)):
+    m = sp.HostCrs(cfg, param).upload()
+    for coarse, st in SETTINGS:
+        lib.spmvtk_k_tune(b"ccs_coarse", coarse)
+        lib.spmvtk_k_tune(b"ccs_sort_threads", st)
+        t = m.transform_kernel_seconds(sp.Format.CCS, 5)
+        print(f"cfg{cfg} coarse={coarse} sort_threads={st}: {t*1e6:8.1f} us", flush=True)
+    m.free()
