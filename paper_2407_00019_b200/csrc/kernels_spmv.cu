@@ -286,31 +286,36 @@ __global__ void __launch_bounds__(256) k_spmv_vec2(int64_t n, Rows rows,
       if (lane == 0) long_rows[1 + atomicAdd(long_rows, 1)] = static_cast<int32_t>(r);
       continue;
     }
+    // row-relative 32-bit offsets from 64-bit row bases (64-bit induction
+    // variables cost ~25% on the 27-point stencil)
+    const double* __restrict__ vr = val + a;
+    const int32_t* __restrict__ cr = col + a;
+    const int32_t len = static_cast<int32_t>(b - a);
     double acc = 0.0;
-    int64_t a2 = a;
-    if ((a & 1) && a < b) {  // odd start: peel one entry
-      if (lane == 0) acc = ld_stream(val + a) * ld_x(x + ld_stream(col + a));
-      a2 = a + 1;
+    int32_t k0 = 0;
+    if ((a & 1) && len > 0) {  // odd start: peel one entry
+      if (lane == 0) acc = ld_stream(vr) * ld_x(x + ld_stream(cr));
+      k0 = 1;
     }
-    for (int64_t p = a2 + 2 * lane; p < b; p += 2 * W * U) {
+    for (int32_t p = k0 + 2 * lane; p < len; p += 2 * W * U) {
       double2 v[U];
       int2 c[U];
 #pragma unroll
       for (int j = 0; j < U; ++j) {
-        const int64_t q = p + 2 * W * j;
-        if (q + 1 < b) {
-          v[j] = ld_stream2(reinterpret_cast<const double2*>(val + q));
-          c[j] = ld_stream2(reinterpret_cast<const int2*>(col + q));
-        } else if (q < b) {
-          v[j].x = ld_stream(val + q);
-          c[j].x = ld_stream(col + q);
+        const int32_t q = p + 2 * W * j;
+        if (q + 1 < len) {
+          v[j] = ld_stream2(reinterpret_cast<const double2*>(vr + q));
+          c[j] = ld_stream2(reinterpret_cast<const int2*>(cr + q));
+        } else if (q < len) {
+          v[j].x = ld_stream(vr + q);
+          c[j].x = ld_stream(cr + q);
         }
       }
 #pragma unroll
       for (int j = 0; j < U; ++j) {
-        const int64_t q = p + 2 * W * j;
-        if (q < b) acc = fma(v[j].x, ld_x(x + c[j].x), acc);
-        if (q + 1 < b) acc = fma(v[j].y, ld_x(x + c[j].y), acc);
+        const int32_t q = p + 2 * W * j;
+        if (q < len) acc = fma(v[j].x, ld_x(x + c[j].x), acc);
+        if (q + 1 < len) acc = fma(v[j].y, ld_x(x + c[j].y), acc);
       }
     }
 #pragma unroll
@@ -740,9 +745,8 @@ void dispatch_vec(double mean, int64_t max_row, int64_t n, Rows rows, const int3
     else if (mean <= 64.0) v = 16;                              // W=8 pairs
     else v = 17;                                                // W=16 pairs
     if constexpr (!std::is_same_v<Rows, CrsRows>) {
-      // row-major ELL: with an odd band count every other row starts at an
-      // odd slot, so pair loads lose to 4 scalar lanes (profiles/r01_tune_rm.txt)
-      if (max_row % 2 == 1 && max_row <= 40) v = 12;
+      // row-major ELL takes the same choice (profiles/r01_tune_rm2.txt: the
+      // pair kernel also wins at odd band counts once its offsets are 32-bit)
       if (g_rm_variant >= 0) v = g_rm_variant;
     }
   }
