@@ -49,6 +49,13 @@ int spmvtk_k_count_descents(const int32_t* key, int64_t len,
 int spmvtk_k_expand_ptr(const int32_t* ptr, int64_t n, int64_t nnz,
                         int32_t* out_idx, void* stream);
 
+/* CRS -> COO-row in one pass (convert.cpp:11-22): col / values copied,
+ * row ids expanded from the row pointers. */
+int spmvtk_k_crs_to_coo_row(int64_t n, int64_t nnz, const int32_t* irp,
+                            const int32_t* icol, const double* val,
+                            int32_t* out_row, int32_t* out_col, double* out_val,
+                            void* stream);
+
 /* CRS -> CCS Phase I (convert.cpp:24-53).  scratch: device buffer of
  * spmvtk_k_ccs_scratch_bytes(n, nnz) bytes.  Row indices come out ascending
  * inside every column, exactly as the reference's cursor scatter. */

@@ -138,4 +138,10 @@ inline int grid_for(int64_t work, int block, int per_sm_blocks = 8) {
   return static_cast<int>(g < 1 ? 1 : g);
 }
 
+// force-load every kernel of a translation unit (lazy module loading would
+// otherwise charge the first timed call); spmvtk_k_preload calls all three
+void preload_convert();
+void preload_util();
+void preload_inverse();
+
 }  // namespace spmvtk_dev

@@ -128,6 +128,51 @@ int rows_per_warp_for(int64_t n, int64_t nnz) {
   return static_cast<int>(r);
 }
 
+// ---- CRS -> COO-row in one pass (convert.cpp:11-22) --------------------------
+// Warp per chunk of rows: the chunk's entries are copied in 32-entry batches
+// (coalesced loads / streaming stores of col and value) and the row id of
+// each entry is resolved from the row pointers in the same pass.
+__global__ void __launch_bounds__(256) k_crs_to_coo_row(const int32_t* __restrict__ ptr,
+                                                        int64_t n, int rows_per_warp,
+                                                        const int32_t* __restrict__ icol,
+                                                        const double* __restrict__ val,
+                                                        int32_t* __restrict__ out_row,
+                                                        int32_t* __restrict__ out_col,
+                                                        double* __restrict__ out_val) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t rb = warp * rows_per_warp;
+  if (rb >= n) return;
+  const int64_t re = min(rb + rows_per_warp, n);
+  const int32_t e0 = __ldg(ptr + rb), e1 = __ldg(ptr + re);
+  SegWindow w;
+  w.r0 = rb;
+  w.load(ptr, re, lane);
+  constexpr int U = 4;
+  for (int32_t base = e0; base < e1; base += 32 * U) {
+    int32_t p[U], c[U], r[U];
+    double v[U];
+    uint32_t need = 0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      p[u] = base + u * 32 + lane;
+      r[u] = 0;
+      const bool ok = p[u] < e1;
+      c[u] = ok ? ld_stream(icol + p[u]) : 0;
+      v[u] = ok ? ld_stream(val + p[u]) : 0.0;
+      if (ok) need |= 1u << u;
+    }
+    resolve_segments<U>(w, ptr, re, lane, p, r, need);
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (p[u] < e1) {
+        out_row[p[u]] = r[u];
+        out_col[p[u]] = c[u];
+        st_stream(out_val + p[u], v[u]);
+      }
+  }
+}
+
 // ---- CRS -> CCS ------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_col_hist(const int32_t* __restrict__ icol,
                                                   int64_t nnz, int32_t* count) {
@@ -984,6 +1029,18 @@ int spmvtk_k_expand_ptr(const int32_t* ptr, int64_t n, int64_t nnz, int32_t* out
   SPMVTK_LAUNCH_RETURN();
 }
 
+int spmvtk_k_crs_to_coo_row(int64_t n, int64_t nnz, const int32_t* irp, const int32_t* icol,
+                            const double* val, int32_t* out_row, int32_t* out_col,
+                            double* out_val, void* stream) {
+  if (n <= 0 || nnz <= 0) SPMVTK_LAUNCH_RETURN();
+  const int rpw = rows_per_warp_for(n, nnz);
+  const int64_t warps = (n + rpw - 1) / rpw;
+  const int64_t blocks = (warps * 32 + 255) / 256;
+  k_crs_to_coo_row<<<static_cast<unsigned>(blocks), 256, 0, as_stream(stream)>>>(
+      irp, n, rpw, icol, val, out_row, out_col, out_val);
+  SPMVTK_LAUNCH_RETURN();
+}
+
 namespace {
 struct BucketPlan {
   int shift;
@@ -1212,3 +1269,26 @@ int spmvtk_k_crs_to_ell_rm(int64_t n, int32_t nz, const int32_t* irp, const int3
 }
 
 }  // extern "C"
+
+namespace spmvtk_dev {
+void preload_convert() {
+  cudaFuncAttributes a;
+  cudaFuncGetAttributes(&a, k_expand_ptr);
+  cudaFuncGetAttributes(&a, k_crs_to_coo_row);
+  cudaFuncGetAttributes(&a, k_col_hist);
+  cudaFuncGetAttributes(&a, k_ccs_scatter);
+  cudaFuncGetAttributes(&a, k_ccs_fix_short);
+  cudaFuncGetAttributes(&a, k_ccs_fix_long);
+  cudaFuncGetAttributes(&a, k_slice_rows);
+  cudaFuncGetAttributes(&a, k_bkt_count);
+  cudaFuncGetAttributes(&a, k_bkt_scatter);
+  cudaFuncGetAttributes(&a, k_bkt_scatter_staged);
+  cudaFuncGetAttributes(&a, k_bkt_refine);
+  cudaFuncGetAttributes(&a, k_bkt_sort<256>);
+  cudaFuncGetAttributes(&a, k_bkt_sort<512>);
+  cudaFuncGetAttributes(&a, k_bkt_sort_big);
+  cudaFuncGetAttributes(&a, k_crs_to_ell_cm<32>);
+  cudaFuncGetAttributes(&a, k_crs_to_ell_cm_flat);
+  cudaFuncGetAttributes(&a, k_crs_to_ell_rm);
+}
+}  // namespace spmvtk_dev

@@ -218,3 +218,14 @@ int spmvtk_k_coo_to_crs(int64_t n, int64_t ncols, int64_t nnz, const int32_t* ro
 }
 
 }  // extern "C"
+
+namespace spmvtk_dev {
+void preload_inverse() {
+  cudaFuncAttributes a;
+  cudaFuncGetAttributes(&a, k_seg_sort_short);
+  cudaFuncGetAttributes(&a, k_seg_sort_long);
+  cudaFuncGetAttributes(&a, k_ell_gather);
+  cudaFuncGetAttributes(&a, k_hist_keys);
+  cudaFuncGetAttributes(&a, k_coo_scatter);
+}
+}  // namespace spmvtk_dev

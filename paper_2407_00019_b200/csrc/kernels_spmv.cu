@@ -903,6 +903,9 @@ int spmvtk_k_tune(const char* key, int value) {
 
 int spmvtk_k_preload(void) {
   // touching the attributes of every kernel forces module load
+  spmvtk_dev::preload_convert();
+  spmvtk_dev::preload_util();
+  spmvtk_dev::preload_inverse();
   cudaFuncAttributes a;
   cudaFuncGetAttributes(&a, k_spmv_crs_long);
   cudaFuncGetAttributes(&a, k_spmv_coo_row);

@@ -288,3 +288,17 @@ int spmvtk_k_exclusive_scan(const int32_t* in, int32_t* out, int64_t n,
 }
 
 }  // extern "C"
+
+namespace spmvtk_dev {
+void preload_util() {
+  cudaFuncAttributes a;
+  cudaFuncGetAttributes(&a, k_row_stats);
+  cudaFuncGetAttributes(&a, k_narrow);
+  cudaFuncGetAttributes(&a, k_widen);
+  cudaFuncGetAttributes(&a, k_out_of_range);
+  cudaFuncGetAttributes(&a, k_descents);
+  cudaFuncGetAttributes(&a, k_scan_tiles);
+  cudaFuncGetAttributes(&a, k_scan_tile_sums);
+  cudaFuncGetAttributes(&a, k_scan_apply);
+}
+}  // namespace spmvtk_dev

@@ -276,11 +276,10 @@ Matrix* convert(const Matrix& a, spmvtk_format to, std::uint64_t max_bytes) {
       m->col.reset(nnz, "COO col_idx");
       m->val.reset(nnz, "COO values");
       cudaStream_t st = rt::stream();
-      if (nnz) {
-        rt::check(cudaMemcpyAsync(m->col.get(), a.col.get(), a.col.bytes(), cudaMemcpyDeviceToDevice, st), "COO copy");
-        rt::check(cudaMemcpyAsync(m->val.get(), a.val.get(), a.val.bytes(), cudaMemcpyDeviceToDevice, st), "COO copy");
-        rt::check_launch(spmvtk_k_expand_ptr(a.ptr.get(), n, nnz, m->row.get(), st), "expand rows");
-      }
+      if (nnz)
+        rt::check_launch(spmvtk_k_crs_to_coo_row(n, nnz, a.ptr.get(), a.col.get(), a.val.get(),
+                                                 m->row.get(), m->col.get(), m->val.get(), st),
+                         "CRS->COO-row");
       return m.release();
     }
     case SPMVTK_FORMAT_CCS:
@@ -440,9 +439,10 @@ double transform_kernel_seconds(const Matrix& a, spmvtk_format to, int repeats) 
         cudaMemcpyAsync(out->val.get(), a.val.get(), a.val.bytes(), cudaMemcpyDeviceToDevice, st);
         break;
       case SPMVTK_FORMAT_COO_ROW:
-        cudaMemcpyAsync(out->col.get(), a.col.get(), a.col.bytes(), cudaMemcpyDeviceToDevice, st);
-        cudaMemcpyAsync(out->val.get(), a.val.get(), a.val.bytes(), cudaMemcpyDeviceToDevice, st);
-        rt::check_launch(spmvtk_k_expand_ptr(a.ptr.get(), n, nnz, out->row.get(), st), "expand");
+        rt::check_launch(spmvtk_k_crs_to_coo_row(n, nnz, a.ptr.get(), a.col.get(), a.val.get(),
+                                                 out->row.get(), out->col.get(), out->val.get(),
+                                                 st),
+                         "CRS->COO-row");
         break;
       case SPMVTK_FORMAT_CCS:
       case SPMVTK_FORMAT_COO_COL:
