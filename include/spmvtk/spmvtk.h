@@ -294,6 +294,64 @@ double spmvtk_find_d_star(const double* d_mat, const double* r, size_t count, do
 /* Library build / device description (for reports). */
 const char* spmvtk_version(void);
 
+/* ---- multi-GPU exchange folded into the SpMV (SURVEY.md §8e stretch) ----
+ * Row-block SpMV x_{t+1} = A x_t with one process per GPU: instead of an
+ * all-gather after the product, the SpMV epilogue stores every result row
+ * straight into the next-x buffers of the ranks that need it (peer memory
+ * over NVLink / NVSwitch), and a flag per (source, step) orders the steps.
+ *
+ * Buffers live in cudaMalloc'ed memory shared through CUDA IPC handles.
+ * dst[w] must point at THIS shard's first row inside rank w's buffer (so
+ * row r of the shard lands at dst[w][r]); mask (device, one byte per local
+ * row, may be NULL = all ranks) selects the ranks that read row r (bit w). */
+#define SPMVTK_MAX_PEERS 8
+#define SPMVTK_IPC_HANDLE_BYTES 64
+typedef struct spmvtk_push {
+  double* dst[SPMVTK_MAX_PEERS];
+  const uint8_t* mask;
+  int32_t ndst;
+} spmvtk_push;
+/* flag targets: ptr[w] = address of this rank's flag slot inside rank w's
+ * flag array (system-scope release stores). */
+typedef struct spmvtk_flag_targets {
+  uint64_t* ptr[SPMVTK_MAX_PEERS];
+  int32_t n;
+} spmvtk_flag_targets;
+/* Step synchronisation done INSIDE the pushed SpMV kernel: every CTA first
+ * waits until wait_flags[s] >= wait_value (s < nwait; bounded by timeout_ns,
+ * bit 0 of *status set on timeout), and the last CTA to finish (counter:
+ * device word, zero, reset by the kernel) stores signal_value to every
+ * signal target after all CTAs' pushes are fenced.  One launch per step. */
+typedef struct spmvtk_push_sync {
+  const uint64_t* wait_flags;
+  int32_t nwait;
+  uint64_t wait_value;
+  uint64_t timeout_ns;
+  uint32_t* status;
+  spmvtk_flag_targets signal;
+  uint64_t signal_value;
+  uint32_t* counter;
+} spmvtk_push_sync;
+
+/* cudaMalloc + zero + IPC handle (handle: SPMVTK_IPC_HANDLE_BYTES bytes). */
+spmvtk_status spmvtk_ipc_alloc(uint64_t bytes, void** dev_ptr, void* handle);
+spmvtk_status spmvtk_ipc_free(void* dev_ptr);
+/* Maps a peer's allocation (cudaIpcOpenMemHandle, lazy peer access). */
+spmvtk_status spmvtk_ipc_open(const void* handle, void** dev_ptr);
+spmvtk_status spmvtk_ipc_close(void* dev_ptr);
+/* SpMV of a CRS (kernel CRS) or ELL (kernel ELL_INNER) handle whose result
+ * rows are pushed to push->dst instead of a local y; sync (may be NULL)
+ * folds the step's flag wait and signal into the same kernel. */
+spmvtk_status spmvtk_spmv_device_push(const spmvtk_matrix* m, spmvtk_kernel kernel,
+                                      const double* x, const spmvtk_push* push,
+                                      const spmvtk_push_sync* sync);
+/* After the preceding work on the stream: *targets->ptr[w] = value for all w
+ * (system-scope release).  wait: until flags[s] >= value for s < n, or the
+ * timeout (ns) passes, in which case bit 0 of *status (device) is set. */
+spmvtk_status spmvtk_flags_signal(const spmvtk_flag_targets* targets, uint64_t value);
+spmvtk_status spmvtk_flags_wait(const uint64_t* flags, int32_t n, uint64_t value,
+                                uint64_t timeout_ns, uint32_t* status);
+
 #ifdef __cplusplus
 } /* extern "C" */
 #endif

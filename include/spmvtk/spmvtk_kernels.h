@@ -155,6 +155,30 @@ int spmvtk_k_spmv_ell_rm(int64_t n, int32_t nz, const double* val,
                          const int32_t* col, const double* x, double* y,
                          void* stream);
 
+/* ---- pushed results (multi-GPU, spmvtk.h "exchange folded into the SpMV")
+ * Same products as spmvtk_k_spmv_crs / spmvtk_k_spmv_ell_cm; row r of the
+ * result goes to dst[w][r] for every w with bit w of mask[r] (mask NULL =
+ * all), then each thread fences at system scope; sync (may be NULL): the
+ * step's flag wait (kernel prologue) and signal (last CTA) in the same launch. */
+struct spmvtk_push;
+struct spmvtk_push_sync;
+int spmvtk_k_spmv_crs_push(int64_t n, const int32_t* irp, const int32_t* icol,
+                           const double* val, const double* x,
+                           const struct spmvtk_push* push,
+                           const struct spmvtk_push_sync* sync, double mean_row,
+                           int32_t max_row, int32_t* long_rows, void* stream);
+int spmvtk_k_spmv_ell_cm_push(int64_t n, int32_t nz, int64_t ld, const double* val,
+                              const int32_t* col, const double* x,
+                              const struct spmvtk_push* push,
+                              const struct spmvtk_push_sync* sync, void* stream);
+/* Step flags (system scope): signal stores value to every target; wait
+ * spins (one thread per source) until flags[s] >= value or timeout_ns. */
+struct spmvtk_flag_targets;
+int spmvtk_k_flags_signal(const struct spmvtk_flag_targets* targets, uint64_t value,
+                          void* stream);
+int spmvtk_k_flags_wait(const uint64_t* flags, int32_t n, uint64_t value,
+                        uint64_t timeout_ns, uint32_t* status, void* stream);
+
 /* Tuning override for experiments ("crs_variant": -1 = heuristic, 0..9 pick
  * a (lanes per row, rows per sub-warp) instance of the CRS kernel). */
 int spmvtk_k_tune(const char* key, int value);

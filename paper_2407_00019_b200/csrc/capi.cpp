@@ -21,6 +21,7 @@
 #include "mmio.hpp"
 #include "runtime.hpp"
 #include "spmvtk/spmvtk.h"
+#include "spmvtk/spmvtk_kernels.h"
 
 using namespace spmvtk;
 
@@ -587,6 +588,82 @@ spmvtk_status spmvtk_transform_kernel_seconds(const spmvtk_matrix* m, spmvtk_for
     const dev::Matrix& a = crs_of(m);
     if (!valid_format(to)) throw Error(ErrorCode::InvalidArgument, "unknown target format");
     *seconds = dev::transform_kernel_seconds(a, to, repeats);
+  });
+}
+
+// ---- multi-GPU push exchange (spmvtk.h) -----------------------------------
+static_assert(sizeof(cudaIpcMemHandle_t) == SPMVTK_IPC_HANDLE_BYTES, "IPC handle size");
+
+spmvtk_status spmvtk_ipc_alloc(uint64_t bytes, void** dev_ptr, void* handle) {
+  return guarded([&] {
+    need(dev_ptr, "null output");
+    need(handle, "null handle buffer");
+    rt::init();
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, static_cast<std::size_t>(bytes));
+    if (e == cudaErrorMemoryAllocation) {
+      cudaGetLastError();
+      throw Error(ErrorCode::MemoryLimit, "IPC buffer: device allocation of " +
+                                              std::to_string(bytes) + " bytes failed");
+    }
+    rt::check(e, "IPC buffer");
+    rt::check(cudaMemset(p, 0, static_cast<std::size_t>(bytes)), "IPC buffer zero");
+    cudaIpcMemHandle_t h;
+    e = cudaIpcGetMemHandle(&h, p);
+    if (e != cudaSuccess) {
+      cudaFree(p);
+      rt::check(e, "cudaIpcGetMemHandle");
+    }
+    std::memcpy(handle, &h, sizeof(h));
+    *dev_ptr = p;
+  });
+}
+
+spmvtk_status spmvtk_ipc_free(void* dev_ptr) {
+  return guarded([&] {
+    if (dev_ptr) rt::check(cudaFree(dev_ptr), "IPC buffer free");
+  });
+}
+
+spmvtk_status spmvtk_ipc_open(const void* handle, void** dev_ptr) {
+  return guarded([&] {
+    need(handle, "null handle");
+    need(dev_ptr, "null output");
+    rt::init();
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof(h));
+    rt::check(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess),
+              "cudaIpcOpenMemHandle");
+  });
+}
+
+spmvtk_status spmvtk_ipc_close(void* dev_ptr) {
+  return guarded([&] {
+    if (dev_ptr) rt::check(cudaIpcCloseMemHandle(dev_ptr), "cudaIpcCloseMemHandle");
+  });
+}
+
+spmvtk_status spmvtk_spmv_device_push(const spmvtk_matrix* m, spmvtk_kernel kernel,
+                                      const double* x, const spmvtk_push* push,
+                                      const spmvtk_push_sync* sync) {
+  return guarded([&] {
+    if (!m || !push || (!x && m->n > 0)) throw Error(ErrorCode::InvalidArgument, "null argument");
+    dev::spmv_device_push(*m, kernel, x, *push, sync);
+  });
+}
+
+spmvtk_status spmvtk_flags_signal(const spmvtk_flag_targets* targets, uint64_t value) {
+  return guarded([&] {
+    need(targets, "null targets");
+    rt::check_launch(spmvtk_k_flags_signal(targets, value, rt::stream()), "flags signal");
+  });
+}
+
+spmvtk_status spmvtk_flags_wait(const uint64_t* flags, int32_t n, uint64_t value,
+                                uint64_t timeout_ns, uint32_t* status) {
+  return guarded([&] {
+    rt::check_launch(spmvtk_k_flags_wait(flags, n, value, timeout_ns, status, rt::stream()),
+                     "flags wait");
   });
 }
 

@@ -8,10 +8,12 @@
 // /root/reference/proj/src/spmv.cpp; each kernel below names the one it
 // replaces.  Summation orders differ from the reference (fp64, FMA), which the
 // contract allows (max-norm relative 1e-12, BASELINE.json north_star).
+#include <algorithm>
 #include <string>
 #include <type_traits>
 
 #include "common.cuh"
+#include "spmvtk/spmvtk.h"
 #include "spmvtk/spmvtk_kernels.h"
 
 using namespace spmvtk_dev;
@@ -23,6 +25,75 @@ __device__ __forceinline__ unsigned subwarp_mask(int W) {
   const int lane = threadIdx.x & 31;
   return ((1u << W) - 1u) << (lane & ~(W - 1));
 }
+
+// ---- where a result row goes -------------------------------------------
+// PlainOut: y[r].  PushOut: the row-block multi-GPU exchange folded into the
+// epilogue -- row r is stored to every rank that reads it (dst[w] points at
+// this shard's rows inside rank w's next-x buffer, peer memory over NVLink),
+// and each thread fences at system scope before it exits so a later flag
+// store (spmvtk_k_flags_signal) orders after all of its pushes.
+struct PlainOut {
+  double* __restrict__ y;
+  __device__ __forceinline__ void begin() const {}
+  __device__ __forceinline__ void put(int64_t r, double v) const { y[r] = v; }
+  __device__ __forceinline__ void done() const {}
+};
+
+__device__ __forceinline__ uint64_t ld_acquire_sys_u64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+struct PushOut {
+  spmvtk_push p;
+  spmvtk_push_sync s;  // nwait = 0 / counter = NULL switch the pieces off
+  // every thread of every CTA, before x is read: the step's flag wait
+  __device__ __forceinline__ void begin() const {
+    if (s.nwait <= 0) return;
+    if (threadIdx.x == 0 && *reinterpret_cast<volatile uint32_t*>(s.status) == 0) {
+      const uint64_t t0 = globaltimer_ns();
+      for (int w = 0; w < s.nwait; ++w)
+        while (ld_acquire_sys_u64(s.wait_flags + w) < s.wait_value) {
+          if (globaltimer_ns() - t0 > s.timeout_ns) {
+            atomicOr(s.status, 1u);
+            break;
+          }
+          __nanosleep(32);
+        }
+    }
+    __syncthreads();
+  }
+  __device__ __forceinline__ void put(int64_t r, double v) const {
+    const unsigned m = p.mask ? __ldg(p.mask + r) : 0xffu;
+#pragma unroll
+    for (int w = 0; w < SPMVTK_MAX_PEERS; ++w)
+      if (w < p.ndst && ((m >> w) & 1u)) p.dst[w][r] = v;
+  }
+  // every thread of every CTA, at the end: fence the pushes at system scope;
+  // the last CTA to arrive stores the step flag to every rank
+  __device__ __forceinline__ void done() const {
+    if (p.ndst > 1) __threadfence_system();
+    if (s.counter == nullptr) return;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const unsigned prev = atomicAdd(s.counter, 1u);
+      if (prev == gridDim.x - 1) {
+        *s.counter = 0;
+        __threadfence_system();
+        for (int w = 0; w < s.signal.n; ++w)
+          asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(s.signal.ptr[w]),
+                       "l"(s.signal_value)
+                       : "memory");
+      }
+    }
+  }
+};
 
 // ---- vector CRS: W lanes per row (spmv_crs, spmv.cpp:64-75) --------------
 // Row extents come from a policy so the same kernel serves CRS (irp) and
@@ -44,13 +115,14 @@ struct EllRowMajorRows {
   }
 };
 
-template <int W, int U, typename Rows>
+template <int W, int U, typename Rows, typename Out = PlainOut>
 __global__ void __launch_bounds__(256) k_spmv_vec(int64_t n, Rows rows,
                                                   const int32_t* __restrict__ col,
                                                   const double* __restrict__ val,
                                                   const double* __restrict__ x,
-                                                  double* __restrict__ y, int64_t long_limit,
+                                                  Out y, int64_t long_limit,
                                                   int32_t* long_rows, bool hint) {
+  y.begin();
   const int lane = threadIdx.x & (W - 1);
   const unsigned mask = subwarp_mask(W);
   const int64_t nsub = (static_cast<int64_t>(gridDim.x) * blockDim.x) / W;
@@ -82,8 +154,9 @@ __global__ void __launch_bounds__(256) k_spmv_vec(int64_t n, Rows rows,
     }
 #pragma unroll
     for (int o = W / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(mask, acc, o, W);
-    if (lane == 0) y[r] = acc;
+    if (lane == 0) y.put(r, acc);
   }
+  y.done();
 }
 
 // ---- multi-row vector CRS -------------------------------------------------
@@ -268,13 +341,14 @@ __global__ void __launch_bounds__(256) k_spmv_tile(int64_t n, Rows rows,
 // (one double2 value load + one int2 index load): half the load
 // instructions and L1 wavefronts per entry of the scalar kernel.  A row
 // starting at an odd position has its first entry taken by lane 0 alone.
-template <int W, int U, typename Rows>
+template <int W, int U, typename Rows, typename Out = PlainOut>
 __global__ void __launch_bounds__(256) k_spmv_vec2(int64_t n, Rows rows,
                                                    const int32_t* __restrict__ col,
                                                    const double* __restrict__ val,
                                                    const double* __restrict__ x,
-                                                   double* __restrict__ y, int64_t long_limit,
+                                                   Out y, int64_t long_limit,
                                                    int32_t* long_rows) {
+  y.begin();
   const int lane = threadIdx.x & (W - 1);
   const unsigned mask = subwarp_mask(W);
   const int64_t nsub = (static_cast<int64_t>(gridDim.x) * blockDim.x) / W;
@@ -320,16 +394,18 @@ __global__ void __launch_bounds__(256) k_spmv_vec2(int64_t n, Rows rows,
     }
 #pragma unroll
     for (int o = W / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(mask, acc, o, W);
-    if (lane == 0) y[r] = acc;
+    if (lane == 0) y.put(r, acc);
   }
+  y.done();
 }
 
 // block per long row (queue filled by k_spmv_vec / k_spmv_multi)
+template <typename Out = PlainOut>
 __global__ void __launch_bounds__(256) k_spmv_crs_long(const int32_t* __restrict__ irp,
                                                        const int32_t* __restrict__ col,
                                                        const double* __restrict__ val,
                                                        const double* __restrict__ x,
-                                                       double* __restrict__ y,
+                                                       Out y,
                                                        const int32_t* long_rows) {
   __shared__ double s_part[8];
   const int32_t count = *long_rows;
@@ -358,10 +434,11 @@ __global__ void __launch_bounds__(256) k_spmv_crs_long(const int32_t* __restrict
     if (threadIdx.x == 0) {
       double t = 0.0;
       for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t += s_part[w];
-      y[r] = t;
+      y.put(r, t);
     }
     __syncthreads();
   }
+  y.done();
 }
 
 // ---- COO row-ordered: deterministic warp-segmented reduction -------------
@@ -602,16 +679,14 @@ __global__ void __launch_bounds__(256) k_spmv_coo_col(int64_t nnz,
 // thread, fully coalesced (ld is a multiple of 32 so every band starts
 // 256-byte aligned).  Bands are walked in order with U loads in flight.
 // Every slot is multiplied, padding included (the ELL contract).
+// one row pair (i, i+1) over bands [k_begin, k_end)
 template <int U, bool H>
-__global__ void __launch_bounds__(256) k_spmv_ell_cm(int64_t n, int32_t k_begin, int32_t k_end,
-                                                     int64_t ld, const double* __restrict__ val,
-                                                     const int32_t* __restrict__ col,
-                                                     const double* __restrict__ x,
-                                                     double* __restrict__ y) {
-  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t i = 2 * t;
-  if (i >= n) return;
-  double a0 = 0.0, a1 = 0.0;
+__device__ __forceinline__ void ell_pair(int64_t i, int32_t k_begin, int32_t k_end, int64_t ld,
+                                         const double* __restrict__ val,
+                                         const int32_t* __restrict__ col,
+                                         const double* __restrict__ x, double& a0, double& a1) {
+  a0 = 0.0;
+  a1 = 0.0;
   const double2* vp = reinterpret_cast<const double2*>(val + i);
   const int2* cp = reinterpret_cast<const int2*>(col + i);
   const int64_t step = ld >> 1;  // in double2 / int2 units
@@ -644,9 +719,37 @@ __global__ void __launch_bounds__(256) k_spmv_ell_cm(int64_t n, int32_t k_begin,
     a0 = fma(v.x, lx(c.x), a0);
     a1 = fma(v.y, lx(c.y), a1);
   }
-  // rows past n in the last pair are ld padding: their result is dropped
-  y[i] = a0;
-  if (i + 1 < n) y[i + 1] = a1;
+}
+
+template <int U, bool H, typename Out = PlainOut>
+__global__ void __launch_bounds__(256) k_spmv_ell_cm(int64_t n, int32_t k_begin, int32_t k_end,
+                                                     int64_t ld, const double* __restrict__ val,
+                                                     const int32_t* __restrict__ col,
+                                                     const double* __restrict__ x,
+                                                     Out y) {
+  const int64_t t0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  double a0, a1;
+  if constexpr (std::is_same_v<Out, PlainOut>) {
+    // one pair per thread, the grid covers every pair
+    const int64_t i = 2 * t0;
+    if (i >= n) return;
+    ell_pair<U, H>(i, k_begin, k_end, ld, val, col, x, a0, a1);
+    // rows past n in the last pair are ld padding: their result is dropped
+    y.put(i, a0);
+    if (i + 1 < n) y.put(i + 1, a1);
+  } else {
+    // pushed results: a capped grid walks the pairs, so the per-CTA step
+    // handshake (flag wait, arrival count) stays cheap; no early return,
+    // done() synchronises the CTA
+    y.begin();
+    for (int64_t t = t0; 2 * t < n; t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+      const int64_t i = 2 * t;
+      ell_pair<U, H>(i, k_begin, k_end, ld, val, col, x, a0, a1);
+      y.put(i, a0);
+      if (i + 1 < n) y.put(i + 1, a1);
+    }
+    y.done();
+  }
 }
 
 // band-split variant (spmv_ell_outer): chunk s of the bands writes
@@ -712,11 +815,11 @@ int g_l2_hint = 0;  // L2 evict_first (matrix) / evict_last (x) policies
 int g_coo_variant = 1;  // 1: 4 entries per lane (k_spmv_coo_row4), 0: scalar
 int g_rm_variant = -1;  // row-major ELL variant override (tuning)
 
-template <int W, int U, typename Rows>
+template <int W, int U, typename Rows, typename Out>
 void launch_vec(int64_t n, Rows rows, const int32_t* col, const double* val, const double* x,
-                double* y, int64_t long_limit, int32_t* long_rows, cudaStream_t s) {
+                Out y, int64_t long_limit, int32_t* long_rows, cudaStream_t s) {
   const int64_t threads = n * W;
-  k_spmv_vec<W, U, Rows><<<grid_for(threads, 256, 8), 256, 0, s>>>(
+  k_spmv_vec<W, U, Rows, Out><<<grid_for(threads, 256, 8), 256, 0, s>>>(
       n, rows, col, val, x, y, long_limit, long_rows, g_l2_hint != 0);
 }
 
@@ -730,9 +833,9 @@ void launch_multi(int64_t n, Rows rows, const int32_t* col, const double* val, c
 
 int g_crs_variant = -1;  // tuning override (spmvtk_k_tune), -1 = heuristic
 
-template <typename Rows>
+template <typename Rows, typename Out>
 void dispatch_vec(double mean, int64_t max_row, int64_t n, Rows rows, const int32_t* col,
-                  const double* val, const double* x, double* y, int64_t long_limit,
+                  const double* val, const double* x, Out y, int64_t long_limit,
                   int32_t* long_rows, cudaStream_t s) {
   int v = g_crs_variant;
   if (v < 0) {
@@ -750,15 +853,19 @@ void dispatch_vec(double mean, int64_t max_row, int64_t n, Rows rows, const int3
       if (g_rm_variant >= 0) v = g_rm_variant;
     }
   }
+  if constexpr (!std::is_same_v<Out, PlainOut>) {
+    // pushed results: the multi-row / tiled variants have no push epilogue
+    if (v < 11 && v != 0) v = 18;
+  }
   switch (v) {
     case 15: case 16: case 17: case 18: case 19: {
       const int64_t W = v == 15 ? 4 : v == 16 ? 8 : v == 17 ? 16 : v == 18 ? 4 : 8;
       const int blocks = grid_for(n * W, 256, 8);
-      if (v == 15) k_spmv_vec2<4, 2, Rows><<<blocks, 256, 0, s>>>(n, rows, col, val, x, y, long_limit, long_rows);
-      if (v == 16) k_spmv_vec2<8, 1, Rows><<<blocks, 256, 0, s>>>(n, rows, col, val, x, y, long_limit, long_rows);
-      if (v == 17) k_spmv_vec2<16, 1, Rows><<<blocks, 256, 0, s>>>(n, rows, col, val, x, y, long_limit, long_rows);
-      if (v == 18) k_spmv_vec2<4, 1, Rows><<<blocks, 256, 0, s>>>(n, rows, col, val, x, y, long_limit, long_rows);
-      if (v == 19) k_spmv_vec2<8, 2, Rows><<<blocks, 256, 0, s>>>(n, rows, col, val, x, y, long_limit, long_rows);
+      if (v == 15) k_spmv_vec2<4, 2, Rows, Out><<<blocks, 256, 0, s>>>(n, rows, col, val, x, y, long_limit, long_rows);
+      if (v == 16) k_spmv_vec2<8, 1, Rows, Out><<<blocks, 256, 0, s>>>(n, rows, col, val, x, y, long_limit, long_rows);
+      if (v == 17) k_spmv_vec2<16, 1, Rows, Out><<<blocks, 256, 0, s>>>(n, rows, col, val, x, y, long_limit, long_rows);
+      if (v == 18) k_spmv_vec2<4, 1, Rows, Out><<<blocks, 256, 0, s>>>(n, rows, col, val, x, y, long_limit, long_rows);
+      if (v == 19) k_spmv_vec2<8, 2, Rows, Out><<<blocks, 256, 0, s>>>(n, rows, col, val, x, y, long_limit, long_rows);
       break;
     }
     case 11: launch_vec<8, 2>(n, rows, col, val, x, y, long_limit, long_rows, s); break;
@@ -766,20 +873,27 @@ void dispatch_vec(double mean, int64_t max_row, int64_t n, Rows rows, const int3
     case 13: launch_vec<32, 4>(n, rows, col, val, x, y, long_limit, long_rows, s); break;
     case 14: launch_vec<32, 2>(n, rows, col, val, x, y, long_limit, long_rows, s); break;
     case 0: launch_vec<16, 2>(n, rows, col, val, x, y, long_limit, long_rows, s); break;
-    case 1: launch_multi<4, 4>(n, rows, col, val, x, y, long_limit, long_rows, s); break;
-    case 2: launch_multi<8, 4>(n, rows, col, val, x, y, long_limit, long_rows, s); break;
-    case 3: launch_multi<16, 4>(n, rows, col, val, x, y, long_limit, long_rows, s); break;
-    case 4: launch_multi<32, 4>(n, rows, col, val, x, y, long_limit, long_rows, s); break;
-    case 5: launch_multi<8, 2>(n, rows, col, val, x, y, long_limit, long_rows, s); break;
-    case 6: launch_multi<8, 8>(n, rows, col, val, x, y, long_limit, long_rows, s); break;
-    case 7: launch_multi<16, 8>(n, rows, col, val, x, y, long_limit, long_rows, s); break;
-    case 8: launch_multi<4, 2>(n, rows, col, val, x, y, long_limit, long_rows, s); break;
-    case 9: launch_multi<16, 2>(n, rows, col, val, x, y, long_limit, long_rows, s); break;
-    case 10:
-      k_spmv_tile<Rows><<<static_cast<unsigned>((n + kTileRows - 1) / kTileRows), kTileRows, 0,
-                          s>>>(n, rows, col, val, x, y);
+    default:
+      if constexpr (std::is_same_v<Out, PlainOut>) {
+        double* yy = y.y;
+        switch (v) {
+          case 1: launch_multi<4, 4>(n, rows, col, val, x, yy, long_limit, long_rows, s); break;
+          case 2: launch_multi<8, 4>(n, rows, col, val, x, yy, long_limit, long_rows, s); break;
+          case 3: launch_multi<16, 4>(n, rows, col, val, x, yy, long_limit, long_rows, s); break;
+          case 4: launch_multi<32, 4>(n, rows, col, val, x, yy, long_limit, long_rows, s); break;
+          case 5: launch_multi<8, 2>(n, rows, col, val, x, yy, long_limit, long_rows, s); break;
+          case 6: launch_multi<8, 8>(n, rows, col, val, x, yy, long_limit, long_rows, s); break;
+          case 7: launch_multi<16, 8>(n, rows, col, val, x, yy, long_limit, long_rows, s); break;
+          case 8: launch_multi<4, 2>(n, rows, col, val, x, yy, long_limit, long_rows, s); break;
+          case 9: launch_multi<16, 2>(n, rows, col, val, x, yy, long_limit, long_rows, s); break;
+          case 10:
+            k_spmv_tile<Rows><<<static_cast<unsigned>((n + kTileRows - 1) / kTileRows), kTileRows,
+                                0, s>>>(n, rows, col, val, x, yy);
+            break;
+          default: launch_multi<8, 4>(n, rows, col, val, x, yy, long_limit, long_rows, s); break;
+        }
+      }
       break;
-    default: launch_multi<8, 4>(n, rows, col, val, x, y, long_limit, long_rows, s); break;
   }
 }
 
@@ -795,9 +909,62 @@ int spmvtk_k_spmv_crs(int64_t n, const int32_t* irp, const int32_t* icol, const 
   const int64_t long_limit = spmvtk_k_crs_long_limit(mean_row);
   const bool use_long = long_rows != nullptr && max_row > long_limit;
   if (use_long) cudaMemsetAsync(long_rows, 0, sizeof(int32_t), s);
-  dispatch_vec(mean_row, max_row, n, CrsRows{irp}, icol, val, x, y,
+  dispatch_vec(mean_row, max_row, n, CrsRows{irp}, icol, val, x, PlainOut{y},
                use_long ? long_limit : INT64_MAX, long_rows, s);
-  if (use_long) k_spmv_crs_long<<<kSMs * 4, 256, 0, s>>>(irp, icol, val, x, y, long_rows);
+  if (use_long)
+    k_spmv_crs_long<<<kSMs * 4, 256, 0, s>>>(irp, icol, val, x, PlainOut{y}, long_rows);
+  SPMVTK_LAUNCH_RETURN();
+}
+
+namespace {
+spmvtk_push_sync no_sync() {
+  spmvtk_push_sync z{};
+  return z;
+}
+// an empty shard launches no SpMV: its step still waits and signals
+int sync_only(const spmvtk_push_sync* sync, void* stream) {
+  if (sync == nullptr) SPMVTK_LAUNCH_RETURN();
+  if (sync->nwait > 0) {
+    const int rc = spmvtk_k_flags_wait(sync->wait_flags, sync->nwait, sync->wait_value,
+                                       sync->timeout_ns, sync->status, stream);
+    if (rc) return rc;
+  }
+  if (sync->counter != nullptr) return spmvtk_k_flags_signal(&sync->signal, sync->signal_value, stream);
+  SPMVTK_LAUNCH_RETURN();
+}
+bool bad_push(const spmvtk_push* push, const spmvtk_push_sync* sync) {
+  if (push == nullptr || push->ndst < 1 || push->ndst > SPMVTK_MAX_PEERS) return true;
+  if (sync && (sync->nwait < 0 || sync->nwait > SPMVTK_MAX_PEERS ||
+               (sync->nwait > 0 && (sync->wait_flags == nullptr || sync->status == nullptr)) ||
+               sync->signal.n < 0 || sync->signal.n > SPMVTK_MAX_PEERS))
+    return true;
+  return false;
+}
+}  // namespace
+
+int spmvtk_k_spmv_crs_push(int64_t n, const int32_t* irp, const int32_t* icol,
+                           const double* val, const double* x, const spmvtk_push* push,
+                           const spmvtk_push_sync* sync, double mean_row, int32_t max_row,
+                           int32_t* long_rows, void* stream) {
+  cudaStream_t s = as_stream(stream);
+  if (bad_push(push, sync)) return static_cast<int>(cudaErrorInvalidValue);
+  if (n <= 0) return sync_only(sync, stream);
+  const int64_t long_limit = spmvtk_k_crs_long_limit(mean_row);
+  const bool use_long = long_rows != nullptr && max_row > long_limit;
+  if (use_long) cudaMemsetAsync(long_rows, 0, sizeof(int32_t), s);
+  PushOut vec{*push, sync ? *sync : no_sync()};
+  if (use_long) {
+    // the long-row pass runs after the vector kernel: it signals, the
+    // vector kernel only waits
+    PushOut lng = vec;
+    vec.s.counter = nullptr;
+    vec.s.signal.n = 0;
+    lng.s.nwait = 0;
+    dispatch_vec(mean_row, max_row, n, CrsRows{irp}, icol, val, x, vec, long_limit, long_rows, s);
+    k_spmv_crs_long<<<kSMs * 4, 256, 0, s>>>(irp, icol, val, x, lng, long_rows);
+  } else {
+    dispatch_vec(mean_row, max_row, n, CrsRows{irp}, icol, val, x, vec, INT64_MAX, long_rows, s);
+  }
   SPMVTK_LAUNCH_RETURN();
 }
 
@@ -845,9 +1012,22 @@ int spmvtk_k_spmv_ell_cm(int64_t n, int32_t nz, int64_t ld, const double* val,
   const int64_t pairs = (n + 1) / 2;
   const unsigned blocks = static_cast<unsigned>((pairs + 255) / 256);
   if (g_l2_hint)
-    k_spmv_ell_cm<4, true><<<blocks, 256, 0, s>>>(n, 0, nz, ld, val, col, x, y);
+    k_spmv_ell_cm<4, true><<<blocks, 256, 0, s>>>(n, 0, nz, ld, val, col, x, PlainOut{y});
   else
-    k_spmv_ell_cm<4, false><<<blocks, 256, 0, s>>>(n, 0, nz, ld, val, col, x, y);
+    k_spmv_ell_cm<4, false><<<blocks, 256, 0, s>>>(n, 0, nz, ld, val, col, x, PlainOut{y});
+  SPMVTK_LAUNCH_RETURN();
+}
+
+int spmvtk_k_spmv_ell_cm_push(int64_t n, int32_t nz, int64_t ld, const double* val,
+                              const int32_t* col, const double* x, const spmvtk_push* push,
+                              const spmvtk_push_sync* sync, void* stream) {
+  cudaStream_t s = as_stream(stream);
+  if (bad_push(push, sync)) return static_cast<int>(cudaErrorInvalidValue);
+  if (n <= 0) return sync_only(sync, stream);
+  const int64_t pairs = (n + 1) / 2;
+  const unsigned blocks = static_cast<unsigned>((pairs + 255) / 256);
+  k_spmv_ell_cm<4, false, PushOut><<<std::min<unsigned>(blocks, kSMs * 8), 256, 0, s>>>(
+      n, 0, nz, ld, val, col, x, PushOut{*push, sync ? *sync : no_sync()});
   SPMVTK_LAUNCH_RETURN();
 }
 
@@ -869,7 +1049,7 @@ int spmvtk_k_spmv_ell_rm(int64_t n, int32_t nz, const double* val, const int32_t
                          const double* x, double* y, void* stream) {
   cudaStream_t s = as_stream(stream);
   if (n <= 0) SPMVTK_LAUNCH_RETURN();
-  dispatch_vec(static_cast<double>(nz), nz, n, EllRowMajorRows{nz}, col, val, x, y, INT64_MAX,
+  dispatch_vec(static_cast<double>(nz), nz, n, EllRowMajorRows{nz}, col, val, x, PlainOut{y}, INT64_MAX,
                nullptr, s);
   SPMVTK_LAUNCH_RETURN();
 }
@@ -907,7 +1087,13 @@ int spmvtk_k_preload(void) {
   spmvtk_dev::preload_util();
   spmvtk_dev::preload_inverse();
   cudaFuncAttributes a;
-  cudaFuncGetAttributes(&a, k_spmv_crs_long);
+  cudaFuncGetAttributes(&a, k_spmv_crs_long<PlainOut>);
+  cudaFuncGetAttributes(&a, k_spmv_crs_long<PushOut>);
+  cudaFuncGetAttributes(&a, k_spmv_ell_cm<4, false, PushOut>);
+  cudaFuncGetAttributes(&a, k_spmv_vec2<4, 1, CrsRows, PushOut>);
+  cudaFuncGetAttributes(&a, k_spmv_vec2<8, 1, CrsRows, PushOut>);
+  cudaFuncGetAttributes(&a, k_spmv_vec2<16, 1, CrsRows, PushOut>);
+  cudaFuncGetAttributes(&a, k_spmv_vec<4, 2, CrsRows, PushOut>);
   cudaFuncGetAttributes(&a, k_spmv_coo_row);
   cudaFuncGetAttributes(&a, k_spmv_coo_row4);
   cudaFuncGetAttributes(&a, k_spmv_coo_col);

@@ -4,6 +4,7 @@
 // HBM-bound integer work: grid-stride loops sized to a multiple of the 148
 // SMs, warp-shuffle reductions, one atomic per warp.
 #include "common.cuh"
+#include "spmvtk/spmvtk.h"
 #include "spmvtk/spmvtk_kernels.h"
 
 using namespace spmvtk_dev;
@@ -225,6 +226,46 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_apply(const int32_t* __re
   if (blockIdx.x == tiles - 1 && threadIdx.x == kScanThreads - 1) out[n] = run;
 }
 
+// ---- step flags of the pushed multi-GPU SpMV ------------------------------
+// signal: one thread per target, system-scope release store of the step
+// number into this rank's slot of a peer's flag array.  wait: one thread per
+// source, acquire loads until the source's flag reaches the step; bounded by
+// a timeout (globaltimer) so a lost peer cannot hang the GPU -- the caller
+// reads *status afterwards.
+__global__ void k_flags_signal(spmvtk_flag_targets t, uint64_t value) {
+  const int w = threadIdx.x;
+  if (w < t.n)
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(t.ptr[w]), "l"(value) : "memory");
+}
+
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+__global__ void k_flags_wait(const uint64_t* flags, int n, uint64_t value, uint64_t timeout_ns,
+                             uint32_t* status) {
+  const int w = threadIdx.x;
+  if (w >= n) return;
+  // an earlier step already timed out: fail fast instead of once per step
+  if (*reinterpret_cast<volatile uint32_t*>(status) != 0) return;
+  if (ld_acquire_sys(flags + w) >= value) return;
+  const uint64_t t0 = global_ns();
+  while (ld_acquire_sys(flags + w) < value) {
+    if (global_ns() - t0 > timeout_ns) {
+      atomicOr(status, 1u);
+      return;
+    }
+    __nanosleep(64);
+  }
+}
+
 }  // namespace
 
 extern "C" {
@@ -292,6 +333,8 @@ int spmvtk_k_exclusive_scan(const int32_t* in, int32_t* out, int64_t n,
 namespace spmvtk_dev {
 void preload_util() {
   cudaFuncAttributes a;
+  cudaFuncGetAttributes(&a, k_flags_signal);
+  cudaFuncGetAttributes(&a, k_flags_wait);
   cudaFuncGetAttributes(&a, k_row_stats);
   cudaFuncGetAttributes(&a, k_narrow);
   cudaFuncGetAttributes(&a, k_widen);
@@ -302,3 +345,24 @@ void preload_util() {
   cudaFuncGetAttributes(&a, k_scan_apply);
 }
 }  // namespace spmvtk_dev
+
+extern "C" {
+
+int spmvtk_k_flags_signal(const spmvtk_flag_targets* targets, uint64_t value, void* stream) {
+  if (targets == nullptr || targets->n < 0 || targets->n > SPMVTK_MAX_PEERS)
+    return static_cast<int>(cudaErrorInvalidValue);
+  if (targets->n == 0) SPMVTK_LAUNCH_RETURN();
+  k_flags_signal<<<1, 32, 0, as_stream(stream)>>>(*targets, value);
+  SPMVTK_LAUNCH_RETURN();
+}
+
+int spmvtk_k_flags_wait(const uint64_t* flags, int32_t n, uint64_t value, uint64_t timeout_ns,
+                        uint32_t* status, void* stream) {
+  if (n < 0 || n > SPMVTK_MAX_PEERS || (n > 0 && (flags == nullptr || status == nullptr)))
+    return static_cast<int>(cudaErrorInvalidValue);
+  if (n == 0) SPMVTK_LAUNCH_RETURN();
+  k_flags_wait<<<1, 32, 0, as_stream(stream)>>>(flags, n, value, timeout_ns, status);
+  SPMVTK_LAUNCH_RETURN();
+}
+
+}  // extern "C"

@@ -599,6 +599,40 @@ void spmv_device(const Matrix& m, spmvtk_kernel kernel, const double* x, double*
   throw Error(ErrorCode::InvalidArgument, "unknown kernel id");
 }
 
+void spmv_device_push(const Matrix& m, spmvtk_kernel kernel, const double* x,
+                      const spmvtk_push& push, const spmvtk_push_sync* sync) {
+  if (push.ndst < 1 || push.ndst > SPMVTK_MAX_PEERS)
+    throw Error(ErrorCode::InvalidArgument, "push needs 1..8 destinations");
+  for (int w = 0; w < push.ndst; ++w)
+    if (push.dst[w] == nullptr && m.n > 0)
+      throw Error(ErrorCode::InvalidArgument, "null push destination");
+  cudaStream_t st = rt::stream();
+  if (kernel == SPMVTK_KERNEL_CRS) {
+    if (m.format != SPMVTK_FORMAT_CRS)
+      throw Error(ErrorCode::InvalidArgument, "operation requires a CRS handle");
+    rt::Moments mo = crs_moments(m);
+    const double mean = m.n > 0 ? static_cast<double>(mo.sum) / static_cast<double>(m.n) : 0;
+    DevArray<std::int32_t> long_rows;
+    if (static_cast<std::int64_t>(mo.max) > spmvtk_k_crs_long_limit(mean))
+      long_rows.reset(m.n + 1, "CRS long-row queue");
+    rt::check_launch(spmvtk_k_spmv_crs_push(m.n, m.ptr.get(), m.col.get(), m.val.get(), x, &push,
+                                            sync, mean,
+                                            static_cast<std::int32_t>(std::min<std::uint64_t>(mo.max, INT32_MAX)),
+                                            long_rows.get(), st),
+                     "spmv crs (push)");
+    return;
+  }
+  if (kernel == SPMVTK_KERNEL_ELL_INNER) {
+    if (m.format != SPMVTK_FORMAT_ELL)
+      throw Error(ErrorCode::InvalidArgument, "kernel requires an ELL handle");
+    rt::check_launch(spmvtk_k_spmv_ell_cm_push(m.n, m.band_count, m.ld, m.val.get(), m.col.get(),
+                                               x, &push, sync, st),
+                     "spmv ell-inner (push)");
+    return;
+  }
+  throw Error(ErrorCode::InvalidArgument, "pushed SpMV supports the CRS and ELL_INNER kernels");
+}
+
 std::int64_t device_array(const Matrix& m, spmvtk_array which, void** out) {
   const DevArray<std::int32_t>* ia = nullptr;
   switch (which) {

@@ -91,6 +91,10 @@ double transform_kernel_seconds(const Matrix& crs, spmvtk_format to, int repeats
 // InvalidArgument when the kernel does not match the handle's format (or
 // COO ordering), with the reference's messages (capi.cpp:230-252).
 void spmv_device(const Matrix& m, spmvtk_kernel kernel, const double* x, double* y);
+// SpMV whose result rows are pushed to peer buffers (spmvtk_spmv_device_push):
+// CRS (kernel CRS) and band-major ELL (kernel ELL_INNER)
+void spmv_device_push(const Matrix& m, spmvtk_kernel kernel, const double* x,
+                      const spmvtk_push& push, const spmvtk_push_sync* sync);
 
 // True when `kernel` on `m` can be launched on row sub-ranges (CRS, ELL
 // band-major inner, row-major ELL): rows are independent and y is written

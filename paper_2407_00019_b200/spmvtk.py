@@ -115,6 +115,27 @@ class MatrixDesc(C.Structure):
                 ("device_bytes", C.c_uint64), ("ncols", C.c_int64), ("row_offset", C.c_int64)]
 
 
+MAX_PEERS = 8
+IPC_HANDLE_BYTES = 64
+
+
+class Push(C.Structure):
+    """spmvtk_push: destinations of pushed result rows (spmvtk.h)."""
+    _fields_ = [("dst", C.c_void_p * MAX_PEERS), ("mask", C.c_void_p), ("ndst", C.c_int32)]
+
+
+class FlagTargets(C.Structure):
+    """spmvtk_flag_targets: this rank's flag slot in every peer's array."""
+    _fields_ = [("ptr", C.c_void_p * MAX_PEERS), ("n", C.c_int32)]
+
+
+class PushSync(C.Structure):
+    """spmvtk_push_sync: the step's flag wait / signal inside the SpMV launch."""
+    _fields_ = [("wait_flags", C.c_void_p), ("nwait", C.c_int32), ("wait_value", C.c_uint64),
+                ("timeout_ns", C.c_uint64), ("status", C.c_void_p), ("signal", FlagTargets),
+                ("signal_value", C.c_uint64), ("counter", C.c_void_p)]
+
+
 class RowStats(C.Structure):
     _fields_ = [("n", C.c_int64), ("nnz", C.c_int64), ("max_row", C.c_int64),
                 ("mu", C.c_double), ("sigma", C.c_double), ("d_mat", C.c_double)]
@@ -178,6 +199,13 @@ SIGNATURES = {
     "spmvtk_conversion_bytes": (C.c_int, [_P, C.c_int, C.POINTER(_u64), C.POINTER(_u64)]),
     "spmvtk_transform_kernel_seconds": (C.c_int, [_P, C.c_int, C.c_int, _pd]),
     "spmvtk_reserve_device_memory": (C.c_int, [_u64]),
+    "spmvtk_ipc_alloc": (C.c_int, [_u64, _PP, _P]),
+    "spmvtk_ipc_free": (C.c_int, [_P]),
+    "spmvtk_ipc_open": (C.c_int, [_P, _PP]),
+    "spmvtk_ipc_close": (C.c_int, [_P]),
+    "spmvtk_spmv_device_push": (C.c_int, [_P, C.c_int, _P, C.POINTER(Push), _P]),
+    "spmvtk_flags_signal": (C.c_int, [C.POINTER(FlagTargets), _u64]),
+    "spmvtk_flags_wait": (C.c_int, [_P, C.c_int32, _u64, _u64, _P]),
     "spmvtk_compute_metrics": (C.c_int, [_d, _d, _d, _pd, _pd, _pd]),
     "spmvtk_amortization_iterations": (C.c_int, [_d, _d, _d, C.POINTER(_i64)]),
     "spmvtk_find_d_star": (_d, [_pd, _pd, C.c_size_t, _d]),
@@ -386,6 +414,15 @@ class Matrix:
         _check(self._lib.spmvtk_spmv_device(self._h, int(kernel), C.c_void_p(x_ptr),
                                             C.c_void_p(y_ptr)))
 
+    def spmv_device_push(self, kernel: Kernel, x_ptr: int, push: "Push",
+                         sync: "PushSync | None" = None) -> None:
+        """SpMV with the result rows stored to push.dst[w] (multi-GPU
+        exchange folded into the product; CRS and ELL_INNER); `sync` folds
+        the step's flag wait and signal into the same launch."""
+        _check(self._lib.spmvtk_spmv_device_push(
+            self._h, int(kernel), C.c_void_p(x_ptr), C.byref(push),
+            C.cast(C.byref(sync), C.c_void_p) if sync is not None else None))
+
     def write_matrix_market(self, path: str) -> None:
         _check(self._lib.spmvtk_write_matrix_market(self._h, path.encode()))
 
@@ -397,6 +434,39 @@ class Matrix:
 
 def reserve_device_memory(nbytes: int) -> None:
     _check(load_library().spmvtk_reserve_device_memory(int(nbytes)))
+
+
+def ipc_alloc(nbytes: int) -> tuple[int, bytes]:
+    """cudaMalloc'ed, zeroed device buffer + its 64-byte CUDA IPC handle."""
+    p = C.c_void_p()
+    h = C.create_string_buffer(IPC_HANDLE_BYTES)
+    _check(load_library().spmvtk_ipc_alloc(int(nbytes), C.byref(p), h))
+    return int(p.value), h.raw
+
+
+def ipc_free(ptr: int) -> None:
+    _check(load_library().spmvtk_ipc_free(C.c_void_p(ptr)))
+
+
+def ipc_open(handle: bytes) -> int:
+    """Maps a peer process's buffer into this process (device pointer)."""
+    p = C.c_void_p()
+    buf = C.create_string_buffer(bytes(handle), IPC_HANDLE_BYTES)
+    _check(load_library().spmvtk_ipc_open(buf, C.byref(p)))
+    return int(p.value)
+
+
+def ipc_close(ptr: int) -> None:
+    _check(load_library().spmvtk_ipc_close(C.c_void_p(ptr)))
+
+
+def flags_signal(targets: "FlagTargets", value: int) -> None:
+    _check(load_library().spmvtk_flags_signal(C.byref(targets), int(value)))
+
+
+def flags_wait(flags_ptr: int, n: int, value: int, timeout_ns: int, status_ptr: int) -> None:
+    _check(load_library().spmvtk_flags_wait(C.c_void_p(flags_ptr), int(n), int(value),
+                                            int(timeout_ns), C.c_void_p(status_ptr)))
 
 
 def bench(m: Matrix, variant: Kernel, lanes: int = 1, repeats: int = 9,

@@ -113,3 +113,82 @@ def test_dist_iteration_gloo(world):
         want = port_lib.spmv_crs(n, rp, ci, v, want)
     for r in range(world):
         assert results[r].tobytes() == want.tobytes(), r
+
+
+def _push_worker(rank, world, port, n, rp0, ci0, v, x0, steps, q):
+    """The push exchange's semantics with gloo standing in for NVLink stores:
+    masks from the gathered needed-column sets, each source's rows delivered
+    only where its mask says; own rows must follow the full iteration."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle.oracle import Port
+    port_lib = Port()
+    r0, lrp, lci, lv = D.shard_arrays(rp0, ci0, v, n, world, rank)
+    chunk = D.block_rows(n, world)
+    npad = chunk * world
+    need = D.needed_columns(torch.from_numpy(lci.astype(np.int32)), npad).to(torch.uint8)
+    allneed = [torch.empty(npad, dtype=torch.uint8) for _ in range(world)]
+    dist.all_gather(allneed, need)
+    allneed = torch.stack(allneed).bool()
+    masks_local = D.push_mask(allneed, rank, chunk)
+    masks = [torch.empty(chunk, dtype=torch.uint8) for _ in range(world)]
+    dist.all_gather(masks, masks_local)
+    x = torch.zeros(npad, dtype=torch.float64)
+    x[:n] = torch.from_numpy(x0)
+    for _ in range(steps):
+        xx = x[:n].numpy()
+        y = (port_lib.spmv_crs(chunk, lrp + 1, lci + 1, lv, xx) if lci.size
+             else np.zeros(chunk))
+        ys = [torch.empty(chunk, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(ys, torch.from_numpy(y))
+        x_next = torch.full((npad,), float("nan"), dtype=torch.float64)  # stale = poison
+        D.apply_pushes(ys, masks, rank, chunk, x_next)
+        x = x_next
+    q.put((rank, x[r0: r0 + chunk].numpy().copy(), masks_local.numpy().copy()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,kind", [(2, "banded"), (3, "random")])
+def test_push_exchange_semantics_gloo(world, kind):
+    rng = np.random.default_rng(5 + world)
+    n = 400
+    if kind == "banded":
+        rows = [np.arange(max(0, i - 4), min(n, i + 5)) for i in range(n)]
+    else:
+        rows = [np.sort(rng.choice(n, size=10, replace=False)) for _ in range(n)]
+    ci0 = np.concatenate(rows).astype(np.int64)
+    rp0 = np.concatenate([[0], np.cumsum([len(r) for r in rows])]).astype(np.int64)
+    v = rng.standard_normal(ci0.shape[0])
+    x0 = rng.uniform(-1, 1, n)
+    steps = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_push_worker,
+                         args=(r, world, port, n, rp0, ci0, v, x0, steps, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    results = {}
+    for _ in range(world):
+        r, xr, m = q.get(timeout=120)
+        results[r] = (xr, m)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    from oracle.oracle import Port
+    port_lib = Port()
+    want = x0.copy()
+    for _ in range(steps):
+        want = port_lib.spmv_crs(n, rp0 + 1, ci0 + 1, v, want)
+    chunk = D.block_rows(n, world)
+    for r in range(world):
+        a, b = D.block_range(n, world, r)
+        assert results[r][0][: b - a].tobytes() == want[a:b].tobytes(), r
+    if kind == "banded":
+        # only the 4-row halos cross between neighbouring ranks
+        m0 = results[0][1].astype(np.int32)
+        assert ((m0 >> 1) & 1).sum() == 4
+        assert (m0 & 1).all()
