@@ -148,7 +148,7 @@ __global__ void __launch_bounds__(256) k_crs_to_coo_row(const int32_t* __restric
   SegWindow w;
   w.r0 = rb;
   w.load(ptr, re, lane);
-  constexpr int U = 4;
+  constexpr int U = 8;
   for (int32_t base = e0; base < e1; base += 32 * U) {
     int32_t p[U], c[U], r[U];
     double v[U];
@@ -934,40 +934,59 @@ __global__ void __launch_bounds__(256) k_crs_to_ell_cm(int64_t n, int32_t nz, in
   }
 }
 
-// Band-major, short bands (nz <= 32): the block's 64 rows are one
-// contiguous CRS range of at most 2048 entries, copied to shared memory with
-// fully coalesced loads, then written band by band.
-constexpr int kFlatRows = 64;
-constexpr int kFlatCap = kFlatRows * 32;
+// Band-major, short bands (nz <= 32): the block's ROWS rows are one
+// contiguous CRS range of at most ROWS*32 entries, copied to shared memory
+// with fully coalesced loads (all of a thread's loads in flight before any
+// shared store), then written band by band (ROWS consecutive rows per band).
+int g_ell_flat_rows = 64;  // tuning: 64 or 128 rows per CTA (64 measured faster)
 
-__global__ void __launch_bounds__(256) k_crs_to_ell_cm_flat(int64_t n, int32_t nz, int64_t ld,
-                                                            const int32_t* __restrict__ irp,
-                                                            const int32_t* __restrict__ icol,
-                                                            const double* __restrict__ val,
-                                                            double* __restrict__ out_val,
-                                                            int32_t* __restrict__ out_col,
-                                                            int32_t* __restrict__ out_count,
-                                                            int64_t pad_base) {
+template <int ROWS, int THREADS>
+__global__ void __launch_bounds__(THREADS) k_crs_to_ell_cm_flat(int64_t n, int32_t nz, int64_t ld,
+                                                                const int32_t* __restrict__ irp,
+                                                                const int32_t* __restrict__ icol,
+                                                                const double* __restrict__ val,
+                                                                double* __restrict__ out_val,
+                                                                int32_t* __restrict__ out_col,
+                                                                int32_t* __restrict__ out_count,
+                                                                int64_t pad_base) {
+  constexpr int kCap = ROWS * 32;
   // staged entry f lives at f + f/32: rows of exactly 16 or 32 entries read
   // in the write phase (one row per lane) would otherwise all hit one bank
-  __shared__ int32_t s_ptr[kFlatRows + 1];
-  __shared__ double s_v[kFlatCap + kFlatCap / 32];
-  __shared__ int32_t s_c[kFlatCap + kFlatCap / 32];
-  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * kFlatRows;
-  for (int t = threadIdx.x; t <= kFlatRows; t += blockDim.x)
-    s_ptr[t] = __ldg(irp + min(r0 + t, n));
+  extern __shared__ unsigned char s_raw[];
+  double* s_v = reinterpret_cast<double*>(s_raw);
+  int32_t* s_c = reinterpret_cast<int32_t*>(s_v + kCap + kCap / 32);
+  __shared__ int32_t s_ptr[ROWS + 1];
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * ROWS;
+  for (int t = threadIdx.x; t <= ROWS; t += THREADS) s_ptr[t] = __ldg(irp + min(r0 + t, n));
   __syncthreads();
-  const int32_t e0 = s_ptr[0], cnt = s_ptr[kFlatRows] - e0;
-  for (int f = threadIdx.x; f < cnt; f += blockDim.x) {
-    s_v[f + (f >> 5)] = ld_stream(val + e0 + f);
-    s_c[f + (f >> 5)] = ld_stream(icol + e0 + f);
+  const int32_t e0 = s_ptr[0], cnt = s_ptr[ROWS] - e0;
+  {
+    constexpr int kPer = kCap / THREADS;
+    double v[kPer];
+    int32_t c[kPer];
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const int f = threadIdx.x + k * THREADS;
+      if (f < cnt) {
+        v[k] = ld_stream(val + e0 + f);
+        c[k] = ld_stream(icol + e0 + f);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const int f = threadIdx.x + k * THREADS;
+      if (f < cnt) {
+        s_v[f + (f >> 5)] = v[k];
+        s_c[f + (f >> 5)] = c[k];
+      }
+    }
   }
-  for (int t = threadIdx.x; t < kFlatRows; t += blockDim.x)
+  for (int t = threadIdx.x; t < ROWS; t += THREADS)
     if (r0 + t < n) out_count[r0 + t] = s_ptr[t + 1] - s_ptr[t];
   __syncthreads();
-  const int slots = nz * kFlatRows;
-  for (int f = threadIdx.x; f < slots; f += blockDim.x) {
-    const int k = f / kFlatRows, row = f % kFlatRows;
+  const int slots = nz * ROWS;
+  for (int f = threadIdx.x; f < slots; f += THREADS) {
+    const int k = f / ROWS, row = f % ROWS;
     const int64_t i = r0 + row;
     if (i >= ld) continue;
     const int32_t a = s_ptr[row], len = s_ptr[row + 1] - a;
@@ -999,18 +1018,34 @@ __global__ void __launch_bounds__(256) k_crs_to_ell_rm(int64_t n, int32_t nz, Fa
     out_count[r0 + t] = s_ptr[t + 1] - s_ptr[t];
   const uint32_t slots = static_cast<uint32_t>(rows) * static_cast<uint32_t>(nz);
   const int64_t base = r0 * nz;
-  for (uint32_t f = threadIdx.x; f < slots; f += blockDim.x) {
-    const uint32_t row = div_nz.div(f);
-    const int32_t k = static_cast<int32_t>(f - row * static_cast<uint32_t>(nz));
-    const int32_t a = s_ptr[row], len = s_ptr[row + 1] - a;
-    double v = 0.0;
-    int32_t c = static_cast<int32_t>(pad_base + r0 + row);
-    if (k < len) {
-      v = ld_stream(val + a + k);
-      c = ld_stream(icol + a + k);
+  constexpr int U = 4;  // slots per thread with their loads in flight together
+  for (uint32_t f0 = threadIdx.x; f0 < slots; f0 += U * blockDim.x) {
+    double v[U];
+    int32_t c[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t f = f0 + u * blockDim.x;
+      v[u] = 0.0;
+      c[u] = 0;
+      if (f < slots) {
+        const uint32_t row = div_nz.div(f);
+        const int32_t k = static_cast<int32_t>(f - row * static_cast<uint32_t>(nz));
+        const int32_t a = s_ptr[row], len = s_ptr[row + 1] - a;
+        c[u] = static_cast<int32_t>(pad_base + r0 + row);
+        if (k < len) {
+          v[u] = ld_stream(val + a + k);
+          c[u] = ld_stream(icol + a + k);
+        }
+      }
     }
-    st_stream(out_val + base + f, v);
-    out_col[base + f] = c;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t f = f0 + u * blockDim.x;
+      if (f < slots) {
+        st_stream(out_val + base + f, v[u]);
+        out_col[base + f] = c[u];
+      }
+    }
   }
 }
 
@@ -1075,6 +1110,10 @@ int spmvtk_k_tune_convert(const char* key, int value) {
   }
   if (key && std::string(key) == "ccs_sort_threads") {
     g_ccs_sort_threads = value == 256 ? 256 : 512;
+    return 0;
+  }
+  if (key && std::string(key) == "ell_flat_rows") {
+    g_ell_flat_rows = value == 64 ? 64 : 128;
     return 0;
   }
   if (key && std::string(key) == "ccs_coarse") {
@@ -1241,9 +1280,21 @@ int spmvtk_k_crs_to_ell_cm(int64_t n, int32_t nz, int64_t ld, const int32_t* irp
                                                 out_count, pad_base);
   };
   if (nz <= 32) {
-    unsigned blocks = static_cast<unsigned>((ld + kFlatRows - 1) / kFlatRows);
-    k_crs_to_ell_cm_flat<<<blocks, 256, 0, s>>>(n, nz, ld, irp, icol, val, out_val, out_col,
-                                                out_count, pad_base);
+    static const bool attrs = [] {
+      cudaFuncSetAttribute(k_crs_to_ell_cm_flat<128, 512>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (4096 + 128) * 12);
+      return true;
+    }();
+    (void)attrs;
+    if (g_ell_flat_rows == 64) {
+      unsigned blocks = static_cast<unsigned>((ld + 63) / 64);
+      k_crs_to_ell_cm_flat<64, 256><<<blocks, 256, (2048 + 64) * 12, s>>>(
+          n, nz, ld, irp, icol, val, out_val, out_col, out_count, pad_base);
+    } else {
+      unsigned blocks = static_cast<unsigned>((ld + 127) / 128);
+      k_crs_to_ell_cm_flat<128, 512><<<blocks, 512, (4096 + 128) * 12, s>>>(
+          n, nz, ld, irp, icol, val, out_val, out_col, out_count, pad_base);
+    }
   } else if (nz <= 4) launch(std::integral_constant<int, 4>{});
   else if (nz <= 8) launch(std::integral_constant<int, 8>{});
   else if (nz <= 16) launch(std::integral_constant<int, 16>{});
@@ -1288,7 +1339,8 @@ void preload_convert() {
   cudaFuncGetAttributes(&a, k_bkt_sort<512>);
   cudaFuncGetAttributes(&a, k_bkt_sort_big);
   cudaFuncGetAttributes(&a, k_crs_to_ell_cm<32>);
-  cudaFuncGetAttributes(&a, k_crs_to_ell_cm_flat);
+  cudaFuncGetAttributes(&a, k_crs_to_ell_cm_flat<64, 256>);
+  cudaFuncGetAttributes(&a, k_crs_to_ell_cm_flat<128, 512>);
   cudaFuncGetAttributes(&a, k_crs_to_ell_rm);
 }
 }  // namespace spmvtk_dev
