@@ -24,82 +24,6 @@ using namespace spmvtk_dev;
 
 namespace {
 
-// A window of 32 consecutive segments [r0, r0+32) of a pointer array; lane l
-// holds the end of segment r0+l (ptr[r0+l+1]) or INT_MAX past the last
-// segment of the chunk.  offset(p) = number of segments of the window that
-// end at or before p, i.e. the segment of entry p relative to r0, valid when
-// ptr[r0] <= p < end.
-struct SegWindow {
-  int64_t r0;
-  int32_t s;
-  int32_t end;
-
-  __device__ __forceinline__ void load(const int32_t* ptr, int64_t r_end, int lane) {
-    int64_t r = r0 + lane + 1;
-    s = (r <= r_end) ? __ldg(ptr + r) : INT_MAX;
-    end = __shfl_sync(kFull, s, 31);
-  }
-  __device__ __forceinline__ int offset(int32_t p) const {
-    int lo = 0;
-#pragma unroll
-    for (int step = 16; step >= 1; step >>= 1) {
-      int32_t v = __shfl_sync(kFull, s, lo + step - 1);
-      if (v <= p) lo += step;
-    }
-    return lo;
-  }
-};
-
-// Segment id of entry p for every lane with `need` set; warp-uniform advance
-// of the window over segments (empty ones included) until all lanes resolve.
-__device__ __forceinline__ int32_t resolve_segment(SegWindow& w, const int32_t* ptr,
-                                                   int64_t r_end, int lane, int32_t p,
-                                                   bool need) {
-  int32_t seg = 0;
-  for (;;) {
-    bool in = need && p < w.end;
-    int off = w.offset(p);
-    if (in) {
-      seg = static_cast<int32_t>(w.r0 + off);
-      need = false;
-    }
-    if (!__any_sync(kFull, need)) break;
-    w.r0 += 32;
-    w.load(ptr, r_end, lane);
-  }
-  return seg;
-}
-
-// resolve_segment for U positions per lane at once: the U binary searches
-// are independent shuffle chains, so their latencies overlap.
-template <int U>
-__device__ __forceinline__ void resolve_segments(SegWindow& w, const int32_t* ptr,
-                                                 int64_t r_end, int lane, const int32_t (&p)[U],
-                                                 int32_t (&seg)[U], uint32_t need) {
-  for (;;) {
-    int lo[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) lo[u] = 0;
-#pragma unroll
-    for (int step = 16; step >= 1; step >>= 1) {
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int32_t v = __shfl_sync(kFull, w.s, lo[u] + step - 1);
-        if (v <= p[u]) lo[u] += step;
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (((need >> u) & 1u) && p[u] < w.end) {
-        seg[u] = static_cast<int32_t>(w.r0 + lo[u]);
-        need &= ~(1u << u);
-      }
-    if (!__any_sync(kFull, need != 0)) break;
-    w.r0 += 32;
-    w.load(ptr, r_end, lane);
-  }
-}
-
 // ---- pointer expansion ---------------------------------------------------
 __global__ void __launch_bounds__(256) k_expand_ptr(const int32_t* __restrict__ ptr,
                                                     int64_t n, int rows_per_warp,

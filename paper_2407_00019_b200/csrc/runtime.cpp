@@ -1,6 +1,8 @@
 // runtime.cpp -- see runtime.hpp.
 #include "runtime.hpp"
 
+#include <cstdlib>
+
 #include <cmath>
 #include <cstdint>
 #include <mutex>
@@ -37,6 +39,8 @@ void init() {
     check(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold),
           "cudaMemPoolSetAttribute");
     check(static_cast<cudaError_t>(spmvtk_k_preload()), "kernel preload");
+    // test hook: force a CRS kernel variant for a whole process
+    if (const char* v = std::getenv("SPMVTK_CRS_VARIANT")) spmvtk_k_tune("crs_variant", std::atoi(v));
   });
 }
 
