@@ -190,20 +190,41 @@ class PushSpMV:
         self.h, self.k, self.group = handle, kernel, group
         self.timeout_ns = int(timeout_s * 1e9)
         npad = self.chunk * world
-        # own buffers: X0, X1, flags (IPC-shareable cudaMalloc memory)
-        self.own = [sp.ipc_alloc(npad * 8), sp.ipc_alloc(npad * 8), sp.ipc_alloc(world * 8)]
-        handles = [h for _, h in self.own]
+        # Every collective below is reached by every rank whatever happens
+        # locally: a local failure is turned into an agreed one (all-reduce
+        # MIN) so no rank is left waiting in a collective the others skipped.
+        self.own, self.opened, self.peer = [], [], []
+        handles, err = None, None
+        try:  # own buffers: X0, X1, flags (IPC-shareable cudaMalloc memory)
+            self.own = [sp.ipc_alloc(npad * 8), sp.ipc_alloc(npad * 8),
+                        sp.ipc_alloc(world * 8)]
+            handles = [h for _, h in self.own]
+        except Exception as e:  # noqa: BLE001
+            err = e
         allh = [None] * world
         dist.all_gather_object(allh, handles, group=group)
-        self.opened = []
-        self.peer = []
-        for w in range(world):
-            if w == rank:
-                self.peer.append([p for p, _ in self.own])
-            else:
-                ptrs = [sp.ipc_open(h) for h in allh[w]]
-                self.opened.extend(ptrs)
-                self.peer.append(ptrs)
+        if err is None and any(h is None for h in allh):
+            err = RuntimeError("a peer could not allocate its IPC buffers")
+        if err is None:
+            try:
+                for w in range(world):
+                    if w == rank:
+                        self.peer.append([p for p, _ in self.own])
+                    else:
+                        ptrs = [sp.ipc_open(h) for h in allh[w]]
+                        self.opened.extend(ptrs)
+                        self.peer.append(ptrs)
+            except Exception as e:  # noqa: BLE001
+                err = e
+        ok = torch.tensor([0.0 if err else 1.0], device="cuda")
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
+        if ok.item() != 1.0:
+            for p in self.opened:
+                sp.ipc_close(p)
+            for p, _ in self.own:
+                sp.ipc_free(p)
+            self.own, self.opened = [], []
+            raise RuntimeError(f"push exchange unavailable: {err or 'failed on a peer'}")
         self.status = torch.zeros(1, dtype=torch.int32, device="cuda")
         # mask: which ranks read each of my rows
         self.mask = None
