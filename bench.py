@@ -10,9 +10,11 @@ measured; the per-format table, the transform times in CRS-SpMV units and
 the AT decision are reported beside the headline).  `value` = algorithmic
 bytes of one SpMV (GPU layout) x steps / device time, inputs
 resident in HBM (the matrix, 222 MB, is larger than the 126 MB L2, so no
-flush is needed between steps).  `e2e` = the same metric through the
-reference-facing C ABI call spmvtk_spmv() with pinned HOST x / y, copies
-inside the timed region.
+flush is needed between steps).  `e2e` = the same metric through the C ABI
+with pinned HOST x / y, every step's copy-in and copy-out inside the timed
+region: the streaming spmvtk_pipeline_* calls (products overlap each
+other's copies), and under e2e.sync the reference's synchronous
+spmvtk_spmv().
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 """
@@ -340,12 +342,30 @@ def impl_ours(args):
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
         h.spmv(xn, k, 1, out=yn)
-    t_e2e = (time.perf_counter() - t0) / e2e_steps
-    ych = y.cpu().numpy()
+    t_e2e_sync = (time.perf_counter() - t0) / e2e_steps
     h.spmv_device(k, x.data_ptr(), y.data_ptr())
     torch.cuda.synchronize()
     assert np.allclose(yn, y.cpu().numpy(), rtol=1e-12, atol=0), "e2e result mismatch"
-    del ych
+    # streaming: spmvtk_pipeline_submit keeps products in flight, so one
+    # product's copy-in, another's SpMV and a third's copy-out overlap (PCIe
+    # is full duplex); every step still copies its own x in and its y out
+    xs = [xh, torch.from_numpy(sp.gen_vector(n, args.seed + 2)).pin_memory()]
+    ys = [torch.empty(n, dtype=torch.float64).pin_memory() for _ in range(2)]
+    pipe = sp.Pipeline(h, k)
+    for i in range(4):
+        pipe.submit(xs[i % 2].numpy(), ys[i % 2].numpy())
+    pipe.wait()
+    t0 = time.perf_counter()
+    for i in range(e2e_steps):
+        pipe.submit(xs[i % 2].numpy(), ys[i % 2].numpy())
+    pipe.wait()
+    t_e2e = (time.perf_counter() - t0) / e2e_steps
+    for i in range(2):
+        xd = xs[i].cuda()
+        h.spmv_device(k, xd.data_ptr(), y.data_ptr())
+        torch.cuda.synchronize()
+        assert np.array_equal(ys[i].numpy(), y.cpu().numpy()), "streaming e2e mismatch"
+    pipe.free()
 
     # ---- the same kernels on config 3 (27-point stencil: x gathers are local,
     # so SpMV meets the HBM roofline there; config 2's random columns make
@@ -412,7 +432,10 @@ def impl_ours(args):
                      "kernel": best, "bytes_per_launch": bytes_step},
         "e2e": {"value": bytes_step / t_e2e / 1e9, "unit": "GB/s", "h2d_bytes_per_step": 8 * n,
                 "d2h_bytes_per_step": 8 * n, "ms_per_step": t_e2e * 1e3,
-                "api": "spmvtk_spmv (C ABI, pinned host x/y)"},
+                "api": "spmvtk_pipeline_submit/wait (C ABI streaming host SpMV, pinned "
+                       "host x/y, copies of one product overlap other products)",
+                "sync": {"value": bytes_step / t_e2e_sync / 1e9, "ms_per_step": t_e2e_sync * 1e3,
+                         "api": "spmvtk_spmv (the reference's synchronous call)"}},
         "gpu_launches": args.steps * launches_per_step,
         "clocks": clk.summary(),
         "formats": table, "transforms": transforms,

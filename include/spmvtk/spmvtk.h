@@ -294,6 +294,21 @@ double spmvtk_find_d_star(const double* d_mat, const double* r, size_t count, do
 /* Library build / device description (for reports). */
 const char* spmvtk_version(void);
 
+/* ---- streaming host SpMV -------------------------------------------------
+ * A pipeline for many products with one handle and host vectors: submit
+ * enqueues H2D(x) -> SpMV -> D2H(y) on three streams with double-buffered
+ * device staging and returns at once, so the copy-in of one product, the
+ * SpMV of another and the copy-out of a third overlap (PCIe is full duplex).
+ * x and y must stay untouched until spmvtk_pipeline_wait returns; pinned
+ * host memory is needed for the copies to be asynchronous.  Every product
+ * is exactly the one spmvtk_spmv computes. */
+typedef struct spmvtk_pipeline spmvtk_pipeline;
+spmvtk_status spmvtk_pipeline_create(const spmvtk_matrix* m, spmvtk_kernel kernel,
+                                     spmvtk_pipeline** out);
+spmvtk_status spmvtk_pipeline_submit(spmvtk_pipeline* p, const double* x, double* y);
+spmvtk_status spmvtk_pipeline_wait(spmvtk_pipeline* p);
+void spmvtk_pipeline_free(spmvtk_pipeline* p);
+
 /* ---- multi-GPU exchange folded into the SpMV (SURVEY.md §8e stretch) ----
  * Row-block SpMV x_{t+1} = A x_t with one process per GPU: instead of an
  * all-gather after the product, the SpMV epilogue stores every result row

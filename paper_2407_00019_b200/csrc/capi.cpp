@@ -310,6 +310,96 @@ spmvtk_status spmvtk_spmv(const spmvtk_matrix* m, spmvtk_kernel kernel, const do
   });
 }
 
+// ---- streaming host SpMV (spmvtk_pipeline_*) -------------------------------
+struct spmvtk_pipeline {
+  const dev::Matrix* m = nullptr;
+  spmvtk_kernel kernel = SPMVTK_KERNEL_CRS;
+  cudaStream_t h2d = nullptr, comp = nullptr, d2h = nullptr;
+  double* x[2] = {nullptr, nullptr};
+  double* y[2] = {nullptr, nullptr};
+  cudaEvent_t h2d_done[2] = {}, comp_done[2] = {}, d2h_done[2] = {};
+  std::uint64_t count = 0;
+  ~spmvtk_pipeline() {
+    if (comp) cudaStreamSynchronize(comp);
+    if (d2h) cudaStreamSynchronize(d2h);
+    if (h2d) cudaStreamSynchronize(h2d);
+    for (int b = 0; b < 2; ++b) {
+      if (x[b]) cudaFree(x[b]);
+      if (y[b]) cudaFree(y[b]);
+      if (h2d_done[b]) cudaEventDestroy(h2d_done[b]);
+      if (comp_done[b]) cudaEventDestroy(comp_done[b]);
+      if (d2h_done[b]) cudaEventDestroy(d2h_done[b]);
+    }
+    if (h2d) cudaStreamDestroy(h2d);
+    if (comp) cudaStreamDestroy(comp);
+    if (d2h) cudaStreamDestroy(d2h);
+  }
+};
+
+spmvtk_status spmvtk_pipeline_create(const spmvtk_matrix* m, spmvtk_kernel kernel,
+                                     spmvtk_pipeline** out) {
+  return guarded([&] {
+    if (!m || !out) throw Error(ErrorCode::InvalidArgument, "null argument");
+    if (!valid_kernel(kernel)) throw Error(ErrorCode::InvalidArgument, "unknown kernel id");
+    rt::init();
+    auto p = std::make_unique<spmvtk_pipeline>();
+    p->m = m;
+    p->kernel = kernel;
+    for (cudaStream_t* st : {&p->h2d, &p->comp, &p->d2h})
+      rt::check(cudaStreamCreateWithFlags(st, cudaStreamNonBlocking), "pipeline stream");
+    const std::size_t nx = std::max<std::int64_t>(m->ncols, 1), ny = std::max<std::int64_t>(m->n, 1);
+    for (int b = 0; b < 2; ++b) {
+      rt::check(cudaMalloc(&p->x[b], nx * sizeof(double)), "pipeline x");
+      rt::check(cudaMalloc(&p->y[b], ny * sizeof(double)), "pipeline y");
+      rt::check(cudaEventCreateWithFlags(&p->h2d_done[b], cudaEventDisableTiming), "event");
+      rt::check(cudaEventCreateWithFlags(&p->comp_done[b], cudaEventDisableTiming), "event");
+      rt::check(cudaEventCreateWithFlags(&p->d2h_done[b], cudaEventDisableTiming), "event");
+    }
+    *out = p.release();
+  });
+}
+
+spmvtk_status spmvtk_pipeline_submit(spmvtk_pipeline* p, const double* x, double* y) {
+  return guarded([&] {
+    if (!p || !x || !y) throw Error(ErrorCode::InvalidArgument, "null argument");
+    const int b = static_cast<int>(p->count & 1);
+    const std::size_t nx = static_cast<std::size_t>(p->m->ncols) * sizeof(double);
+    const std::size_t ny = static_cast<std::size_t>(p->m->n) * sizeof(double);
+    // copy-in waits until the SpMV that last read this staging slot is done
+    rt::check(cudaStreamWaitEvent(p->h2d, p->comp_done[b], 0), "pipeline order");
+    if (nx) rt::check(cudaMemcpyAsync(p->x[b], x, nx, cudaMemcpyHostToDevice, p->h2d), "H2D x");
+    rt::check(cudaEventRecord(p->h2d_done[b], p->h2d), "pipeline event");
+    // the SpMV waits for its x and for the copy-out that last read its y slot
+    rt::check(cudaStreamWaitEvent(p->comp, p->h2d_done[b], 0), "pipeline order");
+    rt::check(cudaStreamWaitEvent(p->comp, p->d2h_done[b], 0), "pipeline order");
+    cudaStream_t saved = rt::stream();
+    rt::set_stream(p->comp);
+    try {
+      dev::spmv_device(*p->m, p->kernel, p->x[b], p->y[b]);
+    } catch (...) {
+      rt::set_stream(saved);
+      throw;
+    }
+    rt::set_stream(saved);
+    rt::check(cudaEventRecord(p->comp_done[b], p->comp), "pipeline event");
+    rt::check(cudaStreamWaitEvent(p->d2h, p->comp_done[b], 0), "pipeline order");
+    if (ny) rt::check(cudaMemcpyAsync(y, p->y[b], ny, cudaMemcpyDeviceToHost, p->d2h), "D2H y");
+    rt::check(cudaEventRecord(p->d2h_done[b], p->d2h), "pipeline event");
+    ++p->count;
+  });
+}
+
+spmvtk_status spmvtk_pipeline_wait(spmvtk_pipeline* p) {
+  return guarded([&] {
+    if (!p) throw Error(ErrorCode::InvalidArgument, "null argument");
+    rt::check(cudaStreamSynchronize(p->h2d), "pipeline wait");
+    rt::check(cudaStreamSynchronize(p->comp), "pipeline wait");
+    rt::check(cudaStreamSynchronize(p->d2h), "pipeline wait");
+  });
+}
+
+void spmvtk_pipeline_free(spmvtk_pipeline* p) { delete p; }
+
 spmvtk_status spmvtk_bench(const spmvtk_matrix* m, spmvtk_kernel variant, int lanes,
                            int repeats, uint64_t max_bytes, spmvtk_bench_result* out) {
   return guarded([&] {

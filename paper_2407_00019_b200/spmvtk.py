@@ -199,6 +199,10 @@ SIGNATURES = {
     "spmvtk_conversion_bytes": (C.c_int, [_P, C.c_int, C.POINTER(_u64), C.POINTER(_u64)]),
     "spmvtk_transform_kernel_seconds": (C.c_int, [_P, C.c_int, C.c_int, _pd]),
     "spmvtk_reserve_device_memory": (C.c_int, [_u64]),
+    "spmvtk_pipeline_create": (C.c_int, [_P, C.c_int, _PP]),
+    "spmvtk_pipeline_submit": (C.c_int, [_P, _P, _P]),
+    "spmvtk_pipeline_wait": (C.c_int, [_P]),
+    "spmvtk_pipeline_free": (None, [_P]),
     "spmvtk_ipc_alloc": (C.c_int, [_u64, _PP, _P]),
     "spmvtk_ipc_free": (C.c_int, [_P]),
     "spmvtk_ipc_open": (C.c_int, [_P, _PP]),
@@ -434,6 +438,41 @@ class Matrix:
 
 def reserve_device_memory(nbytes: int) -> None:
     _check(load_library().spmvtk_reserve_device_memory(int(nbytes)))
+
+
+class Pipeline:
+    """Streaming host SpMV (spmvtk_pipeline_*): submit() enqueues
+    H2D(x) -> SpMV -> D2H(y) and returns; products overlap each other's
+    copies.  x / y must be host buffers (numpy, pinned for asynchrony) that
+    stay alive and untouched until wait()."""
+
+    def __init__(self, m: "Matrix", kernel: Kernel):
+        self._lib = load_library()
+        h = C.c_void_p()
+        _check(self._lib.spmvtk_pipeline_create(m.handle, int(kernel), C.byref(h)))
+        self._h = h.value
+        self._keep = []
+
+    def submit(self, x: np.ndarray, y: np.ndarray) -> None:
+        assert x.dtype == np.float64 and y.dtype == np.float64
+        assert x.flags.c_contiguous and y.flags.c_contiguous
+        self._keep.append((x, y))
+        _check(self._lib.spmvtk_pipeline_submit(self._h, x.ctypes.data, y.ctypes.data))
+
+    def wait(self) -> None:
+        _check(self._lib.spmvtk_pipeline_wait(self._h))
+        self._keep = []
+
+    def free(self) -> None:
+        if self._h:
+            self._lib.spmvtk_pipeline_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:  # noqa: BLE001
+            pass
 
 
 def ipc_alloc(nbytes: int) -> tuple[int, bytes]:

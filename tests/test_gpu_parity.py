@@ -522,6 +522,28 @@ def test_pipelined_host_spmv_matches_device(gpu):
         assert yp.numpy().tobytes() == y_pageable.tobytes(), k
 
 
+def test_streaming_pipeline_matches_spmv(gpu):
+    """spmvtk_pipeline_*: several products in flight (double-buffered device
+    staging, copy-in / SpMV / copy-out on three streams) give bitwise the
+    results of the synchronous spmvtk_spmv for every submitted x."""
+    import torch
+    sp = gpu
+    m = sp.HostCrs(2, 1 << 15).upload()
+    n = m.describe().n
+    for h, k in ((m, sp.Kernel.CRS), (m.convert(sp.Format.ELL), sp.Kernel.ELL_INNER),
+                 (m.convert(sp.Format.COO_ROW), sp.Kernel.COO_ROW_OUTER)):
+        pipe = sp.Pipeline(h, k)
+        xs = [torch.from_numpy(sp.gen_vector(n, 100 + i)).pin_memory() for i in range(5)]
+        ys = [torch.empty(n, dtype=torch.float64).pin_memory() for _ in range(5)]
+        for x, y in zip(xs, ys):
+            pipe.submit(x.numpy(), y.numpy())
+        pipe.wait()
+        for x, y in zip(xs, ys):
+            want, _ = h.spmv(x.numpy(), k)
+            assert y.numpy().tobytes() == want.tobytes(), k
+        pipe.free()
+
+
 def test_row_block_shards_single_gpu(gpu, port):
     """Row-block shards (the multi-GPU layout) run on one GPU: per-shard
     SpMV assembled == full SpMV (1e-12), and each shard's ELL equals the
