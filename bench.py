@@ -262,6 +262,14 @@ def impl_ours(args):
     # reduction's host round trip included); kernel = median device time of
     # the transform's kernels alone with outputs preallocated.
     sp.reserve_device_memory(8 << 30)
+    # process warm-up (first-call costs of the ctypes bindings and the
+    # conversion paths) on a small unrelated matrix, never on the one timed
+    warm = sp.HostCrs(1, 256, 0.0, args.seed).upload()
+    for fmt in (sp.Format.COO_ROW, sp.Format.CCS, sp.Format.COO_COL, sp.Format.ELL,
+                sp.Format.ELL_ROWMAJOR):
+        warm.convert(fmt).free()
+    warm.free()
+    torch.cuda.synchronize()
     handles = {"crs": m}
     transforms = {}
     for name, fmt in (("coo-row", sp.Format.COO_ROW), ("ccs", sp.Format.CCS),

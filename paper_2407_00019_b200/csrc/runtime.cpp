@@ -2,6 +2,7 @@
 #include "runtime.hpp"
 
 #include <cstdlib>
+#include <cstring>
 
 #include <cmath>
 #include <cstdint>
@@ -60,11 +61,32 @@ void* alloc_bytes(std::size_t bytes, const char* what) {
 
 void free_bytes(void* p) { cudaFreeAsync(p, t_stream); }
 
+namespace {
+// per-thread scratch of the row-statistics round trip: a device accumulator
+// and a pinned host landing slot, allocated once (the conversion timing
+// t_trans pays this round trip on every CRS -> ELL call)
+struct StatsScratch {
+  unsigned long long* dev = nullptr;
+  unsigned long long* host = nullptr;
+  ~StatsScratch() {
+    if (dev) cudaFree(dev);
+    if (host) cudaFreeHost(host);
+  }
+};
+thread_local StatsScratch t_stats;
+}  // namespace
+
 Moments row_moments(const std::int32_t* ptr, std::int64_t n) {
-  DevArray<unsigned long long> acc(3, "row statistics");
-  check_launch(spmvtk_k_row_stats(ptr, n, acc.get(), t_stream), "row statistics kernel");
+  init();
+  if (!t_stats.dev) {
+    check(cudaMalloc(&t_stats.dev, 4 * sizeof(unsigned long long)), "row statistics scratch");
+    check(cudaHostAlloc(&t_stats.host, 4 * sizeof(unsigned long long), cudaHostAllocDefault),
+          "row statistics scratch");
+  }
+  check_launch(spmvtk_k_row_stats(ptr, n, t_stats.dev, t_stream), "row statistics kernel");
   unsigned long long h[3];
-  copy_to_host(h, acc.get(), sizeof(h));
+  copy_to_host(t_stats.host, t_stats.dev, 3 * sizeof(unsigned long long));
+  std::memcpy(h, t_stats.host, sizeof(h));
   Moments m;
   m.monotone = (h[0] >> 63) == 0;
   m.max = h[0] & ~(1ull << 63);
