@@ -9,6 +9,7 @@
 // replaces.  Summation orders differ from the reference (fp64, FMA), which the
 // contract allows (max-norm relative 1e-12, BASELINE.json north_star).
 #include <algorithm>
+#include <cstdlib>
 #include <string>
 #include <type_traits>
 
@@ -1086,6 +1087,13 @@ int spmvtk_k_preload(void) {
   spmvtk_dev::preload_convert();
   spmvtk_dev::preload_util();
   spmvtk_dev::preload_inverse();
+  if (const char* c = std::getenv("SPMVTK_L1_CARVEOUT")) {  // experiment hook
+    const int pct = std::atoi(c);
+    cudaFuncSetAttribute(k_spmv_ell_cm<4, false>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+    cudaFuncSetAttribute(k_spmv_vec2<4, 1, CrsRows>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+    cudaFuncSetAttribute(k_spmv_vec2<8, 1, CrsRows>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+    cudaFuncSetAttribute(k_spmv_vec2<16, 1, CrsRows>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+  }
   cudaFuncAttributes a;
   cudaFuncGetAttributes(&a, k_spmv_crs_long<PlainOut>);
   cudaFuncGetAttributes(&a, k_spmv_crs_long<PushOut>);
