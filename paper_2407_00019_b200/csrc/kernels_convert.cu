@@ -296,7 +296,7 @@ constexpr int kSlices = 3 * 148;  // max slices (3 CTAs per SM, 64 KB histograms
 int g_ccs_slices = 148;           // tuning: slices actually used (one per SM)
 int g_ccs_threads = 1024;         // tuning: threads of the count/scatter CTAs
 constexpr int kBktItems = 12;  // records per sort thread (bucket capacity = threads * 12)
-int g_ccs_sort_threads = 512;  // tuning: 256 or 512 (bucket target = threads * 8 entries)
+int g_ccs_sort_threads = 512;  // tuning: 256 or 512 (bucket target = 2/3 of the capacity)
 
 // Two-pass or single-pass partition is decided on the device from the
 // number of non-empty (fine bucket, slice) runs counted by k_bkt_count: few
@@ -1011,7 +1011,9 @@ int g_ccs_coarse = 9;  // tuning: log2 of the coarse bucket count target (0 = on
 BucketPlan bucket_plan(int64_t n, int64_t nnz) {
   const double per_col = n > 0 ? static_cast<double>(nnz) / static_cast<double>(n) : 1.0;
   int shift = 0;
-  const double target = 8.0 * g_ccs_sort_threads;
+  // buckets average 2/3 of the sort capacity: skewed column counts (config 5
+  // at D = 1) overflow a tighter target into the slow global path
+  const double target = (2.0 / 3.0) * kBktItems * g_ccs_sort_threads;
   while (shift < 12 && static_cast<double>(int64_t(1) << (shift + 1)) * per_col <= target) ++shift;
   while (((n + (int64_t(1) << shift) - 1) >> shift) > 32768) ++shift;
   const int nb = static_cast<int>((n + (int64_t(1) << shift) - 1) >> shift);
