@@ -152,6 +152,17 @@ def dist_env():
 
 
 # --------------------------------------------------------------------------
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_reference_run(host, n, nnz, nz, per_call_repeats=3):
     """The reference's own CPU path (oracle/_ref, compiled from the reference
     sources) on this host's cores, on the same matrix."""
@@ -172,12 +183,19 @@ def cpu_reference_run(host, n, nnz, nz, per_call_repeats=3):
     res["ell-inner"] = (ref.measure_spmv(ell, 3, cores, per_call_repeats), cores)
     res["ell-outer"] = (ref.measure_spmv(ell, 4, cores, per_call_repeats), cores)
     res["coo-row"] = (ref.measure_spmv(coo, 1, cores, per_call_repeats), cores)
+    # the lane-parallel kernels also at one lane
+    one = {"ell-inner@1": ref.measure_spmv(ell, 3, 1, per_call_repeats),
+           "ell-outer@1": ref.measure_spmv(ell, 4, 1, per_call_repeats),
+           "coo-row@1": ref.measure_spmv(coo, 1, 1, per_call_repeats)}
     table = {}
     for k, (t, lanes) in res.items():
         b = spmv_bytes(k, n, nnz, nz)
         table[k] = {"gbs": b / t / 1e9, "gflops": 2 * nnz / t / 1e9, "ms": t * 1e3, "lanes": lanes}
     best = max(table, key=lambda k: table[k]["gbs"])
-    out = {"table": table, "best": best, "cores": cores,
+    for k, t in one.items():
+        b = spmv_bytes(k.split("@")[0], n, nnz, nz)
+        table[k] = {"gbs": b / t / 1e9, "gflops": 2 * nnz / t / 1e9, "ms": t * 1e3, "lanes": 1}
+    out = {"table": table, "best": best, "cores": cores, "cpu_model": cpu_model(),
            "transforms": {"ell": {"ms": t_ell * 1e3, "tt": t_ell / t_crs},
                           "coo-row": {"ms": t_coo * 1e3, "tt": t_coo / t_crs}},
            "handles": (ref, h, ell, coo)}
@@ -225,7 +243,8 @@ def impl_reference(args):
         "cpu_baseline": {"value": value, "unit": "GB/s", "cores": lanes, "kind": "reference",
                          "sample": f"{args.steps} SpMVs ({best}, {lanes} lanes) of the full "
                                    f"config-{args.config} matrix; oracle/_ref = reference "
-                                   "compiled from its sources; std::thread lanes, no OpenMP"},
+                                   "compiled from its sources; std::thread lanes, no OpenMP",
+                         "cpu_model": r.get("cpu_model"), "nproc": r.get("cores")},
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "formats": r["table"], "transforms": r["transforms"],
     }
@@ -420,7 +439,8 @@ def impl_ours(args):
                               f"same config-{args.config} matrix; best = {r['best']} at "
                               f"{b['lanes']} lanes of {r['cores']} cores; std::thread lanes "
                               "(the reference has no OpenMP)"),
-                   "formats": r["table"], "transforms": r["transforms"]}
+                   "formats": r["table"], "transforms": r["transforms"],
+                   "cpu_model": r["cpu_model"], "nproc": r["cores"]}
         except Exception as e:  # reported, never silently replaced
             cpu = {"value": None, "unit": "GB/s", "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"unavailable: {e}"}
