@@ -1,0 +1,30 @@
+"""bench.py's reference arm runs on the host only, so its JSON contract is
+checked here on CPU (config 1, a few steps): the driver parses this line."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_reference_arm_json_line():
+    if not os.path.exists(os.path.join(ROOT, "oracle", "_ref", "libspmvtk_ref.so")):
+        pytest.skip("oracle/_ref not built")
+    out = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--config", "1",
+                          "--steps", "3", "--warmup", "1"], cwd=ROOT, capture_output=True,
+                         text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    for key in ("impl", "metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+                "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config",
+                "cpu_baseline", "e2e"):
+        assert key in line, key
+    assert line["impl"] == "reference" and line["value"] > 0
+    cb = line["cpu_baseline"]
+    assert cb["kind"] == "reference" and cb["cores"] >= 1 and cb["value"] == line["value"]
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["d2h_bytes_per_step"] == 0
+    # the lane-parallel reference kernels are reported at one lane too
+    assert {"ell-inner@1", "coo-row@1", "crs"} <= set(line["formats"])
