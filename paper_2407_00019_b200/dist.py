@@ -393,7 +393,7 @@ def bench_main(args, rank: int, world: int, local: int) -> int:
 
     import sys
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-    from bench import ClockSampler, hbm_peak
+    from bench import ClockSampler, hbm_peak, spmv_bytes
     with ClockSampler(local) as clk:
         t_step = timed(args.steps, True)
     t_local = timed(max(20, args.steps // 4), False)
@@ -448,22 +448,31 @@ def bench_main(args, rank: int, world: int, local: int) -> int:
     if t_push is not None and t_push < t_step:
         push_info["used"] = True
         t_step = t_push
+    # shard bytes (each rank's own kernel, for the per-GPU roofline) and the
+    # whole product's algorithmic bytes -- the same formula as the 1-GPU
+    # bench line, so value(N) / value(1) is the speed-up of one SpMV step
     b = torch.tensor([bytes_of(fmt)], dtype=torch.float64, device="cuda")
     dist.all_reduce(b, op=dist.ReduceOp.SUM)
-    total_bytes = float(b.item())
+    shard_bytes = float(b.item())
+    total_bytes = float(spmv_bytes(fmt, n, nnz, nz_global))
 
-    # e2e: the C ABI call with pinned host x (ncols) and y (local rows)
+    # e2e: the streaming C ABI calls with pinned host x (ncols) and y (local
+    # rows): every step copies its x in and its row block out on every rank
     xh = torch.from_numpy(sp.gen_vector(n, args.seed + 1)).pin_memory()
-    yh = torch.empty(block_rows(n, world), dtype=torch.float64).pin_memory()
-    for _ in range(3):
-        h.spmv(xh.numpy(), k, 1, out=yh.numpy())
+    yhs = [torch.empty(block_rows(n, world), dtype=torch.float64).pin_memory() for _ in range(2)]
+    pipe = sp.Pipeline(h, k)
+    for i in range(4):
+        pipe.submit(xh.numpy(), yhs[i % 2].numpy())
+    pipe.wait()
     dist.barrier()
     t0 = time.perf_counter()
     e2e_steps = max(10, min(args.steps, 100))
-    for _ in range(e2e_steps):
-        h.spmv(xh.numpy(), k, 1, out=yh.numpy())
+    for i in range(e2e_steps):
+        pipe.submit(xh.numpy(), yhs[i % 2].numpy())
+    pipe.wait()
     te = torch.tensor([(time.perf_counter() - t0) / e2e_steps], dtype=torch.float64,
                       device="cuda")
+    pipe.free()
     dist.all_reduce(te, op=dist.ReduceOp.MAX)
     t_e2e = float(te.item())
 
@@ -483,16 +492,18 @@ def bench_main(args, rank: int, world: int, local: int) -> int:
                                         "NCCL all_gather of x per step")),
                        "gflops": 2 * nnz / t_step / 1e9},
             "push_exchange": push_info,
+            "bytes": {"whole_product": total_bytes, "sum_of_shards": shard_bytes},
             "no_comm": {"ms_per_step": t_local * 1e3,
                         "value": total_bytes / t_local / 1e9},
             "e2e": {"value": total_bytes / t_e2e / 1e9, "unit": "GB/s",
-                    "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * block_rows(n, world),
-                    "api": "spmvtk_spmv per rank (pinned host x / y block)"},
+                    "h2d_bytes_per_step": 8 * n * world,
+                    "d2h_bytes_per_step": 8 * block_rows(n, world) * world,
+                    "api": "spmvtk_pipeline_submit/wait per rank (pinned host x, y block)"},
             "gpu_launches": args.steps,
             "clocks": clk.summary(),
         }
         peak, kind = hbm_peak()
-        per_gpu = total_bytes / world / t_local / 1e9
+        per_gpu = shard_bytes / world / t_local / 1e9
         line["roofline"] = {"bound": "hbm", "achieved": per_gpu, "peak": peak, "unit": "GB/s",
                             "frac": per_gpu / peak, "traffic": None, "peak_kind": kind,
                             "kernel": fmt, "note": "per GPU, SpMV shard without the exchange"}
