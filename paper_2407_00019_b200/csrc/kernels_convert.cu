@@ -451,24 +451,29 @@ __global__ void __launch_bounds__(1024) k_bkt_scatter(
 // entries each per step; the step's 4096 records are counting-sorted by
 // bucket in shared memory and written out run by run, so consecutive lanes
 // store consecutive addresses instead of 32 scattered 16-byte records.
-constexpr int kStageThreads = 1024;
 constexpr int kStageU = 4;
-constexpr int kStageTile = kStageThreads * kStageU;
 constexpr int kStageMaxB = 1024;
+int g_stage_threads = 1024;  // tuning: 1024 (one CTA per slice per SM) or 512
 
+template <int kStageThreads>
 __global__ void __launch_bounds__(kStageThreads) k_bkt_scatter_staged(
     const int32_t* __restrict__ irp, const int32_t* __restrict__ icol,
     const double* __restrict__ val, const int32_t* __restrict__ slice_row, int shift, int nb,
     const int32_t* __restrict__ Toff, int4* __restrict__ rec, const int32_t* runs, bool as_two) {
   if (runs && two_pass(runs) != as_two) return;
-  extern __shared__ int4 s_rec[];  // kStageTile records
+  constexpr int kP = kStageMaxB / kStageThreads;  // buckets owned per thread
+  extern __shared__ int4 s_rec[];  // kStageThreads * kStageU records
   __shared__ int32_t s_cur[kStageMaxB], s_cnt[kStageMaxB], s_off[kStageMaxB];
-  __shared__ int32_t s_wsum[32];
+  __shared__ int32_t s_wsum[kStageThreads / 32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int nwarps = kStageThreads / 32;
-  if (tid < nb) {
-    s_cur[tid] = Toff[static_cast<int64_t>(tid) * gridDim.x + blockIdx.x];
-    s_cnt[tid] = 0;
+#pragma unroll
+  for (int j = 0; j < kP; ++j) {
+    const int b = tid * kP + j;
+    if (b < nb) {
+      s_cur[b] = Toff[static_cast<int64_t>(b) * gridDim.x + blockIdx.x];
+      s_cnt[b] = 0;
+    }
   }
   const int64_t r_begin = slice_row[blockIdx.x], r_end = slice_row[blockIdx.x + 1];
   const int32_t E0 = __ldg(irp + r_begin), E1 = __ldg(irp + r_end);
@@ -522,8 +527,16 @@ __global__ void __launch_bounds__(kStageThreads) k_bkt_scatter_staged(
     for (int u = 0; u < kStageU; ++u)
       rk[u] = pp[u] < p1 ? atomicAdd(&s_cnt[c[u] >> shift], 1) : 0;
     __syncthreads();
-    // exclusive scan of the step's bucket counts (thread t owns bucket t)
-    const int32_t x = tid < nb ? s_cnt[tid] : 0;
+    // exclusive scan of the step's bucket counts (thread t owns buckets
+    // [t*kP, t*kP + kP))
+    int32_t loc[kP];
+    int32_t x = 0;
+#pragma unroll
+    for (int j = 0; j < kP; ++j) {
+      const int b = tid * kP + j;
+      loc[j] = b < nb ? s_cnt[b] : 0;
+      x += loc[j];
+    }
     int32_t inc = x;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
@@ -533,17 +546,25 @@ __global__ void __launch_bounds__(kStageThreads) k_bkt_scatter_staged(
     if (lane == 31) s_wsum[warp] = inc;
     __syncthreads();
     if (warp == 0) {
-      const int32_t wv = s_wsum[lane];
+      const int32_t wv = lane < nwarps ? s_wsum[lane] : 0;
       int32_t wi = wv;
 #pragma unroll
       for (int d = 1; d < 32; d <<= 1) {
         const int32_t t = __shfl_up_sync(kFull, wi, d);
         if (lane >= d) wi += t;
       }
-      s_wsum[lane] = wi - wv;
+      if (lane < nwarps) s_wsum[lane] = wi - wv;
     }
     __syncthreads();
-    if (tid < nb) s_off[tid] = s_wsum[warp] + inc - x;
+    {
+      int32_t e = s_wsum[warp] + inc - x;
+#pragma unroll
+      for (int j = 0; j < kP; ++j) {
+        const int b = tid * kP + j;
+        if (b < nb) s_off[b] = e;
+        e += loc[j];
+      }
+    }
     __syncthreads();
 #pragma unroll
     for (int u = 0; u < kStageU; ++u)
@@ -558,9 +579,13 @@ __global__ void __launch_bounds__(kStageThreads) k_bkt_scatter_staged(
       rec[s_cur[b] + i - s_off[b]] = r;
     }
     __syncthreads();
-    if (tid < nb) {
-      s_cur[tid] += s_cnt[tid];
-      s_cnt[tid] = 0;
+#pragma unroll
+    for (int j = 0; j < kP; ++j) {
+      const int b = tid * kP + j;
+      if (b < nb) {
+        s_cur[b] += s_cnt[b];
+        s_cnt[b] = 0;
+      }
     }
 #pragma unroll
     for (int u = 0; u < kStageU; ++u) {
@@ -1042,6 +1067,10 @@ int spmvtk_k_tune_convert(const char* key, int value) {
     g_ell_flat_rows = value == 64 ? 64 : 128;
     return 0;
   }
+  if (key && std::string(key) == "ccs_stage_threads") {
+    g_stage_threads = value == 512 ? 512 : 1024;
+    return 0;
+  }
   if (key && std::string(key) == "ccs_coarse") {
     g_ccs_coarse = value;
     return 0;
@@ -1063,6 +1092,19 @@ size_t spmvtk_k_ccs_scratch_bytes(int64_t n, int64_t nnz) {
                         spmvtk_k_scan_scratch_bytes(n + 1) + 1024;
   return bucketed > atomic ? bucketed : atomic;
 }
+
+namespace {
+void launch_staged(int ns, cudaStream_t s, const int32_t* irp, const int32_t* icol,
+                   const double* val, const int32_t* slice_row, int shift, int nb,
+                   const int32_t* Toff, int4* rec, const int32_t* runs, bool as_two) {
+  if (g_stage_threads == 512)
+    k_bkt_scatter_staged<512><<<ns, 512, 512 * kStageU * sizeof(int4), s>>>(
+        irp, icol, val, slice_row, shift, nb, Toff, rec, runs, as_two);
+  else
+    k_bkt_scatter_staged<1024><<<ns, 1024, 1024 * kStageU * sizeof(int4), s>>>(
+        irp, icol, val, slice_row, shift, nb, Toff, rec, runs, as_two);
+}
+}  // namespace
 
 int spmvtk_k_crs_to_ccs(int64_t n, int64_t nnz, const int32_t* irp, const int32_t* icol,
                         const double* val, int32_t* col_ptr, int32_t* row_idx,
@@ -1105,8 +1147,10 @@ int spmvtk_k_crs_to_ccs(int64_t n, int64_t nnz, const int32_t* irp, const int32_
   static const bool attrs = [] {  // thread-safe one-time setup
     cudaFuncSetAttribute(k_bkt_count, cudaFuncAttributeMaxDynamicSharedMemorySize, 32768 * 4);
     cudaFuncSetAttribute(k_bkt_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, 32768 * 4);
-    cudaFuncSetAttribute(k_bkt_scatter_staged, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         kStageTile * static_cast<int>(sizeof(int4)));
+    cudaFuncSetAttribute(k_bkt_scatter_staged<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         1024 * kStageU * static_cast<int>(sizeof(int4)));
+    cudaFuncSetAttribute(k_bkt_scatter_staged<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         512 * kStageU * static_cast<int>(sizeof(int4)));
     cudaFuncSetAttribute(k_bkt_sort<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(((4097 * 4 + 15) & ~15) + 512 * kBktItems * 14));
     cudaFuncSetAttribute(k_bkt_sort<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1128,8 +1172,8 @@ int spmvtk_k_crs_to_ccs(int64_t n, int64_t nnz, const int32_t* irp, const int32_
     if (rc) return rc;
     cudaMemsetAsync(fcur, 0, static_cast<size_t>(bp.nb) * 4, s);
     if (bp.nc <= kStageMaxB)
-      k_bkt_scatter_staged<<<ns, kStageThreads, kStageTile * sizeof(int4), s>>>(
-          irp, icol, val, slice_row, bp.shift + bp.fshift, bp.nc, Tcoff, rec, runs, true);
+      launch_staged(ns, s, irp, icol, val, slice_row, bp.shift + bp.fshift, bp.nc, Tcoff, rec,
+                    runs, true);
     else
       k_bkt_scatter<<<ns, nt, static_cast<size_t>(bp.nc) * 4, s>>>(
           irp, icol, val, slice_row, bp.shift + bp.fshift, bp.nc, Tcoff, rec, runs, true);
@@ -1139,8 +1183,7 @@ int spmvtk_k_crs_to_ccs(int64_t n, int64_t nnz, const int32_t* irp, const int32_
     k_bkt_scatter<<<ns, nt, hist_smem, s>>>(irp, icol, val, slice_row, bp.shift, bp.nb, Toff,
                                             rec, runs, false);
   } else if (bp.nb <= kStageMaxB && g_ccs_coarse > 0) {
-    k_bkt_scatter_staged<<<ns, kStageThreads, kStageTile * sizeof(int4), s>>>(
-        irp, icol, val, slice_row, bp.shift, bp.nb, Toff, rec, nullptr, false);
+    launch_staged(ns, s, irp, icol, val, slice_row, bp.shift, bp.nb, Toff, rec, nullptr, false);
   } else {
     k_bkt_scatter<<<ns, nt, hist_smem, s>>>(irp, icol, val, slice_row, bp.shift, bp.nb, Toff,
                                             rec, nullptr, false);
@@ -1259,7 +1302,8 @@ void preload_convert() {
   cudaFuncGetAttributes(&a, k_slice_rows);
   cudaFuncGetAttributes(&a, k_bkt_count);
   cudaFuncGetAttributes(&a, k_bkt_scatter);
-  cudaFuncGetAttributes(&a, k_bkt_scatter_staged);
+  cudaFuncGetAttributes(&a, k_bkt_scatter_staged<1024>);
+  cudaFuncGetAttributes(&a, k_bkt_scatter_staged<512>);
   cudaFuncGetAttributes(&a, k_bkt_refine);
   cudaFuncGetAttributes(&a, k_bkt_sort<256>);
   cudaFuncGetAttributes(&a, k_bkt_sort<512>);
