@@ -753,6 +753,128 @@ __global__ void __launch_bounds__(256) k_spmv_ell_cm(int64_t n, int32_t k_begin,
   }
 }
 
+// ---- ELL band-major with the matrix streamed by the TMA engine ------------
+// The bands of a CTA's 256 rows are contiguous 2 KB (values) / 1 KB (column)
+// runs: one elected thread moves them into a shared-memory ring with 1-D bulk
+// copies (cp.async.bulk, completion counted on an mbarrier), so the matrix
+// stream never occupies the LSU / L1 request path that the random x gathers
+// saturate; threads read their row pair's slots from shared memory and keep
+// KB bands of gathers in flight.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <int THREADS, int KB, int STAGES>
+__global__ void __launch_bounds__(THREADS) k_spmv_ell_bulk(int64_t n, int32_t nz, int64_t ld,
+                                                           const double* __restrict__ val,
+                                                           const int32_t* __restrict__ col,
+                                                           const double* __restrict__ x,
+                                                           double* __restrict__ y) {
+  // persistent: the CTA walks row blocks blockIdx, +gridDim, ... and its
+  // ring of STAGES x KB bands runs continuously across them
+  constexpr int R = 2 * THREADS;  // rows per block (2 per thread)
+  extern __shared__ __align__(128) unsigned char s_raw[];
+  double* s_val = reinterpret_cast<double*>(s_raw);                 // [STAGES][KB][R]
+  int32_t* s_col = reinterpret_cast<int32_t*>(s_val + STAGES * KB * R);
+  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int T = (nz + KB - 1) / KB;                       // band chunks per row block
+  const int64_t nblocks = (ld + R - 1) / R;
+  const int64_t my_blocks = blockIdx.x < nblocks ? (nblocks - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int64_t total = my_blocks * T;                    // ring items of this CTA
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], THREADS / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int64_t g) {
+    const int s = static_cast<int>(g % STAGES);
+    const int64_t rb = blockIdx.x + (g / T) * gridDim.x;
+    const int k0 = static_cast<int>(g % T) * KB, kb = min(KB, nz - k0);
+    const int64_t r0 = rb * R;
+    const int rows = static_cast<int>(min(static_cast<int64_t>(R), ld - r0));
+    mbar_expect_tx(&full[s], static_cast<uint32_t>(kb * rows * 12));
+    for (int j = 0; j < kb; ++j) {
+      const int64_t off = static_cast<int64_t>(k0 + j) * ld + r0;
+      bulk_g2s(s_val + (s * KB + j) * R, val + off, rows * 8, &full[s]);
+      bulk_g2s(s_col + (s * KB + j) * R, col + off, rows * 4, &full[s]);
+    }
+  };
+  if (tid == 0)
+    for (int64_t g = 0; g < min(static_cast<int64_t>(STAGES), total); ++g) issue(g);
+  double a0 = 0.0, a1 = 0.0;
+  for (int64_t g = 0; g < total; ++g) {
+    const int s = static_cast<int>(g % STAGES);
+    const uint32_t parity = static_cast<uint32_t>((g / STAGES) & 1);
+    const int t = static_cast<int>(g % T);
+    const int64_t r0 = (blockIdx.x + (g / T) * gridDim.x) * R;
+    const int rows = static_cast<int>(min(static_cast<int64_t>(R), ld - r0));
+    mbar_wait(&full[s], parity);
+    const int kb = min(KB, nz - t * KB);
+    if (2 * tid < rows) {
+      double2 v[KB];
+      int2 c[KB];
+#pragma unroll
+      for (int j = 0; j < KB; ++j)
+        if (j < kb) {
+          v[j] = reinterpret_cast<const double2*>(s_val + (s * KB + j) * R)[tid];
+          c[j] = reinterpret_cast<const int2*>(s_col + (s * KB + j) * R)[tid];
+        }
+#pragma unroll
+      for (int j = 0; j < KB; ++j)
+        if (j < kb) {
+          a0 = fma(v[j].x, ld_x(x + c[j].x), a0);
+          a1 = fma(v[j].y, ld_x(x + c[j].y), a1);
+        }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+    if (tid == 0 && g + STAGES < total) {
+      mbar_wait(&empty[s], parity);
+      issue(g + STAGES);
+    }
+    if (t == T - 1) {  // row block done
+      const int64_t i = r0 + 2 * tid;
+      if (i < n) y[i] = a0;
+      if (i + 1 < n) y[i + 1] = a1;
+      a0 = a1 = 0.0;
+    }
+  }
+}
+
 // band-split variant (spmv_ell_outer): chunk s of the bands writes
 // partial[s*n + i]; then an ascending-chunk reduction (reduce_partials,
 // spmv.cpp:56-62) makes the result independent of scheduling.
@@ -815,6 +937,7 @@ __global__ void k_reduce_partials(int64_t n, int32_t splits, const double* __res
 int g_l2_hint = 0;  // L2 evict_first (matrix) / evict_last (x) policies
 int g_coo_variant = 1;  // 1: 4 entries per lane (k_spmv_coo_row4), 0: scalar
 int g_rm_variant = -1;  // row-major ELL variant override (tuning)
+int g_ell_variant = 0;  // band-major ELL: 0 = LSU loads, 1/2 = TMA bulk-copy ring (8x3 / 4x4)
 
 template <int W, int U, typename Rows, typename Out>
 void launch_vec(int64_t n, Rows rows, const int32_t* col, const double* val, const double* x,
@@ -1010,6 +1133,21 @@ int spmvtk_k_spmv_ell_cm(int64_t n, int32_t nz, int64_t ld, const double* val,
     cudaMemsetAsync(y, 0, static_cast<size_t>(n) * sizeof(double), s);
     SPMVTK_LAUNCH_RETURN();
   }
+  if (g_ell_variant >= 1 && g_ell_variant <= 4) {  // matrix streamed by TMA bulk copies
+    auto go = [&](auto kern, int threads, int kb, int stages, int ctas_per_sm) {
+      const int smem = stages * kb * 2 * threads * 12;
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      const int64_t nblocks = (ld + 2 * threads - 1) / (2 * threads);
+      const unsigned grid =
+          static_cast<unsigned>(std::min<int64_t>(nblocks, int64_t(kSMs) * ctas_per_sm));
+      kern<<<grid, threads, smem, s>>>(n, nz, ld, val, col, x, y);
+    };
+    if (g_ell_variant == 1) go(k_spmv_ell_bulk<128, 8, 4>, 128, 8, 4, 2);
+    if (g_ell_variant == 2) go(k_spmv_ell_bulk<256, 4, 4>, 256, 4, 4, 2);
+    if (g_ell_variant == 3) go(k_spmv_ell_bulk<256, 4, 3>, 256, 4, 3, 3);
+    if (g_ell_variant == 4) go(k_spmv_ell_bulk<512, 2, 4>, 512, 2, 4, 2);
+    SPMVTK_LAUNCH_RETURN();
+  }
   const int64_t pairs = (n + 1) / 2;
   const unsigned blocks = static_cast<unsigned>((pairs + 255) / 256);
   if (g_l2_hint)
@@ -1073,6 +1211,10 @@ int spmvtk_k_tune(const char* key, int value) {
   }
   if (key && std::string(key) == "coo_variant") {
     g_coo_variant = value;
+    return 0;
+  }
+  if (key && std::string(key) == "ell_variant") {
+    g_ell_variant = value;
     return 0;
   }
   if (key && std::string(key) == "rm_variant") {
