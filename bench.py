@@ -152,6 +152,48 @@ def dist_env():
 
 
 # --------------------------------------------------------------------------
+def l2_resident_graph(sp, torch, seed, peak, iters=1000):
+    """Config 1 SpMVs captured into one CUDA graph of `iters` launches
+    (x -> y -> x ping-pong), replayed and timed with events: per-SpMV time
+    of an L2-resident matrix without the launch overhead."""
+    m = sp.HostCrs(1, 256, 0.0, seed).upload()
+    d = m.describe()
+    nz = m.row_stats().max_row
+    ell = m.convert(sp.Format.ELL)
+    out = {"label": "L2-resident", "n": d.n, "nnz": d.nnz, "iters_per_graph": iters}
+    for name, h, k in (("crs", m, sp.Kernel.CRS), ("ell-inner", ell, sp.Kernel.ELL_INNER)):
+        a = torch.from_numpy(sp.gen_vector(d.n, seed + 1)).cuda()
+        b = torch.empty_like(a)
+        stream = torch.cuda.Stream()
+        with torch.cuda.stream(stream):
+            sp.set_stream(stream.cuda_stream)
+            for _ in range(3):  # warm-up (caches row statistics, loads modules)
+                h.spmv_device(k, a.data_ptr(), b.data_ptr())
+            stream.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=stream):
+                for i in range(iters):
+                    src, dst = (a, b) if i % 2 == 0 else (b, a)
+                    h.spmv_device(k, src.data_ptr(), dst.data_ptr())
+            g.replay()
+            stream.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(5):
+                g.replay()
+            e1.record(stream)
+            stream.synchronize()
+        sp.set_stream(torch.cuda.current_stream().cuda_stream)
+        t = e0.elapsed_time(e1) * 1e-3 / (5 * iters)
+        by = spmv_bytes(name, d.n, d.nnz, nz)
+        out[name] = {"us": t * 1e6, "gbs": by / t / 1e9, "gflops": 2 * d.nnz / t / 1e9,
+                     "frac_of_hbm_peak": by / t / 1e9 / peak}
+        del g
+    ell.free()
+    m.free()
+    return out
+
+
 def cpu_model() -> str:
     try:
         with open("/proc/cpuinfo") as f:
@@ -426,6 +468,12 @@ def impl_ours(args):
                                m3.transform_kernel_seconds(sp.Format.ELL, 3) * 1e3}
         for h3 in (e3, c3, m3):
             h3.free()
+        # config 1 (5 MB, L2-resident, launch-bound): SURVEY.md §8d asks for a
+        # CUDA graph of >= 1000 SpMVs so launch overhead does not dominate
+        try:
+            also["config1_graph"] = l2_resident_graph(sp, torch, args.seed, peak)
+        except Exception as e:  # reported, not fatal for the headline
+            also["config1_graph"] = {"error": f"{type(e).__name__}: {e}"[:200]}
 
     # ---- CPU baseline: the reference itself on this host (bounded sample)
     cpu = None
