@@ -544,6 +544,46 @@ def test_streaming_pipeline_matches_spmv(gpu):
         pipe.free()
 
 
+def test_concurrent_threads_share_a_handle(gpu):
+    """Handles are immutable and safe for concurrent reads (SPEC.md:100-101,
+    SURVEY.md 8b): 4 host threads, each on its own CUDA stream, run SpMVs,
+    conversions and statistics on one handle at once; every result equals
+    the single-threaded one bitwise."""
+    import threading
+
+    import torch
+    sp = gpu
+    m = sp.HostCrs(2, 1 << 16).upload()
+    n = m.describe().n
+    xs = [sp.gen_vector(n, 50 + i) for i in range(4)]
+    want = [m.spmv(x, sp.Kernel.CRS)[0] for x in xs]
+    ell_want = m.convert(sp.Format.ELL)
+    want_ell = [ell_want.spmv(x, sp.Kernel.ELL_INNER)[0] for x in xs]
+    errors = []
+
+    def work(i):
+        try:
+            stream = torch.cuda.Stream()
+            sp.set_stream(stream.cuda_stream)  # thread-local
+            for _ in range(5):
+                y, _ = m.spmv(xs[i], sp.Kernel.CRS)
+                assert y.tobytes() == want[i].tobytes()
+                e = m.convert(sp.Format.ELL)
+                y2, _ = e.spmv(xs[i], sp.Kernel.ELL_INNER)
+                assert y2.tobytes() == want_ell[i].tobytes()
+                e.free()
+                assert m.row_stats().max_row == m.info().max_row_entries
+        except Exception as ex:  # noqa: BLE001
+            errors.append(f"thread {i}: {ex!r}")
+
+    threads = [threading.Thread(target=work, args=(i,)) for i in range(4)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+
+
 def test_row_block_shards_single_gpu(gpu, port):
     """Row-block shards (the multi-GPU layout) run on one GPU: per-shard
     SpMV assembled == full SpMV (1e-12), and each shard's ELL equals the
