@@ -64,13 +64,6 @@ int spmvtk_k_crs_to_ccs(int64_t n, int64_t nnz, const int32_t* irp,
                         const int32_t* icol, const double* val,
                         int32_t* col_ptr, int32_t* row_idx, double* out_val,
                         void* scratch, void* stream);
-/* Earlier formulation (column histogram + atomic cursors + per-column
- * fix-up sort); same result, kept for comparison. */
-int spmvtk_k_crs_to_ccs_atomic(int64_t n, int64_t nnz, const int32_t* irp,
-                               const int32_t* icol, const double* val,
-                               int32_t* col_ptr, int32_t* row_idx, double* out_val,
-                               void* scratch, void* stream);
-
 /* Exclusive scan of n int32 counts into out[0..n] (out[n] = total). */
 size_t spmvtk_k_scan_scratch_bytes(int64_t n);
 int spmvtk_k_exclusive_scan(const int32_t* in, int32_t* out, int64_t n,

@@ -98,112 +98,8 @@ __global__ void __launch_bounds__(256) k_crs_to_coo_row(const int32_t* __restric
 }
 
 // ---- CRS -> CCS ------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_col_hist(const int32_t* __restrict__ icol,
-                                                  int64_t nnz, int32_t* count) {
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; p < nnz;
-       p += stride)
-    atomicAdd(count + ld_stream(icol + p), 1);
-}
-
-// pass 3 (convert.cpp:43-51): each entry takes the next free slot of its
-// column.  Slot order inside a column is arbitrary here; k_ccs_fix_* restore
-// ascending rows afterwards (rows are distinct within a column, so sorting on
-// the row reproduces the reference order exactly).
-__global__ void __launch_bounds__(256) k_ccs_scatter(const int32_t* __restrict__ irp,
-                                                     const int32_t* __restrict__ icol,
-                                                     const double* __restrict__ val,
-                                                     int64_t n, int rows_per_warp,
-                                                     int32_t* cursor,
-                                                     int4* __restrict__ rec) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int64_t rb = warp * rows_per_warp;
-  if (rb >= n) return;
-  const int64_t re = min(rb + rows_per_warp, n);
-  const int32_t e0 = __ldg(irp + rb), e1 = __ldg(irp + re);
-  SegWindow w;
-  w.r0 = rb;
-  w.load(irp, re, lane);
-  for (int32_t base = e0; base < e1; base += 32) {
-    int32_t p = base + lane;
-    bool valid = p < e1;
-    int32_t c = 0;
-    double v = 0.0;
-    if (valid) {
-      c = ld_stream(icol + p);
-      v = ld_stream(val + p);
-    }
-    int32_t row = resolve_segment(w, irp, re, lane, p, valid);
-    if (valid) {
-      // one 16-byte (row, value) record per entry: a single half-sector
-      // store instead of a 4-byte and an 8-byte store into two arrays (the
-      // random partial-sector writes dominated this kernel's DRAM traffic)
-      const int32_t slot = atomicAdd(cursor + c, 1);
-      rec[slot] = make_int4(row, 0, __double2loint(v), __double2hiint(v));
-    }
-  }
-}
-
+// 16-byte (col, row, value) records of the partition passes
 __device__ __forceinline__ double rec_val(const int4& r) { return __hiloint2double(r.w, r.z); }
-
-// Columns of length <= 32: one warp per column, bitonic sort in registers on
-// a packed key (row << 5 | source lane); values follow by shuffle.  Sorted
-// columns (the common case) exit after one ballot.  Longer columns are queued
-// for the block-level passes.
-constexpr int kShortCol = 32;
-constexpr int kMediumCol = 4096;
-
-__global__ void __launch_bounds__(256) k_ccs_fix_short(const int32_t* __restrict__ col_ptr,
-                                                       int64_t n, const int4* __restrict__ rec,
-                                                       int32_t* __restrict__ row_idx,
-                                                       double* __restrict__ vals, int32_t* queue,
-                                                       int32_t* queue_len, bool packed_ok) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-  for (int64_t j = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; j < n;
-       j += warps) {
-    const int32_t a = __ldg(col_ptr + j), b = __ldg(col_ptr + j + 1);
-    const int32_t len = b - a;
-    if (len <= 0) continue;
-    if (len > kShortCol || !packed_ok) {
-      if (lane == 0) queue[atomicAdd(queue_len, 1)] = static_cast<int32_t>(j);
-      continue;
-    }
-    int4 rc = make_int4(INT_MAX, 0, 0, 0);
-    if (lane < len) rc = ld_stream4(rec + a + lane);
-    const int32_t r = rc.x;
-    const double v = rec_val(rc);
-    const int32_t rn = __shfl_down_sync(kFull, r, 1);
-    const bool desc = (lane + 1 < len) && rn < r;
-    if (!__any_sync(kFull, desc)) {
-      if (lane < len) {
-        row_idx[a + lane] = r;
-        vals[a + lane] = v;
-      }
-      continue;
-    }
-    // rows < 2^26 so (row << 5 | lane) fits; padding lanes sort last
-    uint32_t key = lane < len ? (static_cast<uint32_t>(r) << 5) | lane : 0xffffffffu;
-#pragma unroll
-    for (int size = 2; size <= 32; size <<= 1) {
-#pragma unroll
-      for (int d = size >> 1; d > 0; d >>= 1) {
-        uint32_t other = __shfl_xor_sync(kFull, key, d);
-        bool up = ((lane & size) == 0);
-        bool lower = (lane & d) == 0;
-        uint32_t mn = min(key, other), mx = max(key, other);
-        key = (lower == up) ? mn : mx;
-      }
-    }
-    int src = static_cast<int>(key & 31u);
-    double sv = __shfl_sync(kFull, v, src);
-    if (lane < len) {
-      row_idx[a + lane] = static_cast<int32_t>(key >> 5);
-      vals[a + lane] = sv;
-    }
-  }
-}
 
 // Bitonic sort (all comparators ascending, "flip" first stage) of the
 // segment key[0..len) with payload; elements past len act as +inf and are
@@ -235,43 +131,6 @@ __device__ void block_bitonic(KeyPtr key, ValPtr val, int32_t len) {
       }
       __syncthreads();
     }
-  }
-}
-
-__global__ void __launch_bounds__(512) k_ccs_fix_long(const int32_t* __restrict__ col_ptr,
-                                                      const int4* __restrict__ rec,
-                                                      int32_t* row_idx, double* vals,
-                                                      const int32_t* queue,
-                                                      const int32_t* queue_len) {
-  __shared__ int32_t s_key[kMediumCol];
-  __shared__ double s_val[kMediumCol];
-  const int32_t count = *queue_len;
-  for (int32_t q = blockIdx.x; q < count; q += gridDim.x) {
-    const int32_t j = queue[q];
-    const int32_t a = col_ptr[j], len = col_ptr[j + 1] - a;
-    if (len <= kMediumCol) {
-      for (int32_t t = threadIdx.x; t < len; t += blockDim.x) {
-        const int4 rc = rec[a + t];
-        s_key[t] = rc.x;
-        s_val[t] = rec_val(rc);
-      }
-      __syncthreads();
-      block_bitonic(s_key, s_val, len);
-      for (int32_t t = threadIdx.x; t < len; t += blockDim.x) {
-        row_idx[a + t] = s_key[t];
-        vals[a + t] = s_val[t];
-      }
-    } else {
-      // very long column: unpack, then the same network in global memory (L2)
-      for (int32_t t = threadIdx.x; t < len; t += blockDim.x) {
-        const int4 rc = rec[a + t];
-        row_idx[a + t] = rc.x;
-        vals[a + t] = rec_val(rc);
-      }
-      __syncthreads();
-      block_bitonic(row_idx + a, vals + a, len);
-    }
-    __syncthreads();
   }
 }
 
@@ -1086,11 +945,7 @@ size_t spmvtk_k_ccs_scratch_bytes(int64_t n, int64_t nnz) {
                           align256((kSlices + 1) * 4) + 2 * align256(t * 4) +
                           2 * align256(tc * 4) + 2 * align256((static_cast<size_t>(bp.nb) + 1) * 4) +
                           align256(spmvtk_k_scan_scratch_bytes(static_cast<int64_t>(t))) + 1024;
-  // the atomic-cursor variant needs count/cursor/queue over n columns
-  const size_t atomic = static_cast<size_t>(nnz) * 16 +
-                        (static_cast<size_t>(n + 1) * 3 + 4) * sizeof(int32_t) +
-                        spmvtk_k_scan_scratch_bytes(n + 1) + 1024;
-  return bucketed > atomic ? bucketed : atomic;
+  return bucketed;
 }
 
 namespace {
@@ -1198,42 +1053,6 @@ int spmvtk_k_crs_to_ccs(int64_t n, int64_t nnz, const int32_t* irp, const int32_
   SPMVTK_LAUNCH_RETURN();
 }
 
-// the previous, atomic-cursor formulation (kept for comparison / tuning)
-int spmvtk_k_crs_to_ccs_atomic(int64_t n, int64_t nnz, const int32_t* irp, const int32_t* icol,
-                               const double* val, int32_t* col_ptr, int32_t* row_idx,
-                               double* out_val, void* scratch, void* stream) {
-  cudaStream_t s = as_stream(stream);
-  uintptr_t base = (reinterpret_cast<uintptr_t>(scratch) + 255) & ~static_cast<uintptr_t>(255);
-  int4* rec = reinterpret_cast<int4*>(base);
-  int32_t* count = reinterpret_cast<int32_t*>(rec + nnz);
-  int32_t* cursor = count + (n + 1);
-  int32_t* queue = cursor + (n + 1);
-  int32_t* queue_len = queue + n;
-  // keep the scan scratch aligned
-  uintptr_t sp = reinterpret_cast<uintptr_t>(queue_len + 4);
-  sp = (sp + 255) & ~static_cast<uintptr_t>(255);
-  void* scan_scratch = reinterpret_cast<void*>(sp);
-
-  cudaMemsetAsync(count, 0, static_cast<size_t>(n + 1) * sizeof(int32_t), s);
-  cudaMemsetAsync(queue_len, 0, sizeof(int32_t), s);
-  if (nnz > 0) k_col_hist<<<grid_for(nnz, 256), 256, 0, s>>>(icol, nnz, count);
-  int rc = spmvtk_k_exclusive_scan(count, col_ptr, n, scan_scratch, stream);
-  if (rc) return rc;
-  if (nnz == 0 || n == 0) SPMVTK_LAUNCH_RETURN();
-  cudaMemcpyAsync(cursor, col_ptr, static_cast<size_t>(n) * sizeof(int32_t),
-                  cudaMemcpyDeviceToDevice, s);
-  int rpw = rows_per_warp_for(n, nnz);
-  int64_t warps = (n + rpw - 1) / rpw;
-  int64_t blocks = (warps * 32 + 255) / 256;
-  k_ccs_scatter<<<static_cast<unsigned>(blocks), 256, 0, s>>>(irp, icol, val, n, rpw, cursor,
-                                                             rec);
-  k_ccs_fix_short<<<grid_for(n * 32, 256, 16), 256, 0, s>>>(col_ptr, n, rec, row_idx, out_val,
-                                                            queue, queue_len,
-                                                            n < (int64_t(1) << 26));
-  k_ccs_fix_long<<<kSMs * 2, 512, 0, s>>>(col_ptr, rec, row_idx, out_val, queue, queue_len);
-  SPMVTK_LAUNCH_RETURN();
-}
-
 int spmvtk_k_crs_to_ell_cm(int64_t n, int32_t nz, int64_t ld, const int32_t* irp,
                            const int32_t* icol, const double* val, double* out_val,
                            int32_t* out_col, int32_t* out_count, int64_t pad_base,
@@ -1295,10 +1114,6 @@ void preload_convert() {
   cudaFuncAttributes a;
   cudaFuncGetAttributes(&a, k_expand_ptr);
   cudaFuncGetAttributes(&a, k_crs_to_coo_row);
-  cudaFuncGetAttributes(&a, k_col_hist);
-  cudaFuncGetAttributes(&a, k_ccs_scatter);
-  cudaFuncGetAttributes(&a, k_ccs_fix_short);
-  cudaFuncGetAttributes(&a, k_ccs_fix_long);
   cudaFuncGetAttributes(&a, k_slice_rows);
   cudaFuncGetAttributes(&a, k_bkt_count);
   cudaFuncGetAttributes(&a, k_bkt_scatter);
