@@ -12,7 +12,7 @@ from paper_2407_00019_b200 import spmvtk as sp  # noqa: E402
 
 lib = sp.load_library()
 sp.set_stream(torch.cuda.current_stream().cuda_stream)
-SETTINGS = [(9, 148, 1024), (9, 296, 512), (9, 444, 512), (9, 296, 1024)]
+SETTINGS = [(9, 148, 1024)]
 for cfg, param in ((2, 1 << 20), (3, 128), (4, 1 << 22), (5, 1 << 21)):
     m = sp.HostCrs(cfg, param).upload()
     for coarse, ns, stt in SETTINGS:
