@@ -194,6 +194,26 @@ def l2_resident_graph(sp, torch, seed, peak, iters=1000):
     return out
 
 
+def gather_peak(sp, torch, n_pow2=1 << 20, iters=256):
+    """Measured random-gather rate (8-byte loads, L2-resident x of n_pow2
+    doubles, nothing else in flight): the denominator of the gather roofline."""
+    lib = sp.load_library()
+    x = torch.zeros(n_pow2, dtype=torch.float64, device="cuda")
+    out = torch.zeros(1, dtype=torch.float64, device="cuda")
+    stream = torch.cuda.current_stream().cuda_stream
+    rc = lib.spmvtk_k_gather_probe(x.data_ptr(), n_pow2, iters, out.data_ptr(), stream)
+    if rc:
+        raise RuntimeError(f"gather probe failed ({rc})")
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(10):
+        lib.spmvtk_k_gather_probe(x.data_ptr(), n_pow2, iters, out.data_ptr(), stream)
+    e1.record()
+    torch.cuda.synchronize()
+    t = e0.elapsed_time(e1) * 1e-3 / 10
+    return 1024 * 148 * iters / t
+
+
 def cpu_model() -> str:
     try:
         with open("/proc/cpuinfo") as f:
@@ -398,6 +418,18 @@ def impl_ours(args):
         t_step = timed(best, args.steps)
     bytes_step = spmv_bytes(best, n, nnz, nz)
     value = bytes_step / t_step / 1e9
+    # second roofline: the x gathers.  Random columns make every x load an
+    # L2 sector fetch; their rate, not HBM bandwidth, bounds config 2
+    # (DESIGN.md §3).  Gathers per step = nnz (padding slots read the own
+    # row's x, coalesced); peak = the measured random-gather rate.
+    try:
+        gpk = gather_peak(sp, torch)
+        gather_roofline = {"bound": "l2-gather", "achieved": nnz / t_step / 1e9,
+                           "peak": gpk / 1e9, "unit": "Ggathers/s",
+                           "frac": (nnz / t_step) / gpk,
+                           "peak_kind": "measured live (spmvtk_k_gather_probe)"}
+    except Exception as e:  # noqa: BLE001 -- reported, not fatal
+        gather_roofline = {"error": f"{type(e).__name__}: {e}"[:200]}
 
     # ---- e2e: through spmvtk_spmv() with pinned host buffers
     xh = torch.from_numpy(sp.gen_vector(n, args.seed + 1)).pin_memory()
@@ -506,6 +538,7 @@ def impl_ours(args):
                      "frac": value / peak, "traffic": ncu_traffic(args.config, best),
                      "peak_kind": peak_kind,
                      "kernel": best, "bytes_per_launch": bytes_step},
+        "roofline_gather": gather_roofline,
         "e2e": {"value": bytes_step / t_e2e / 1e9, "unit": "GB/s", "h2d_bytes_per_step": 8 * n,
                 "d2h_bytes_per_step": 8 * n, "ms_per_step": t_e2e * 1e3,
                 "api": "spmvtk_pipeline_submit/wait (C ABI streaming host SpMV, pinned "

@@ -172,6 +172,12 @@ int spmvtk_k_flags_signal(const struct spmvtk_flag_targets* targets, uint64_t va
 int spmvtk_k_flags_wait(const uint64_t* flags, int32_t n, uint64_t value,
                         uint64_t timeout_ns, uint32_t* status, void* stream);
 
+/* Random 8-byte gathers from x[0..n_pow2) (L2-resident), 2 CTAs x 512
+ * threads per SM, `iters` per thread: the gather-rate roofline of the SpMV
+ * kernels (gathers = 1024 * SMs * iters). */
+int spmvtk_k_gather_probe(const double* x, int64_t n_pow2, int iters, double* out,
+                          void* stream);
+
 /* Tuning override for experiments ("crs_variant": -1 = heuristic, 0..9 pick
  * a (lanes per row, rows per sub-warp) instance of the CRS kernel). */
 int spmvtk_k_tune(const char* key, int value);

@@ -266,6 +266,30 @@ __global__ void k_flags_wait(const uint64_t* flags, int n, uint64_t value, uint6
   }
 }
 
+// ---- random-gather rate probe -------------------------------------------
+// The roofline denominator of the x gathers: 8-byte loads at hashed
+// addresses of an L2-resident vector, nothing else in flight (B200: ~1 per
+// SM-cycle, profiles/r01_microbench_gather.txt).
+__device__ __forceinline__ uint32_t probe_hash(uint32_t x) {
+  x ^= x >> 16;
+  x *= 0x7feb352du;
+  x ^= x >> 15;
+  x *= 0x846ca68bu;
+  x ^= x >> 16;
+  return x;
+}
+__global__ void __launch_bounds__(512) k_gather_probe(const double* __restrict__ x, uint32_t mask,
+                                                      int iters, double* out) {
+  double acc = 0.0;
+  uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+#pragma unroll 8
+  for (int i = 0; i < iters; ++i) {
+    s = probe_hash(s + i);
+    acc += __ldg(x + (s & mask));
+  }
+  if (acc == 1.2345) out[0] = acc;  // keeps the loads alive
+}
+
 }  // namespace
 
 extern "C" {
@@ -333,6 +357,7 @@ int spmvtk_k_exclusive_scan(const int32_t* in, int32_t* out, int64_t n,
 namespace spmvtk_dev {
 void preload_util() {
   cudaFuncAttributes a;
+  cudaFuncGetAttributes(&a, k_gather_probe);
   cudaFuncGetAttributes(&a, k_flags_signal);
   cudaFuncGetAttributes(&a, k_flags_wait);
   cudaFuncGetAttributes(&a, k_row_stats);
@@ -366,3 +391,12 @@ int spmvtk_k_flags_wait(const uint64_t* flags, int32_t n, uint64_t value, uint64
 }
 
 }  // extern "C"
+
+extern "C" int spmvtk_k_gather_probe(const double* x, int64_t n_pow2, int iters, double* out,
+                                     void* stream) {
+  if (n_pow2 <= 0 || (n_pow2 & (n_pow2 - 1)) != 0 || iters <= 0)
+    return static_cast<int>(cudaErrorInvalidValue);
+  k_gather_probe<<<kSMs * 2, 512, 0, as_stream(stream)>>>(x, static_cast<uint32_t>(n_pow2 - 1),
+                                                          iters, out);
+  SPMVTK_LAUNCH_RETURN();
+}

@@ -216,6 +216,7 @@ SIGNATURES = {
     "spmvtk_version": (C.c_char_p, []),
     # lower C ABI (device pointers); only the tuning knob is used from Python
     "spmvtk_k_tune": (C.c_int, [C.c_char_p, C.c_int]),
+    "spmvtk_k_gather_probe": (C.c_int, [_P, _i64, C.c_int, _P, _P]),
 }
 
 _lib: C.CDLL | None = None
