@@ -133,7 +133,7 @@ __global__ void k_descents(const int32_t* __restrict__ key, int64_t len,
   if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(bad, cnt);
 }
 
-// ---- exclusive scan (reduce-then-scan, tiles of 4096) --------------------
+// ---- exclusive scan (tiles of 4096) -----------------------------------------
 constexpr int kScanThreads = 256;
 constexpr int kScanItems = 16;
 constexpr int kScanTile = kScanThreads * kScanItems;
@@ -171,59 +171,68 @@ __device__ __forceinline__ void load_items(const int32_t* in, int64_t n, int64_t
   }
 }
 
-__global__ void __launch_bounds__(kScanThreads) k_scan_tiles(const int32_t* __restrict__ in,
-                                                             int64_t n, int32_t* tile_sums) {
-  __shared__ int32_t s_warp[kScanThreads / 32];
-  __shared__ int32_t total;
-  int32_t it[kScanItems];
-  int64_t first = static_cast<int64_t>(blockIdx.x) * kScanTile +
-                  static_cast<int64_t>(threadIdx.x) * kScanItems;
-  load_items(in, n, first, it);
-  int32_t s = 0;
-#pragma unroll
-  for (int j = 0; j < kScanItems; ++j) s += it[j];
-  block_exclusive_scan(s, s_warp, &total);
-  if (threadIdx.x == 0) tile_sums[blockIdx.x] = total;
+// ---- single-pass exclusive scan (decoupled look-back) --------------------
+// One launch: tiles take tickets in launch order, publish their aggregate,
+// then walk back over predecessors (aggregate or inclusive prefix) and
+// publish their inclusive prefix.  Status word per tile: bits 63:62 flag
+// (0 none, 1 aggregate, 2 inclusive), bits 31:0 the value.
+__device__ __forceinline__ void publish(unsigned long long* st, unsigned long long flag,
+                                        int32_t v) {
+  const unsigned long long w = (flag << 62) | static_cast<uint32_t>(v);
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(st), "l"(w) : "memory");
+}
+__device__ __forceinline__ unsigned long long peek(const unsigned long long* st) {
+  unsigned long long w;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(w) : "l"(st) : "memory");
+  return w;
 }
 
-// single block: exclusive scan of the tile sums, in place
-__global__ void __launch_bounds__(kScanThreads) k_scan_tile_sums(int32_t* tile_sums,
-                                                                 int64_t tiles) {
+__global__ void __launch_bounds__(kScanThreads) k_scan_lookback(const int32_t* __restrict__ in,
+                                                                int32_t* __restrict__ out,
+                                                                int64_t n, int64_t tiles,
+                                                                unsigned long long* status,
+                                                                unsigned int* ticket) {
   __shared__ int32_t s_warp[kScanThreads / 32];
   __shared__ int32_t total;
-  int32_t carry = 0;
-  for (int64_t base = 0; base < tiles; base += kScanThreads) {
-    int64_t i = base + threadIdx.x;
-    int32_t v = i < tiles ? tile_sums[i] : 0;
-    int32_t ex = block_exclusive_scan(v, s_warp, &total);
-    if (i < tiles) tile_sums[i] = ex + carry;
-    carry += total;
-    __syncthreads();
+  __shared__ int32_t s_prefix;
+  __shared__ unsigned int s_tile;
+  if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+  __syncthreads();
+  const int64_t tile = s_tile;
+  int32_t it[kScanItems];
+  const int64_t first = tile * kScanTile + static_cast<int64_t>(threadIdx.x) * kScanItems;
+  load_items(in, n, first, it);
+  int32_t sum = 0;
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) sum += it[j];
+  const int32_t ex = block_exclusive_scan(sum, s_warp, &total);
+  if (threadIdx.x == 0) {
+    int32_t prefix = 0;
+    if (tile == 0) {
+      publish(status, 2, total);
+    } else {
+      publish(status + tile, 1, total);
+      for (int64_t p = tile - 1;; ) {
+        const unsigned long long w = peek(status + p);
+        const unsigned long long flag = w >> 62;
+        if (flag == 0) continue;  // predecessor still scanning its tile
+        prefix += static_cast<int32_t>(static_cast<uint32_t>(w));
+        if (flag == 2) break;
+        --p;
+      }
+      publish(status + tile, 2, prefix + total);
+    }
+    s_prefix = prefix;
   }
-}
-
-__global__ void __launch_bounds__(kScanThreads) k_scan_apply(const int32_t* __restrict__ in,
-                                                             int32_t* __restrict__ out,
-                                                             int64_t n,
-                                                             const int32_t* tile_sums,
-                                                             int64_t tiles) {
-  __shared__ int32_t s_warp[kScanThreads / 32];
-  __shared__ int32_t total;
-  int32_t it[kScanItems];
-  int64_t first = static_cast<int64_t>(blockIdx.x) * kScanTile +
-                  static_cast<int64_t>(threadIdx.x) * kScanItems;
-  load_items(in, n, first, it);
-  int32_t s = 0;
-#pragma unroll
-  for (int j = 0; j < kScanItems; ++j) s += it[j];
-  int32_t run = block_exclusive_scan(s, s_warp, &total) + tile_sums[blockIdx.x];
+  __syncthreads();
+  int32_t run = s_prefix + ex;
 #pragma unroll
   for (int j = 0; j < kScanItems; ++j) {
-    int64_t i = first + j;
+    const int64_t i = first + j;
     if (i < n) out[i] = run;
     run += it[j];
   }
-  if (blockIdx.x == tiles - 1 && threadIdx.x == kScanThreads - 1) out[n] = run;
+  if (tile == tiles - 1 && threadIdx.x == kScanThreads - 1) out[n] = run;
 }
 
 // ---- step flags of the pushed multi-GPU SpMV ------------------------------
@@ -333,8 +342,8 @@ int spmvtk_k_count_descents(const int32_t* key, int64_t len,
 }
 
 size_t spmvtk_k_scan_scratch_bytes(int64_t n) {
-  int64_t tiles = (n + kScanTile - 1) / kScanTile;
-  return static_cast<size_t>((tiles < 1 ? 1 : tiles) * sizeof(int32_t));
+  const int64_t tiles = (n + kScanTile - 1) / kScanTile;
+  return static_cast<size_t>((tiles < 1 ? 1 : tiles) + 1) * sizeof(unsigned long long);
 }
 
 int spmvtk_k_exclusive_scan(const int32_t* in, int32_t* out, int64_t n,
@@ -344,11 +353,12 @@ int spmvtk_k_exclusive_scan(const int32_t* in, int32_t* out, int64_t n,
     cudaMemsetAsync(out, 0, sizeof(int32_t), s);
     SPMVTK_LAUNCH_RETURN();
   }
-  int64_t tiles = (n + kScanTile - 1) / kScanTile;
-  int32_t* sums = static_cast<int32_t*>(scratch);
-  k_scan_tiles<<<static_cast<unsigned>(tiles), kScanThreads, 0, s>>>(in, n, sums);
-  k_scan_tile_sums<<<1, kScanThreads, 0, s>>>(sums, tiles);
-  k_scan_apply<<<static_cast<unsigned>(tiles), kScanThreads, 0, s>>>(in, out, n, sums, tiles);
+  const int64_t tiles = (n + kScanTile - 1) / kScanTile;
+  auto* status = static_cast<unsigned long long*>(scratch);
+  auto* ticket = reinterpret_cast<unsigned int*>(status + tiles);
+  cudaMemsetAsync(status, 0, static_cast<size_t>(tiles + 1) * sizeof(unsigned long long), s);
+  k_scan_lookback<<<static_cast<unsigned>(tiles), kScanThreads, 0, s>>>(in, out, n, tiles,
+                                                                       status, ticket);
   SPMVTK_LAUNCH_RETURN();
 }
 
@@ -365,9 +375,7 @@ void preload_util() {
   cudaFuncGetAttributes(&a, k_widen);
   cudaFuncGetAttributes(&a, k_out_of_range);
   cudaFuncGetAttributes(&a, k_descents);
-  cudaFuncGetAttributes(&a, k_scan_tiles);
-  cudaFuncGetAttributes(&a, k_scan_tile_sums);
-  cudaFuncGetAttributes(&a, k_scan_apply);
+  cudaFuncGetAttributes(&a, k_scan_lookback);
 }
 }  // namespace spmvtk_dev
 
