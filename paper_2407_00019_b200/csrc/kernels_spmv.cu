@@ -936,6 +936,8 @@ __global__ void k_reduce_partials(int64_t n, int32_t splits, const double* __res
 
 int g_l2_hint = 0;  // L2 evict_first (matrix) / evict_last (x) policies
 int g_coo_variant = 1;  // 1: 4 entries per lane (k_spmv_coo_row4), 0: scalar
+int g_coo_chunk = 2048;  // entries per warp of k_spmv_coo_row4 (multiple of 128)
+bool g_coo_chunk_auto = true;  // wave-aware choice between 2048 and 1024
 int g_rm_variant = -1;  // row-major ELL variant override (tuning)
 int g_ell_variant = 0;  // band-major ELL: 0 = LSU loads, 1/2 = TMA bulk-copy ring (8x3 / 4x4)
 
@@ -1103,7 +1105,23 @@ int spmvtk_k_spmv_coo_row(int64_t n, int64_t nnz, const int32_t* row, const int3
   const bool quad = g_coo_variant != 0 && (reinterpret_cast<uintptr_t>(row) & 15) == 0 &&
                     (reinterpret_cast<uintptr_t>(col) & 15) == 0 &&
                     (reinterpret_cast<uintptr_t>(val) & 15) == 0;
-  const int64_t chunk = quad ? 2048 : 1024;
+  int64_t chunk = quad ? g_coo_chunk : 1024;
+  if (quad && g_coo_chunk_auto) {
+    // wave quantisation: one warp per chunk, so pick the chunk (2048 or
+    // 1024 entries) whose warp count fills the last wave of resident warps
+    // best (config 2: 8192 warps = 1.15 waves at 2048 vs 2.3 at 1024;
+    // profiles/r01_tune_coo_chunk.txt)
+    static const int64_t cap = [] {
+      int per_sm = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spmv_coo_row4, 256, 0);
+      return static_cast<int64_t>(kSMs) * std::max(per_sm, 1) * 8;
+    }();
+    auto eff = [&](int64_t c) {
+      const int64_t w = (nnz + c - 1) / c;
+      return static_cast<double>(w) / static_cast<double>(((w + cap - 1) / cap) * cap);
+    };
+    chunk = eff(1024) > eff(2048) + 0.05 ? 1024 : 2048;
+  }
   const int64_t warps = (nnz + chunk - 1) / chunk;
   const int64_t blocks = (warps * 32 + 255) / 256;
   if (quad)
@@ -1215,6 +1233,11 @@ int spmvtk_k_tune(const char* key, int value) {
   }
   if (key && std::string(key) == "ell_variant") {
     g_ell_variant = value;
+    return 0;
+  }
+  if (key && std::string(key) == "coo_chunk") {  // <= 0: automatic
+    g_coo_chunk_auto = value <= 0;
+    g_coo_chunk = value >= 128 ? (value / 128) * 128 : 2048;
     return 0;
   }
   if (key && std::string(key) == "rm_variant") {
