@@ -44,11 +44,14 @@ __global__ void __launch_bounds__(256) k_expand_ptr(const int32_t* __restrict__ 
   }
 }
 
+int g_warp_entries = 512;  // tuning: entries per warp chunk of the row-expanding kernels
+
 int rows_per_warp_for(int64_t n, int64_t nnz) {
-  // aim at ~1024 entries per warp chunk
+  // aim at ~g_warp_entries entries per warp chunk: small chunks, many
+  // warps -- the last wave's tail shrinks (profiles/r01_tune_warp_entries.txt)
   double mean = n > 0 ? static_cast<double>(nnz) / static_cast<double>(n) : 1.0;
-  int64_t r = 32;
-  while (r < 8192 && static_cast<double>(r) * mean < 1024.0) r <<= 1;
+  int64_t r = 8;
+  while (r < 8192 && static_cast<double>(r) * mean < static_cast<double>(g_warp_entries)) r <<= 1;
   return static_cast<int>(r);
 }
 
@@ -920,6 +923,10 @@ int spmvtk_k_tune_convert(const char* key, int value) {
   }
   if (key && std::string(key) == "ccs_sort_threads") {
     g_ccs_sort_threads = value == 256 ? 256 : 512;
+    return 0;
+  }
+  if (key && std::string(key) == "warp_entries") {
+    g_warp_entries = value > 0 ? value : 512;
     return 0;
   }
   if (key && std::string(key) == "ell_flat_rows") {
