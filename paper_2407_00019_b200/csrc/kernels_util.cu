@@ -206,23 +206,34 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_lookback(const int32_t* _
 #pragma unroll
   for (int j = 0; j < kScanItems; ++j) sum += it[j];
   const int32_t ex = block_exclusive_scan(sum, s_warp, &total);
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 32) {
+    // warp 0 looks back 32 predecessors at a time: the nearest one with an
+    // inclusive prefix ends the walk, the aggregates before it add up
+    const int lane = threadIdx.x;
     int32_t prefix = 0;
     if (tile == 0) {
-      publish(status, 2, total);
+      if (lane == 0) publish(status, 2, total);
     } else {
-      publish(status + tile, 1, total);
-      for (int64_t p = tile - 1;; ) {
-        const unsigned long long w = peek(status + p);
+      if (lane == 0) publish(status + tile, 1, total);
+      int64_t end = tile;  // window = predecessors [end - 32, end)
+      for (;;) {
+        const int64_t p = end - 1 - lane;
+        const unsigned long long w = p >= 0 ? peek(status + p) : (2ull << 62);  // p < 0: zero
         const unsigned long long flag = w >> 62;
-        if (flag == 0) continue;  // predecessor still scanning its tile
-        prefix += static_cast<int32_t>(static_cast<uint32_t>(w));
-        if (flag == 2) break;
-        --p;
+        const unsigned incl = __ballot_sync(kFull, flag == 2);
+        const unsigned none = __ballot_sync(kFull, flag == 0);
+        const int stop = incl ? __ffs(incl) - 1 : 31;  // nearest inclusive predecessor
+        const unsigned upto = stop == 31 ? kFull : ((2u << stop) - 1u);
+        if (none & upto) continue;  // a needed predecessor is still scanning: re-read
+        int32_t v = lane <= stop ? static_cast<int32_t>(static_cast<uint32_t>(w)) : 0;
+        for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(kFull, v, d);
+        prefix += v;
+        if (incl) break;
+        end -= 32;
       }
-      publish(status + tile, 2, prefix + total);
+      if (lane == 0) publish(status + tile, 2, prefix + total);
     }
-    s_prefix = prefix;
+    if (lane == 0) s_prefix = prefix;
   }
   __syncthreads();
   int32_t run = s_prefix + ex;
