@@ -46,10 +46,7 @@ def test_reference_unit_suites_pass_on_b200_library(gpu):
 @pytest.mark.gpu
 def test_reference_acceptance_on_b200_library(gpu, tmp_path):
     r = _run("acceptance_b200", "/bin/false", str(tmp_path))
-    status = dict(re.findall(r"\[(PASS|FAIL|SKIP)\] criterion (\d+)", r.stdout)[::-1])
-    got = {}
-    for st, num in re.findall(r"\[(PASS|FAIL|SKIP)\] criterion (\d+)", r.stdout):
-        got[int(num)] = st
+    got = {int(num): st for st, num in
+           re.findall(r"\[(PASS|FAIL|SKIP)\] criterion (\d+)", r.stdout)}
     for c in (1, 2, 3, 4, 5, 9):
         assert got.get(c) == "PASS", (c, r.stdout[-3000:])
-    del status
