@@ -105,6 +105,9 @@ __device__ __forceinline__ double ld_x(const double* p) { return __ldg(p); }
 __device__ __forceinline__ void st_stream(double* p, double v) {
   asm volatile("st.global.L1::no_allocate.f64 [%0], %1;" ::"l"(p), "d"(v));
 }
+__device__ __forceinline__ void st_stream2(double2* p, double2 v) {
+  asm volatile("st.global.L1::no_allocate.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y));
+}
 
 template <typename T>
 __device__ __forceinline__ T warp_sum(T v, int width = 32) {

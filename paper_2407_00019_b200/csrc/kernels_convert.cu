@@ -795,17 +795,29 @@ __global__ void __launch_bounds__(THREADS) k_crs_to_ell_cm_flat(int64_t n, int32
   for (int t = threadIdx.x; t < ROWS; t += THREADS)
     if (r0 + t < n) out_count[r0 + t] = s_ptr[t + 1] - s_ptr[t];
   __syncthreads();
-  const int slots = nz * ROWS;
+  // write phase: a thread stores a row PAIR of one band (16-byte value and
+  // 8-byte column stores; r0 and ld are multiples of 32, so pairs never
+  // straddle ld)
+  constexpr int PAIRS = ROWS / 2;
+  const int slots = nz * PAIRS;
   for (int f = threadIdx.x; f < slots; f += THREADS) {
-    const int k = f / ROWS, row = f % ROWS;
+    const int k = f / PAIRS, row = 2 * (f % PAIRS);
     const int64_t i = r0 + row;
     if (i >= ld) continue;
-    const int32_t a = s_ptr[row], len = s_ptr[row + 1] - a;
-    const bool real = k < len;
+    double v[2];
+    int32_t c[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int32_t a = s_ptr[row + h], len = s_ptr[row + h + 1] - a;
+      const int fs = a - e0 + k;
+      const bool real = k < len;
+      v[h] = real ? s_v[fs + (fs >> 5)] : 0.0;
+      c[h] = real ? s_c[fs + (fs >> 5)]
+                  : static_cast<int32_t>(pad_base + (i + h < n ? i + h : 0));
+    }
     const int64_t slot = static_cast<int64_t>(k) * ld + i;
-    const int fs = a - e0 + k;
-    st_stream(out_val + slot, real ? s_v[fs + (fs >> 5)] : 0.0);
-    out_col[slot] = real ? s_c[fs + (fs >> 5)] : static_cast<int32_t>(pad_base + (i < n ? i : 0));
+    st_stream2(reinterpret_cast<double2*>(out_val + slot), make_double2(v[0], v[1]));
+    *reinterpret_cast<int2*>(out_col + slot) = make_int2(c[0], c[1]);
   }
 }
 
