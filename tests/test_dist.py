@@ -192,3 +192,27 @@ def test_push_exchange_semantics_gloo(world, kind):
         m0 = results[0][1].astype(np.int32)
         assert ((m0 >> 1) & 1).sum() == 4
         assert (m0 & 1).all()
+
+
+def test_interior_range_banded_and_random():
+    """Interior rows (every column in the rank's own block) of a banded shard
+    are the middle run; a scattered shard has none."""
+    n, world, half = 300, 3, 4
+    rows = [np.arange(max(0, i - half), min(n, i + half + 1)) for i in range(n)]
+    ci = np.concatenate(rows).astype(np.int64)
+    rp = np.concatenate([[0], np.cumsum([len(r) for r in rows])]).astype(np.int64)
+    chunk = D.block_rows(n, world)
+    for rank in range(world):
+        r0, lrp, lci, lv = D.shard_arrays(rp, ci, np.ones(ci.shape[0]), n, world, rank)
+        rows_here = D.block_range(n, world, rank)[1] - r0
+        ia, ib = D.interior_range(lrp, lci, r0, rows_here, chunk)
+        want_a = 0 if rank == 0 else half
+        want_b = rows_here if rank == world - 1 else rows_here - half
+        assert (ia, ib) == (want_a, want_b), (rank, ia, ib)
+    rng = np.random.default_rng(1)
+    rows = [np.sort(rng.choice(n, size=12, replace=False)) for _ in range(n)]
+    ci = np.concatenate(rows).astype(np.int64)
+    rp = np.concatenate([[0], np.cumsum([len(r) for r in rows])]).astype(np.int64)
+    r0, lrp, lci, lv = D.shard_arrays(rp, ci, np.ones(ci.shape[0]), n, world, 1)
+    ia, ib = D.interior_range(lrp, lci, r0, chunk, chunk)
+    assert ib - ia <= 2

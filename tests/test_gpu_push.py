@@ -176,3 +176,35 @@ def test_ipc_buffers_roundtrip(gpu):
     ok.ndst = 1
     with pytest.raises(sp.SpmvtkError):
         m.spmv_device_push(sp.Kernel.COO_ROW_OUTER, x.data_ptr(), ok)
+
+
+def test_overlap_step_matches_plain_iteration(gpu, port):
+    """OverlapSpMV (interior rows on a side stream, boundary rows after the
+    exchange) iterates exactly like the plain product: one rank, the rows
+    split into head / interior / tail parts of CRS and ELL handles."""
+    import torch
+    from paper_2407_00019_b200 import dist as D
+    sp = gpu
+    sp.set_stream(torch.cuda.current_stream().cuda_stream)
+    rng = np.random.default_rng(5)
+    n = 5000
+    rp, ci, v = _banded(rng, n, 6)
+    x0 = rng.uniform(-1, 1, n)
+    for fmt in ("crs", "ell"):
+        parts = []
+        kern = sp.Kernel.CRS if fmt == "crs" else sp.Kernel.ELL_INNER
+        for a, b, inner in ((0, 700, False), (700, 4300, True), (4300, n, False)):
+            prp = (rp[a:b + 1] - rp[a]).astype(np.int64)
+            h = sp.Matrix.from_crs_block(b - a, n, a, prp, ci[rp[a]:rp[b]], v[rp[a]:rp[b]])
+            if fmt == "ell":
+                h = h.convert(sp.Format.ELL)
+            parts.append((h, kern, a, b, inner))
+        it = D.OverlapSpMV(n, 1, 0, parts, "cuda")
+        it.set_x(x0)
+        for _ in range(3):
+            it.step(True)
+        torch.cuda.synchronize()
+        want = x0.copy()
+        for _ in range(3):
+            want = port.spmv_crs(n, rp + 1, ci + 1, v, want)
+        assert max_rel_error(it.x.cpu().numpy(), want) <= TOL, fmt
