@@ -50,3 +50,16 @@ def test_reference_acceptance_on_b200_library(gpu, tmp_path):
            re.findall(r"\[(PASS|FAIL|SKIP)\] criterion (\d+)", r.stdout)}
     for c in (1, 2, 3, 4, 5, 9):
         assert got.get(c) == "PASS", (c, r.stdout[-3000:])
+
+
+@pytest.mark.gpu
+def test_plain_c_example_runs(gpu):
+    """examples/spmv_capi.c: generate, convert, multiply, profile and select
+    through the C ABI from plain C (built by __graft_entry__.build())."""
+    exe = os.path.join(os.path.dirname(HERE), "examples", "spmv_capi")
+    if not os.path.exists(exe):
+        pytest.skip("examples/spmv_capi not built")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert r.stdout.strip().endswith("ok")
+    assert "decision=" in r.stdout
