@@ -938,6 +938,12 @@ int g_l2_hint = 0;  // L2 evict_first (matrix) / evict_last (x) policies
 int g_coo_variant = 1;  // 1: 4 entries per lane (k_spmv_coo_row4), 0: scalar
 int g_coo_chunk = 2048;  // entries per warp of k_spmv_coo_row4 (multiple of 128)
 bool g_coo_chunk_auto = true;  // wave-aware choice between 2048 and 1024
+int64_t g_coo_cap = 0;          // resident warps of k_spmv_coo_row4 (occupancy API)
+void coo_row4_capacity() {
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spmv_coo_row4, 256, 0);
+  g_coo_cap = static_cast<int64_t>(kSMs) * std::max(per_sm, 1) * 8;
+}
 int g_rm_variant = -1;  // row-major ELL variant override (tuning)
 int g_ell_variant = 0;  // band-major ELL: 0 = LSU loads, 1/2 = TMA bulk-copy ring (8x3 / 4x4)
 
@@ -1111,11 +1117,8 @@ int spmvtk_k_spmv_coo_row(int64_t n, int64_t nnz, const int32_t* row, const int3
     // 1024 entries) whose warp count fills the last wave of resident warps
     // best (config 2: 8192 warps = 1.15 waves at 2048 vs 2.3 at 1024;
     // profiles/r01_tune_coo_chunk.txt)
-    static const int64_t cap = [] {
-      int per_sm = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spmv_coo_row4, 256, 0);
-      return static_cast<int64_t>(kSMs) * std::max(per_sm, 1) * 8;
-    }();
+    if (g_coo_cap == 0) coo_row4_capacity();  // normally done by spmvtk_k_preload
+    const int64_t cap = g_coo_cap;
     auto eff = [&](int64_t c) {
       const int64_t w = (nnz + c - 1) / c;
       return static_cast<double>(w) / static_cast<double>(((w + cap - 1) / cap) * cap);
@@ -1269,6 +1272,7 @@ int spmvtk_k_preload(void) {
   cudaFuncGetAttributes(&a, k_spmv_vec<4, 2, CrsRows, PushOut>);
   cudaFuncGetAttributes(&a, k_spmv_coo_row);
   cudaFuncGetAttributes(&a, k_spmv_coo_row4);
+  coo_row4_capacity();
   cudaFuncGetAttributes(&a, k_spmv_coo_col);
   cudaFuncGetAttributes(&a, k_spmv_ell_cm<4, false>);
   cudaFuncGetAttributes(&a, k_spmv_ell_cm<4, true>);
