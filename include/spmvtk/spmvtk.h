@@ -262,6 +262,10 @@ spmvtk_status spmvtk_gen_baseline_host(int config, int64_t param, double dparam,
 spmvtk_status spmvtk_host_crs_export(const spmvtk_host_crs* h, int64_t* row_ptr,
                                      int64_t* col_idx, double* values, int index_base);
 void spmvtk_host_crs_free(spmvtk_host_crs* h);
+/* Matrix Market file -> host CRS (no device work; same parser and refusals
+ * as spmvtk_read_matrix_market, multi-threaded). */
+spmvtk_status spmvtk_read_matrix_market_host(const char* path, spmvtk_host_crs** out,
+                                             int64_t* n, int64_t* nnz);
 /* Uploads a host CRS (from spmvtk_gen_baseline_host) into a device handle. */
 spmvtk_status spmvtk_matrix_from_host_crs(const spmvtk_host_crs* h, spmvtk_matrix** out);
 

@@ -225,6 +225,15 @@ class Ref:
         L.spmvtk_gen_cv_target.argtypes = [_i64, C.c_double, C.c_double, C.c_uint64,
                                            C.POINTER(_P)]
         L.spmvtk_matrix_get_format.argtypes = [_P]
+        L.spmvtk_read_matrix_market.argtypes = [C.c_char_p, C.POINTER(_P)]
+        L.spmvtk_write_matrix_market.argtypes = [_P, C.c_char_p]
+
+    def read_matrix_market(self, path: str):
+        """The reference parser: (status, message, handle or None)."""
+        h = C.c_void_p()
+        st = self.lib.spmvtk_read_matrix_market(str(path).encode(), C.byref(h))
+        msg = (self.lib.spmvtk_last_error() or b"").decode()
+        return st, msg, (h if st == 0 else None)
 
     def err(self) -> str:
         return (self.lib.ref_last_error() or b"").decode()

@@ -646,6 +646,19 @@ spmvtk_status spmvtk_host_crs_export(const spmvtk_host_crs* hc, int64_t* row_ptr
 
 void spmvtk_host_crs_free(spmvtk_host_crs* h) { delete h; }
 
+spmvtk_status spmvtk_read_matrix_market_host(const char* path, spmvtk_host_crs** out, int64_t* n,
+                                             int64_t* nnz) {
+  return guarded([&] {
+    need(path);
+    need(out, "null output");
+    auto h = std::make_unique<spmvtk_host_crs>();
+    h->h = mm::read(path);
+    if (n) *n = h->h.n;
+    if (nnz) *nnz = h->h.nnz();
+    *out = h.release();
+  });
+}
+
 spmvtk_status spmvtk_matrix_from_host_crs(const spmvtk_host_crs* h, spmvtk_matrix** out) {
   return guarded([&] {
     need(h);

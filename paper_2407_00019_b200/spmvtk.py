@@ -193,6 +193,8 @@ SIGNATURES = {
     "spmvtk_gen_vector": (C.c_int, [_i64, _u64, _P]),
     "spmvtk_gen_baseline_host": (C.c_int, [C.c_int, _i64, _d, _u64, _PP, C.POINTER(_i64),
                                            C.POINTER(_i64)]),
+    "spmvtk_read_matrix_market_host": (C.c_int, [C.c_char_p, _PP, C.POINTER(_i64),
+                                                 C.POINTER(_i64)]),
     "spmvtk_host_crs_export": (C.c_int, [_P, _P, _P, _P, C.c_int]),
     "spmvtk_host_crs_free": (None, [_P]),
     "spmvtk_matrix_from_host_crs": (C.c_int, [_P, _PP]),
@@ -623,6 +625,18 @@ class HostCrs:
         _check(self._lib.spmvtk_gen_baseline_host(config, param, float(dparam), seed,
                                                   C.byref(self._h), C.byref(n), C.byref(nnz)))
         self.n, self.nnz = n.value, nnz.value
+
+    @classmethod
+    def read_matrix_market(cls, path: str) -> "HostCrs":
+        """Matrix Market file -> host CRS (no device work)."""
+        self = cls.__new__(cls)
+        self._lib = load_library()
+        self._h = C.c_void_p()
+        n, nnz = _i64(), _i64()
+        _check(self._lib.spmvtk_read_matrix_market_host(str(path).encode(), C.byref(self._h),
+                                                        C.byref(n), C.byref(nnz)))
+        self.n, self.nnz = n.value, nnz.value
+        return self
 
     def arrays(self, index_base: int = 1):
         rp = np.empty(self.n + 1, np.int64)
