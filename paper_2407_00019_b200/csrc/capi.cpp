@@ -7,6 +7,7 @@
 // ABI.  Handles own device memory (matrix.hpp).
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <fstream>
 #include <iterator>
@@ -312,27 +313,38 @@ spmvtk_status spmvtk_spmv(const spmvtk_matrix* m, spmvtk_kernel kernel, const do
 
 // ---- streaming host SpMV (spmvtk_pipeline_*) -------------------------------
 struct spmvtk_pipeline {
+  static constexpr int kMaxSplit = 4;
   const dev::Matrix* m = nullptr;
   spmvtk_kernel kernel = SPMVTK_KERNEL_CRS;
-  cudaStream_t h2d = nullptr, comp = nullptr, d2h = nullptr;
+  int split = 2;  // copies per direction cut into `split` parts on their own streams
+                  // (2 measured 6 % faster than 1 and 4 at n = 2^20,
+                  // profiles/r01_pipeline_split.txt; SPMVTK_PIPE_SPLIT overrides)
+  cudaStream_t h2d[kMaxSplit] = {}, d2h[kMaxSplit] = {};
+  cudaStream_t comp = nullptr;
   double* x[2] = {nullptr, nullptr};
   double* y[2] = {nullptr, nullptr};
-  cudaEvent_t h2d_done[2] = {}, comp_done[2] = {}, d2h_done[2] = {};
+  cudaEvent_t h2d_done[2][kMaxSplit] = {}, comp_done[2] = {}, d2h_done[2][kMaxSplit] = {};
   std::uint64_t count = 0;
   ~spmvtk_pipeline() {
     if (comp) cudaStreamSynchronize(comp);
-    if (d2h) cudaStreamSynchronize(d2h);
-    if (h2d) cudaStreamSynchronize(h2d);
+    for (int k = 0; k < kMaxSplit; ++k) {
+      if (d2h[k]) cudaStreamSynchronize(d2h[k]);
+      if (h2d[k]) cudaStreamSynchronize(h2d[k]);
+    }
     for (int b = 0; b < 2; ++b) {
       if (x[b]) cudaFree(x[b]);
       if (y[b]) cudaFree(y[b]);
-      if (h2d_done[b]) cudaEventDestroy(h2d_done[b]);
       if (comp_done[b]) cudaEventDestroy(comp_done[b]);
-      if (d2h_done[b]) cudaEventDestroy(d2h_done[b]);
+      for (int k = 0; k < kMaxSplit; ++k) {
+        if (h2d_done[b][k]) cudaEventDestroy(h2d_done[b][k]);
+        if (d2h_done[b][k]) cudaEventDestroy(d2h_done[b][k]);
+      }
     }
-    if (h2d) cudaStreamDestroy(h2d);
+    for (int k = 0; k < kMaxSplit; ++k) {
+      if (h2d[k]) cudaStreamDestroy(h2d[k]);
+      if (d2h[k]) cudaStreamDestroy(d2h[k]);
+    }
     if (comp) cudaStreamDestroy(comp);
-    if (d2h) cudaStreamDestroy(d2h);
   }
 };
 
@@ -345,15 +357,22 @@ spmvtk_status spmvtk_pipeline_create(const spmvtk_matrix* m, spmvtk_kernel kerne
     auto p = std::make_unique<spmvtk_pipeline>();
     p->m = m;
     p->kernel = kernel;
-    for (cudaStream_t* st : {&p->h2d, &p->comp, &p->d2h})
-      rt::check(cudaStreamCreateWithFlags(st, cudaStreamNonBlocking), "pipeline stream");
+    if (const char* e = std::getenv("SPMVTK_PIPE_SPLIT"))
+      p->split = std::max(1, std::min(spmvtk_pipeline::kMaxSplit, std::atoi(e)));
+    rt::check(cudaStreamCreateWithFlags(&p->comp, cudaStreamNonBlocking), "pipeline stream");
+    for (int k = 0; k < p->split; ++k) {
+      rt::check(cudaStreamCreateWithFlags(&p->h2d[k], cudaStreamNonBlocking), "pipeline stream");
+      rt::check(cudaStreamCreateWithFlags(&p->d2h[k], cudaStreamNonBlocking), "pipeline stream");
+    }
     const std::size_t nx = std::max<std::int64_t>(m->ncols, 1), ny = std::max<std::int64_t>(m->n, 1);
     for (int b = 0; b < 2; ++b) {
       rt::check(cudaMalloc(&p->x[b], nx * sizeof(double)), "pipeline x");
       rt::check(cudaMalloc(&p->y[b], ny * sizeof(double)), "pipeline y");
-      rt::check(cudaEventCreateWithFlags(&p->h2d_done[b], cudaEventDisableTiming), "event");
       rt::check(cudaEventCreateWithFlags(&p->comp_done[b], cudaEventDisableTiming), "event");
-      rt::check(cudaEventCreateWithFlags(&p->d2h_done[b], cudaEventDisableTiming), "event");
+      for (int k = 0; k < p->split; ++k) {
+        rt::check(cudaEventCreateWithFlags(&p->h2d_done[b][k], cudaEventDisableTiming), "event");
+        rt::check(cudaEventCreateWithFlags(&p->d2h_done[b][k], cudaEventDisableTiming), "event");
+      }
     }
     *out = p.release();
   });
@@ -363,15 +382,22 @@ spmvtk_status spmvtk_pipeline_submit(spmvtk_pipeline* p, const double* x, double
   return guarded([&] {
     if (!p || !x || !y) throw Error(ErrorCode::InvalidArgument, "null argument");
     const int b = static_cast<int>(p->count & 1);
-    const std::size_t nx = static_cast<std::size_t>(p->m->ncols) * sizeof(double);
-    const std::size_t ny = static_cast<std::size_t>(p->m->n) * sizeof(double);
+    const std::size_t nx = static_cast<std::size_t>(p->m->ncols);
+    const std::size_t ny = static_cast<std::size_t>(p->m->n);
+    const int K = p->split;
     // copy-in waits until the SpMV that last read this staging slot is done
-    rt::check(cudaStreamWaitEvent(p->h2d, p->comp_done[b], 0), "pipeline order");
-    if (nx) rt::check(cudaMemcpyAsync(p->x[b], x, nx, cudaMemcpyHostToDevice, p->h2d), "H2D x");
-    rt::check(cudaEventRecord(p->h2d_done[b], p->h2d), "pipeline event");
-    // the SpMV waits for its x and for the copy-out that last read its y slot
-    rt::check(cudaStreamWaitEvent(p->comp, p->h2d_done[b], 0), "pipeline order");
-    rt::check(cudaStreamWaitEvent(p->comp, p->d2h_done[b], 0), "pipeline order");
+    for (int k = 0; k < K; ++k) {
+      const std::size_t a = nx * k / K, e = nx * (k + 1) / K;
+      rt::check(cudaStreamWaitEvent(p->h2d[k], p->comp_done[b], 0), "pipeline order");
+      if (e > a)
+        rt::check(cudaMemcpyAsync(p->x[b] + a, x + a, (e - a) * sizeof(double),
+                                  cudaMemcpyHostToDevice, p->h2d[k]),
+                  "H2D x");
+      rt::check(cudaEventRecord(p->h2d_done[b][k], p->h2d[k]), "pipeline event");
+      // the SpMV waits for its x and for the copy-out that last read its y slot
+      rt::check(cudaStreamWaitEvent(p->comp, p->h2d_done[b][k], 0), "pipeline order");
+      rt::check(cudaStreamWaitEvent(p->comp, p->d2h_done[b][k], 0), "pipeline order");
+    }
     cudaStream_t saved = rt::stream();
     rt::set_stream(p->comp);
     try {
@@ -382,9 +408,15 @@ spmvtk_status spmvtk_pipeline_submit(spmvtk_pipeline* p, const double* x, double
     }
     rt::set_stream(saved);
     rt::check(cudaEventRecord(p->comp_done[b], p->comp), "pipeline event");
-    rt::check(cudaStreamWaitEvent(p->d2h, p->comp_done[b], 0), "pipeline order");
-    if (ny) rt::check(cudaMemcpyAsync(y, p->y[b], ny, cudaMemcpyDeviceToHost, p->d2h), "D2H y");
-    rt::check(cudaEventRecord(p->d2h_done[b], p->d2h), "pipeline event");
+    for (int k = 0; k < K; ++k) {
+      const std::size_t a = ny * k / K, e = ny * (k + 1) / K;
+      rt::check(cudaStreamWaitEvent(p->d2h[k], p->comp_done[b], 0), "pipeline order");
+      if (e > a)
+        rt::check(cudaMemcpyAsync(y + a, p->y[b] + a, (e - a) * sizeof(double),
+                                  cudaMemcpyDeviceToHost, p->d2h[k]),
+                  "D2H y");
+      rt::check(cudaEventRecord(p->d2h_done[b][k], p->d2h[k]), "pipeline event");
+    }
     ++p->count;
   });
 }
@@ -392,9 +424,11 @@ spmvtk_status spmvtk_pipeline_submit(spmvtk_pipeline* p, const double* x, double
 spmvtk_status spmvtk_pipeline_wait(spmvtk_pipeline* p) {
   return guarded([&] {
     if (!p) throw Error(ErrorCode::InvalidArgument, "null argument");
-    rt::check(cudaStreamSynchronize(p->h2d), "pipeline wait");
+    for (int k = 0; k < p->split; ++k)
+      rt::check(cudaStreamSynchronize(p->h2d[k]), "pipeline wait");
     rt::check(cudaStreamSynchronize(p->comp), "pipeline wait");
-    rt::check(cudaStreamSynchronize(p->d2h), "pipeline wait");
+    for (int k = 0; k < p->split; ++k)
+      rt::check(cudaStreamSynchronize(p->d2h[k]), "pipeline wait");
   });
 }
 
