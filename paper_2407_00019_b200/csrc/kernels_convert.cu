@@ -147,7 +147,10 @@ __device__ void block_bitonic(KeyPtr key, ValPtr val, int32_t len) {
 //   3. k_bkt_scatter each slice re-reads its rows and appends 16-byte
 //                    records (col, row, value) to its runs with shared-memory
 //                    cursors: writes are kSlices x NB sequential streams that
-//                    fill whole sectors in L2
+//                    fill whole sectors in L2 (variants: staged through shared
+//                    memory for coalesced run writes -- a coarse pass + refine
+//                    when columns scatter over many runs, or per slice over a
+//                    banded matrix's bucket window, k_bkt_scatter_single)
 //   4. k_bkt_sort    one CTA per bucket: counting sort by column in shared
 //                    memory, per-column sort by row (rows are distinct within
 //                    a column, so this restores the reference's order,
@@ -159,12 +162,15 @@ int g_ccs_slices = 148;           // tuning: slices actually used (one per SM)
 int g_ccs_threads = 1024;         // tuning: threads of the count/scatter CTAs
 constexpr int kBktItems = 12;  // records per sort thread (bucket capacity = threads * 12)
 int g_ccs_sort_threads = 512;  // tuning: 256 or 512 (bucket target = 2/3 of the capacity)
+int g_ccs_window = 1;          // tuning: single pass stages slices with <= 1024-bucket windows
 
 // Two-pass or single-pass partition is decided on the device from the
 // number of non-empty (fine bucket, slice) runs counted by k_bkt_count: few
 // runs (banded matrices) keep their write streams L2-resident in one pass;
 // many runs (scattered columns) go through the coarse pass + refine.
 constexpr int32_t kTwoPassRuns = 1 << 17;
+constexpr int kStageU = 4;        // 32-entry batches per lane per staged step
+constexpr int kStageMaxB = 1024;  // buckets (or bucket window) of the staged scatter
 __device__ __forceinline__ bool two_pass(const int32_t* runs) {
   return runs != nullptr && *runs > kTwoPassRuns;
 }
@@ -195,16 +201,33 @@ __global__ void __launch_bounds__(1024) k_bkt_count(const int32_t* __restrict__ 
                                                            const int32_t* __restrict__ slice_row,
                                                            int shift, int nb, int32_t* T,
                                                            int fshift, int32_t* Tc,
-                                                           int32_t* runs) {
+                                                           int32_t* runs, int32_t* win) {
   extern __shared__ int32_t s_hist[];
+  __shared__ int32_t s_lo, s_hi, s_chg, s_smp;
   for (int b = threadIdx.x; b < nb; b += blockDim.x) s_hist[b] = 0;
+  if (threadIdx.x == 0) {
+    s_lo = nb;
+    s_hi = -1;
+    s_chg = 0;
+    s_smp = 0;
+  }
   __syncthreads();
   const int32_t e0 = irp[slice_row[blockIdx.x]], e1 = irp[slice_row[blockIdx.x + 1]];
   const int32_t step = static_cast<int32_t>(blockDim.x);
+  const int lane = threadIdx.x & 31;
   int32_t p = e0 + static_cast<int32_t>(threadIdx.x);
-  for (; p + 3 * step < e1; p += 4 * step) {  // 4 loads in flight per thread
+  int32_t chg = 0, smp = 0;
+  // warp-uniform main loop (its last lane bounds it), 4 loads in flight
+  for (int it = 0; p - lane + 31 + 3 * step < e1; p += 4 * step, ++it) {
     const int32_t c0 = ld_stream(icol + p), c1 = ld_stream(icol + p + step);
     const int32_t c2 = ld_stream(icol + p + 2 * step), c3 = ld_stream(icol + p + 3 * step);
+    if (win && (it & 7) == 0) {  // sample: is an entry in its CRS predecessor's bucket?
+      const int32_t prev = __shfl_up_sync(kFull, c0 >> shift, 1);
+      if (lane) {
+        ++smp;
+        chg += prev != (c0 >> shift);
+      }
+    }
     atomicAdd(&s_hist[c0 >> shift], 1);
     atomicAdd(&s_hist[c1 >> shift], 1);
     atomicAdd(&s_hist[c2 >> shift], 1);
@@ -212,14 +235,39 @@ __global__ void __launch_bounds__(1024) k_bkt_count(const int32_t* __restrict__ 
   }
   for (; p < e1; p += step) atomicAdd(&s_hist[ld_stream(icol + p) >> shift], 1);
   __syncthreads();
-  int32_t nz = 0;
+  int32_t nz = 0, lo = nb, hi = -1;
   for (int b = threadIdx.x; b < nb; b += blockDim.x) {
     T[static_cast<int64_t>(b) * gridDim.x + blockIdx.x] = s_hist[b];
-    nz += s_hist[b] != 0;
+    if (s_hist[b]) {
+      ++nz;
+      lo = min(lo, b);
+      hi = max(hi, b);
+    }
   }
   if (runs) {
     nz = __reduce_add_sync(kFull, static_cast<unsigned>(nz));
     if ((threadIdx.x & 31) == 0 && nz) atomicAdd(runs, nz);
+  }
+  if (win) {  // the slice's non-empty buckets span [lo, hi]
+    lo = __reduce_min_sync(kFull, lo);
+    hi = __reduce_max_sync(kFull, hi);
+    chg = __reduce_add_sync(kFull, static_cast<unsigned>(chg));
+    smp = __reduce_add_sync(kFull, static_cast<unsigned>(smp));
+    if (lane == 0) {
+      atomicMin(&s_lo, lo);
+      atomicMax(&s_hi, hi);
+      atomicAdd(&s_chg, chg);
+      atomicAdd(&s_smp, smp);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      // staged only where most CRS neighbours change bucket: runs of one
+      // bucket inside a row already give the cursor scatter contiguous
+      // stores (27-point stencil), and it skips the staging barriers
+      const bool scattered = 2 * static_cast<int64_t>(s_chg) > s_smp;
+      win[2 * blockIdx.x] = s_hi < 0 ? 0 : s_lo;
+      win[2 * blockIdx.x + 1] = s_hi < 0 ? 0 : scattered ? s_hi + 1 - s_lo : kStageMaxB + 1;
+    }
   }
   if (Tc) {  // coarse buckets of 2^fshift fine buckets (two-pass partition)
     const int F = 1 << fshift, nc = (nb + F - 1) >> fshift;
@@ -234,12 +282,11 @@ __global__ void __launch_bounds__(1024) k_bkt_count(const int32_t* __restrict__ 
   }
 }
 
-__global__ void __launch_bounds__(1024) k_bkt_scatter(
+// cursor scatter: every lane appends its record at a shared cursor of its bucket
+__device__ __forceinline__ void bkt_scatter_cursor(
     const int32_t* __restrict__ irp, const int32_t* __restrict__ icol,
     const double* __restrict__ val, const int32_t* __restrict__ slice_row, int shift, int nb,
-    const int32_t* __restrict__ Toff, int4* __restrict__ rec, const int32_t* runs, bool as_two) {
-  if (runs && two_pass(runs) != as_two) return;
-  extern __shared__ int32_t s_cur[];
+    const int32_t* __restrict__ Toff, int4* __restrict__ rec, int32_t* s_cur) {
   for (int b = threadIdx.x; b < nb; b += blockDim.x)
     s_cur[b] = Toff[static_cast<int64_t>(b) * gridDim.x + blockIdx.x];
   __syncthreads();
@@ -308,23 +355,31 @@ __global__ void __launch_bounds__(1024) k_bkt_scatter(
   }
 }
 
+__global__ void __launch_bounds__(1024) k_bkt_scatter(
+    const int32_t* __restrict__ irp, const int32_t* __restrict__ icol,
+    const double* __restrict__ val, const int32_t* __restrict__ slice_row, int shift, int nb,
+    const int32_t* __restrict__ Toff, int4* __restrict__ rec, const int32_t* runs, bool as_two) {
+  if (runs && two_pass(runs) != as_two) return;
+  extern __shared__ int32_t s_dyn[];
+  bkt_scatter_cursor(irp, icol, val, slice_row, shift, nb, Toff, rec, s_dyn);
+}
+
 // Staged variant for at most kStageMaxB buckets (the coarse pass, or a
 // single pass over few buckets): the 32 warps advance in lock step, 128
 // entries each per step; the step's 4096 records are counting-sorted by
 // bucket in shared memory and written out run by run, so consecutive lanes
 // store consecutive addresses instead of 32 scattered 16-byte records.
-constexpr int kStageU = 4;
-constexpr int kStageMaxB = 1024;
 int g_stage_threads = 1024;  // tuning: 1024 (one CTA per slice per SM) or 512
 
+// Buckets [blo, blo + nbw) (nbw <= kStageMaxB) are renumbered from 0: a
+// window of a banded matrix's buckets, or all of them.
 template <int kStageThreads>
-__global__ void __launch_bounds__(kStageThreads) k_bkt_scatter_staged(
+__device__ __forceinline__ void bkt_scatter_staged(
     const int32_t* __restrict__ irp, const int32_t* __restrict__ icol,
-    const double* __restrict__ val, const int32_t* __restrict__ slice_row, int shift, int nb,
-    const int32_t* __restrict__ Toff, int4* __restrict__ rec, const int32_t* runs, bool as_two) {
-  if (runs && two_pass(runs) != as_two) return;
+    const double* __restrict__ val, const int32_t* __restrict__ slice_row, int shift,
+    int32_t blo, int nbw, const int32_t* __restrict__ Toff, int4* __restrict__ rec,
+    int4* s_rec /* kStageThreads * kStageU records */) {
   constexpr int kP = kStageMaxB / kStageThreads;  // buckets owned per thread
-  extern __shared__ int4 s_rec[];  // kStageThreads * kStageU records
   __shared__ int32_t s_cur[kStageMaxB], s_cnt[kStageMaxB], s_off[kStageMaxB];
   __shared__ int32_t s_wsum[kStageThreads / 32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -332,8 +387,8 @@ __global__ void __launch_bounds__(kStageThreads) k_bkt_scatter_staged(
 #pragma unroll
   for (int j = 0; j < kP; ++j) {
     const int b = tid * kP + j;
-    if (b < nb) {
-      s_cur[b] = Toff[static_cast<int64_t>(b) * gridDim.x + blockIdx.x];
+    if (b < nbw) {
+      s_cur[b] = Toff[static_cast<int64_t>(b + blo) * gridDim.x + blockIdx.x];
       s_cnt[b] = 0;
     }
   }
@@ -387,7 +442,7 @@ __global__ void __launch_bounds__(kStageThreads) k_bkt_scatter_staged(
     resolve_segments<kStageU>(w, irp, r_end, lane, pp, row, need);
 #pragma unroll
     for (int u = 0; u < kStageU; ++u)
-      rk[u] = pp[u] < p1 ? atomicAdd(&s_cnt[c[u] >> shift], 1) : 0;
+      rk[u] = pp[u] < p1 ? atomicAdd(&s_cnt[(c[u] >> shift) - blo], 1) : 0;
     __syncthreads();
     // exclusive scan of the step's bucket counts (thread t owns buckets
     // [t*kP, t*kP + kP))
@@ -396,7 +451,7 @@ __global__ void __launch_bounds__(kStageThreads) k_bkt_scatter_staged(
 #pragma unroll
     for (int j = 0; j < kP; ++j) {
       const int b = tid * kP + j;
-      loc[j] = b < nb ? s_cnt[b] : 0;
+      loc[j] = b < nbw ? s_cnt[b] : 0;
       x += loc[j];
     }
     int32_t inc = x;
@@ -423,7 +478,7 @@ __global__ void __launch_bounds__(kStageThreads) k_bkt_scatter_staged(
 #pragma unroll
       for (int j = 0; j < kP; ++j) {
         const int b = tid * kP + j;
-        if (b < nb) s_off[b] = e;
+        if (b < nbw) s_off[b] = e;
         e += loc[j];
       }
     }
@@ -431,20 +486,20 @@ __global__ void __launch_bounds__(kStageThreads) k_bkt_scatter_staged(
 #pragma unroll
     for (int u = 0; u < kStageU; ++u)
       if (pp[u] < p1)
-        s_rec[s_off[c[u] >> shift] + rk[u]] =
+        s_rec[s_off[(c[u] >> shift) - blo] + rk[u]] =
             make_int4(c[u], row[u], __double2loint(v[u]), __double2hiint(v[u]));
     __syncthreads();
-    const int32_t count = s_off[nb - 1] + s_cnt[nb - 1];
+    const int32_t count = s_off[nbw - 1] + s_cnt[nbw - 1];
     for (int32_t i = tid; i < count; i += kStageThreads) {
       const int4 r = s_rec[i];
-      const int b = r.x >> shift;
+      const int b = (r.x >> shift) - blo;
       rec[s_cur[b] + i - s_off[b]] = r;
     }
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < kP; ++j) {
       const int b = tid * kP + j;
-      if (b < nb) {
+      if (b < nbw) {
         s_cur[b] += s_cnt[b];
         s_cnt[b] = 0;
       }
@@ -456,6 +511,38 @@ __global__ void __launch_bounds__(kStageThreads) k_bkt_scatter_staged(
     }
     __syncthreads();
   }
+}
+
+template <int kStageThreads>
+__global__ void __launch_bounds__(kStageThreads) k_bkt_scatter_staged(
+    const int32_t* __restrict__ irp, const int32_t* __restrict__ icol,
+    const double* __restrict__ val, const int32_t* __restrict__ slice_row, int shift, int nb,
+    const int32_t* __restrict__ Toff, int4* __restrict__ rec, const int32_t* runs, bool as_two) {
+  if (runs && two_pass(runs) != as_two) return;
+  extern __shared__ int4 s_dyn4[];
+  bkt_scatter_staged<kStageThreads>(irp, icol, val, slice_row, shift, 0, nb, Toff, rec, s_dyn4);
+}
+
+// Single pass over more buckets than the staged scatter holds: each slice
+// (CTA) picks its scatter from the window k_bkt_count measured -- staged over
+// its bucket window when that is narrow and CRS neighbours mostly change
+// bucket (banded random columns), else the cursor scatter.  One launch for
+// both, so the choice costs no host round trip and no idle CTAs.
+__global__ void __launch_bounds__(1024) k_bkt_scatter_single(
+    const int32_t* __restrict__ irp, const int32_t* __restrict__ icol,
+    const double* __restrict__ val, const int32_t* __restrict__ slice_row, int shift, int nb,
+    const int32_t* __restrict__ Toff, int4* __restrict__ rec, const int32_t* runs,
+    const int32_t* __restrict__ win) {
+  if (runs && two_pass(runs)) return;
+  const int32_t blo = win[2 * blockIdx.x];
+  const int nbw = win[2 * blockIdx.x + 1];
+  if (nbw == 0) return;  // empty slice
+  extern __shared__ int4 s_dyn4[];
+  if (nbw <= kStageMaxB)
+    bkt_scatter_staged<1024>(irp, icol, val, slice_row, shift, blo, nbw, Toff, rec, s_dyn4);
+  else
+    bkt_scatter_cursor(irp, icol, val, slice_row, shift, nb, Toff, rec,
+                       reinterpret_cast<int32_t*>(s_dyn4));
 }
 
 // Two-pass partition, second pass: the coarse-partitioned records are cut
@@ -929,6 +1016,10 @@ int spmvtk_k_tune_convert(const char* key, int value) {
     g_ccs_slices = value;
     return 0;
   }
+  if (key && std::string(key) == "ccs_window") {
+    g_ccs_window = value != 0;
+    return 0;
+  }
   if (key && std::string(key) == "ccs_threads") {
     g_ccs_threads = value;
     return 0;
@@ -961,7 +1052,8 @@ size_t spmvtk_k_ccs_scratch_bytes(int64_t n, int64_t nnz) {
   const size_t t = static_cast<size_t>(bp.nb) * kSlices + 1;
   const size_t tc = static_cast<size_t>(bp.nc) * kSlices + 1;
   const size_t bucketed = 2 * align256(static_cast<size_t>(nnz) * 16) + 256 +
-                          align256((kSlices + 1) * 4) + 2 * align256(t * 4) +
+                          align256((kSlices + 1) * 4) + align256(kSlices * 2 * 4) +
+                          2 * align256(t * 4) +
                           2 * align256(tc * 4) + 2 * align256((static_cast<size_t>(bp.nb) + 1) * 4) +
                           align256(spmvtk_k_scan_scratch_bytes(static_cast<int64_t>(t))) + 1024;
   return bucketed;
@@ -1001,6 +1093,8 @@ int spmvtk_k_crs_to_ccs(int64_t n, int64_t nnz, const int32_t* irp, const int32_
   };
   int4* rec = static_cast<int4*>(take(static_cast<size_t>(nnz) * 16));
   int32_t* slice_row = static_cast<int32_t*>(take((kSlices + 1) * 4));
+  int32_t* win = g_ccs_window && bp.fshift > 0 ? static_cast<int32_t*>(take(kSlices * 2 * 4))
+                                                : nullptr;
   int32_t* T = static_cast<int32_t*>(take(static_cast<size_t>(tlen + 1) * 4));
   int32_t* Toff = static_cast<int32_t*>(take(static_cast<size_t>(tlen + 1) * 4));
   int32_t* big = static_cast<int32_t*>(take((static_cast<size_t>(bp.nb) + 1) * 4));
@@ -1015,12 +1109,15 @@ int spmvtk_k_crs_to_ccs(int64_t n, int64_t nnz, const int32_t* irp, const int32_
   int32_t* runs = two ? static_cast<int32_t*>(take(4)) : nullptr;
 
   const size_t hist_smem = static_cast<size_t>(bp.nb) * 4;
+  const size_t single_smem = std::max(hist_smem, size_t(1024) * kStageU * sizeof(int4));
   const int cb = 1 << bp.shift;
   const size_t sort_smem = ((static_cast<size_t>(cb + 1) * 4 + 15) & ~static_cast<size_t>(15)) +
                            static_cast<size_t>(g_ccs_sort_threads) * kBktItems * 14;
   static const bool attrs = [] {  // thread-safe one-time setup
     cudaFuncSetAttribute(k_bkt_count, cudaFuncAttributeMaxDynamicSharedMemorySize, 32768 * 4);
     cudaFuncSetAttribute(k_bkt_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, 32768 * 4);
+    cudaFuncSetAttribute(k_bkt_scatter_single, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         32768 * 4);
     cudaFuncSetAttribute(k_bkt_scatter_staged<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          1024 * kStageU * static_cast<int>(sizeof(int4)));
     cudaFuncSetAttribute(k_bkt_scatter_staged<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1036,7 +1133,7 @@ int spmvtk_k_crs_to_ccs(int64_t n, int64_t nnz, const int32_t* irp, const int32_
   if (two) cudaMemsetAsync(runs, 0, sizeof(int32_t), s);
   k_slice_rows<<<(ns + 1 + 3) / 4, 128, 0, s>>>(irp, n, ns, slice_row);
   k_bkt_count<<<ns, nt, hist_smem, s>>>(irp, icol, slice_row, bp.shift, bp.nb, T, bp.fshift,
-                                        Tc, runs);
+                                        Tc, runs, win);
   int rc = spmvtk_k_exclusive_scan(T, Toff, tlen, scan_scratch, stream);
   if (rc) return rc;
   if (two) {
@@ -1054,8 +1151,13 @@ int spmvtk_k_crs_to_ccs(int64_t n, int64_t nnz, const int32_t* irp, const int32_
     k_bkt_refine<<<static_cast<unsigned>((nnz + kRefineItems - 1) / kRefineItems),
                    kRefineThreads, 0, s>>>(rec, nnz, bp.shift, bp.fshift, Toff, ns, fcur, rec2,
                                            runs);
-    k_bkt_scatter<<<ns, nt, hist_smem, s>>>(irp, icol, val, slice_row, bp.shift, bp.nb, Toff,
-                                            rec, runs, false);
+    // single pass: per slice, staged over its bucket window or cursor
+    if (win && nt == 1024)
+      k_bkt_scatter_single<<<ns, 1024, single_smem, s>>>(irp, icol, val, slice_row, bp.shift,
+                                                         bp.nb, Toff, rec, runs, win);
+    else
+      k_bkt_scatter<<<ns, nt, hist_smem, s>>>(irp, icol, val, slice_row, bp.shift, bp.nb, Toff,
+                                              rec, runs, false);
   } else if (bp.nb <= kStageMaxB && g_ccs_coarse > 0) {
     launch_staged(ns, s, irp, icol, val, slice_row, bp.shift, bp.nb, Toff, rec, nullptr, false);
   } else {
@@ -1136,6 +1238,7 @@ void preload_convert() {
   cudaFuncGetAttributes(&a, k_slice_rows);
   cudaFuncGetAttributes(&a, k_bkt_count);
   cudaFuncGetAttributes(&a, k_bkt_scatter);
+  cudaFuncGetAttributes(&a, k_bkt_scatter_single);
   cudaFuncGetAttributes(&a, k_bkt_scatter_staged<1024>);
   cudaFuncGetAttributes(&a, k_bkt_scatter_staged<512>);
   cudaFuncGetAttributes(&a, k_bkt_refine);

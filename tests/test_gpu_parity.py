@@ -321,7 +321,9 @@ def test_ccs_partition_paths(gpu, port):
     """CRS->CCS through each partition path against the C port, bit-exact:
     scattered columns (many runs -> coarse pass + refine) with a 1000-entry
     column (block network inside a bucket) and two dense columns (oversized
-    bucket path); a banded matrix (few runs -> single pass)."""
+    bucket path); a banded matrix (few runs -> single pass); a matrix whose
+    slices split between the windowed staged scatter and the cursor scatter.
+    Both with and without the windowed staged pass."""
     sp = gpu
     rng = np.random.default_rng(21)
     n = 300_000
@@ -338,15 +340,30 @@ def test_ccs_partition_paths(gpu, port):
     rb = np.repeat(np.arange(nb), 24)
     cb = np.clip(rb + rng.integers(-500, 500, size=rb.shape[0]), 0, nb - 1)
     cases.append((nb, *_crs_from_pairs(nb, rb, cb, rng)))
-    for nn, rp, ci, v in cases:
-        m = upload(sp, nn, rp, ci, v)
-        cp, ri, cv = port.crs_to_ccs(nn, rp, ci, v)
-        ccs = m.convert(sp.Format.CCS)
-        np.testing.assert_array_equal(ref_layout(ccs, sp, sp.Array.POINTER), cp)
-        np.testing.assert_array_equal(ref_layout(ccs, sp, sp.Array.ROW_IDX), ri)
-        assert ccs.array(sp.Array.VALUES).tobytes() == cv.tobytes()
-        ccs.free()
-        m.free()
+    # mixed single pass: banded slices (narrow bucket windows -> staged) and,
+    # in the last eighth of the rows, scattered slices (every bucket -> cursor
+    # scatter), with few enough runs to stay single-pass
+    nm = 1 << 20
+    rm = np.repeat(np.arange(nm), 8)
+    cm = np.clip(rm + rng.integers(-2000, 2000, size=rm.shape[0]), 0, nm - 1)
+    tail = rm >= nm - nm // 8
+    cm[tail] = rng.integers(0, nm, size=int(tail.sum()))
+    cases.append((nm, *_crs_from_pairs(nm, rm, cm, rng)))
+    lib = sp.load_library()
+    try:
+        for window in (1, 0):
+            lib.spmvtk_k_tune(b"ccs_window", window)
+            for nn, rp, ci, v in cases:
+                m = upload(sp, nn, rp, ci, v)
+                cp, ri, cv = port.crs_to_ccs(nn, rp, ci, v)
+                ccs = m.convert(sp.Format.CCS)
+                np.testing.assert_array_equal(ref_layout(ccs, sp, sp.Array.POINTER), cp)
+                np.testing.assert_array_equal(ref_layout(ccs, sp, sp.Array.ROW_IDX), ri)
+                assert ccs.array(sp.Array.VALUES).tobytes() == cv.tobytes()
+                ccs.free()
+                m.free()
+    finally:
+        lib.spmvtk_k_tune(b"ccs_window", 1)
 
 
 def test_crs_long_rows_path(gpu, port):

@@ -1,10 +1,12 @@
 """Aggregates an ncu report's per-instruction warp-stall samples of one kernel
 by CUDA source line, using the line table of the kernel's cubin.
 
-    python tools/sass_lines.py rep.ncu-rep KERNEL_SUBSTR build/obj.o [top]
+    python tools/sass_lines.py rep.ncu-rep KERNEL_SUBSTR build/obj.o [top] [skip]
 
 KERNEL_SUBSTR selects the kernel both in the report (regex) and among the
-cubin's mangled names (substring, e.g. k_bkt_sortILi512).  Needs the object
+cubin's mangled names (substring, e.g. k_bkt_sortILi512); "REGEX::SUBSTR"
+gives the two separately (e.g. k_bkt_scatter::13k_bkt_scatterP with skip 1
+for the second matching launch).  Needs the object
 compiled with -lineinfo (the Makefile does)."""
 import collections
 import csv
@@ -17,11 +19,13 @@ import tempfile
 
 rep, kern, obj = sys.argv[1], sys.argv[2], sys.argv[3]
 top = int(sys.argv[4]) if len(sys.argv) > 4 else 30
+skip = sys.argv[5] if len(sys.argv) > 5 else "0"  # matching launches to skip
+kregex, kern = kern.split("::", 1) if "::" in kern else (re.sub(r"ILi\d+E?.*", "", kern), kern)
 
 # ncu: instructions in address order with samples
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass",
-                      "--kernel-name", "regex:" + re.sub(r"ILi\d+E?.*", "", kern),
-                      "--launch-count", "1"], capture_output=True, text=True).stdout
+                      "--kernel-name", "regex:" + kregex,
+                      "--launch-skip", skip, "--launch-count", "1"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 hi = next(i for i, r in enumerate(rows) if r and r[0] == "Address")
 h = rows[hi]
