@@ -22,7 +22,8 @@ from typing import Iterable, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libspmvtk.so")
+# SPMVTK_LIBRARY: another build of the same library (A/B timing in tools/)
+LIB_PATH = os.environ.get("SPMVTK_LIBRARY") or os.path.join(_HERE, "libspmvtk.so")
 
 
 class Status(enum.IntEnum):
