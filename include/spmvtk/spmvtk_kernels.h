@@ -64,6 +64,14 @@ int spmvtk_k_crs_to_ccs(int64_t n, int64_t nnz, const int32_t* irp,
                         const int32_t* icol, const double* val,
                         int32_t* col_ptr, int32_t* row_idx, double* out_val,
                         void* scratch, void* stream);
+/* CRS -> COO-col (convert.cpp:68-70 = Phase I then Phase II, ccs_to_coo_col
+ * :55-66) in one pass: as spmvtk_k_crs_to_ccs, and the sort that places each
+ * entry also writes its column into col_idx (no separate col_ptr expansion).
+ * Same scratch as spmvtk_k_crs_to_ccs. */
+int spmvtk_k_crs_to_coo_col(int64_t n, int64_t nnz, const int32_t* irp,
+                            const int32_t* icol, const double* val,
+                            int32_t* col_ptr, int32_t* row_idx, int32_t* col_idx,
+                            double* out_val, void* scratch, void* stream);
 /* Exclusive scan of n int32 counts into out[0..n] (out[n] = total). */
 size_t spmvtk_k_scan_scratch_bytes(int64_t n);
 int spmvtk_k_exclusive_scan(const int32_t* in, int32_t* out, int64_t n,

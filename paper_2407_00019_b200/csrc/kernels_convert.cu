@@ -613,7 +613,8 @@ __global__ void __launch_bounds__(kBktThreads) k_bkt_sort(
     const int4* rec1, const int4* rec2, const int32_t* runs,
     const int32_t* __restrict__ Toff, int64_t n, int shift,
     int nb, int ns, int32_t* __restrict__ col_ptr, int32_t* __restrict__ row_idx,
-    double* __restrict__ out_val, int32_t* big_queue, int32_t* big_len) {
+    double* __restrict__ out_val, int32_t* big_queue, int32_t* big_len,
+    int32_t* __restrict__ out_col) {  // out_col: COO-col column indices (Phase II), or null
   constexpr int kBktCap = kBktThreads * kBktItems;
   const int4* __restrict__ rec = two_pass(runs) ? rec2 : rec1;
   extern __shared__ unsigned char s_raw[];
@@ -709,6 +710,7 @@ __global__ void __launch_bounds__(kBktThreads) k_bkt_sort(
       const int32_t slot = atomicAdd(&cnt[r.x - c0], 1);
       row_idx[bs + slot] = r.y;
       out_val[bs + slot] = rec_val(r);
+      if (out_col) out_col[bs + slot] = r.x;
     }
     if (threadIdx.x == 0) big_queue[atomicAdd(big_len, 1)] = b;
     return;
@@ -746,6 +748,7 @@ __global__ void __launch_bounds__(kBktThreads) k_bkt_sort(
     for (int32_t j = a; j < e; ++j) rank += s_row[j] < row;
     row_idx[bs + a + rank] = row;
     st_stream(out_val + bs + a + rank, s_val[q]);
+    if (out_col) out_col[bs + a + rank] = static_cast<int32_t>(c0) + col;
   }
   __syncthreads();
   if (!s_long) return;
@@ -757,6 +760,7 @@ __global__ void __launch_bounds__(kBktThreads) k_bkt_sort(
     for (int32_t q = a + threadIdx.x; q < e; q += blockDim.x) {
       row_idx[bs + q] = s_row[q];
       st_stream(out_val + bs + q, s_val[q]);
+      if (out_col) out_col[bs + q] = static_cast<int32_t>(c0) + i;
     }
     __syncthreads();
   }
@@ -1072,9 +1076,10 @@ void launch_staged(int ns, cudaStream_t s, const int32_t* irp, const int32_t* ic
 }
 }  // namespace
 
-int spmvtk_k_crs_to_ccs(int64_t n, int64_t nnz, const int32_t* irp, const int32_t* icol,
-                        const double* val, int32_t* col_ptr, int32_t* row_idx,
-                        double* out_val, void* scratch, void* stream) {
+namespace {
+int crs_to_ccs_impl(int64_t n, int64_t nnz, const int32_t* irp, const int32_t* icol,
+                    const double* val, int32_t* col_ptr, int32_t* row_idx, double* out_val,
+                    int32_t* out_col, void* scratch, void* stream) {
   cudaStream_t s = as_stream(stream);
   if (n <= 0) SPMVTK_LAUNCH_RETURN();
   if (nnz == 0) {
@@ -1166,12 +1171,29 @@ int spmvtk_k_crs_to_ccs(int64_t n, int64_t nnz, const int32_t* irp, const int32_
   }
   if (g_ccs_sort_threads == 256)
     k_bkt_sort<256><<<bp.nb, 256, sort_smem, s>>>(rec, rec2, runs, Toff, n, bp.shift, bp.nb, ns,
-                                                  col_ptr, row_idx, out_val, big, big_len);
+                                                  col_ptr, row_idx, out_val, big, big_len,
+                                                  out_col);
   else
     k_bkt_sort<512><<<bp.nb, 512, sort_smem, s>>>(rec, rec2, runs, Toff, n, bp.shift, bp.nb, ns,
-                                                  col_ptr, row_idx, out_val, big, big_len);
+                                                  col_ptr, row_idx, out_val, big, big_len,
+                                                  out_col);
   k_bkt_sort_big<<<kSMs, 512, 0, s>>>(col_ptr, n, bp.shift, row_idx, out_val, big, big_len);
   SPMVTK_LAUNCH_RETURN();
+}
+}  // namespace
+
+int spmvtk_k_crs_to_ccs(int64_t n, int64_t nnz, const int32_t* irp, const int32_t* icol,
+                        const double* val, int32_t* col_ptr, int32_t* row_idx,
+                        double* out_val, void* scratch, void* stream) {
+  return crs_to_ccs_impl(n, nnz, irp, icol, val, col_ptr, row_idx, out_val, nullptr, scratch,
+                         stream);
+}
+
+int spmvtk_k_crs_to_coo_col(int64_t n, int64_t nnz, const int32_t* irp, const int32_t* icol,
+                            const double* val, int32_t* col_ptr, int32_t* row_idx,
+                            int32_t* col_idx, double* out_val, void* scratch, void* stream) {
+  return crs_to_ccs_impl(n, nnz, irp, icol, val, col_ptr, row_idx, out_val, col_idx, scratch,
+                         stream);
 }
 
 int spmvtk_k_crs_to_ell_cm(int64_t n, int32_t nz, int64_t ld, const int32_t* irp,

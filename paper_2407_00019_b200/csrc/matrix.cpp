@@ -298,17 +298,19 @@ Matrix* convert(const Matrix& a, spmvtk_format to, std::uint64_t max_bytes) {
       DevArray<std::int32_t> colptr(n + 1, "CCS col_ptr");
       DevArray<unsigned char> scratch(spmvtk_k_ccs_scratch_bytes(n, nnz), "CCS scratch");
       cudaStream_t st = rt::stream();
-      rt::check_launch(spmvtk_k_crs_to_ccs(n, nnz, a.ptr.get(), a.col.get(), a.val.get(),
-                                           colptr.get(), m->row.get(), m->val.get(),
-                                           scratch.get(), st),
-                       "CRS->CCS");
       if (coo) {
+        // Phase II folded into Phase I: the sort writes each entry's column
         m->ordering = 1;
         m->col.reset(nnz, "COO col_idx");
-        if (nnz)
-          rt::check_launch(spmvtk_k_expand_ptr(colptr.get(), n, nnz, m->col.get(), st),
-                           "expand columns");
+        rt::check_launch(spmvtk_k_crs_to_coo_col(n, nnz, a.ptr.get(), a.col.get(), a.val.get(),
+                                                 colptr.get(), m->row.get(), m->col.get(),
+                                                 m->val.get(), scratch.get(), st),
+                         "CRS->COO-col");
       } else {
+        rt::check_launch(spmvtk_k_crs_to_ccs(n, nnz, a.ptr.get(), a.col.get(), a.val.get(),
+                                             colptr.get(), m->row.get(), m->val.get(),
+                                             scratch.get(), st),
+                         "CRS->CCS");
         m->ptr = std::move(colptr);
       }
       return m.release();
@@ -446,12 +448,17 @@ double transform_kernel_seconds(const Matrix& a, spmvtk_format to, int repeats) 
         break;
       case SPMVTK_FORMAT_CCS:
       case SPMVTK_FORMAT_COO_COL:
-        rt::check_launch(spmvtk_k_crs_to_ccs(n, nnz, a.ptr.get(), a.col.get(), a.val.get(),
-                                             colptr.get(), out->row.get(), out->val.get(),
-                                             scratch.get(), st),
-                         "CRS->CCS");
         if (to == SPMVTK_FORMAT_COO_COL)
-          rt::check_launch(spmvtk_k_expand_ptr(colptr.get(), n, nnz, out->col.get(), st), "expand");
+          rt::check_launch(spmvtk_k_crs_to_coo_col(n, nnz, a.ptr.get(), a.col.get(),
+                                                   a.val.get(), colptr.get(), out->row.get(),
+                                                   out->col.get(), out->val.get(), scratch.get(),
+                                                   st),
+                           "CRS->COO-col");
+        else
+          rt::check_launch(spmvtk_k_crs_to_ccs(n, nnz, a.ptr.get(), a.col.get(), a.val.get(),
+                                               colptr.get(), out->row.get(), out->val.get(),
+                                               scratch.get(), st),
+                           "CRS->CCS");
         break;
       case SPMVTK_FORMAT_ELL:
         rt::check_launch(spmvtk_k_row_stats(a.ptr.get(), n, acc.get(), st), "row stats");
