@@ -300,8 +300,8 @@ const char* spmvtk_version(void);
 
 /* ---- streaming host SpMV -------------------------------------------------
  * A pipeline for many products with one handle and host vectors: submit
- * enqueues H2D(x) -> SpMV -> D2H(y) on three streams with double-buffered
- * device staging and returns at once, so the copy-in of one product, the
+ * enqueues H2D(x) -> SpMV -> D2H(y) on separate streams with three device
+ * staging slots and returns at once, so the copy-in of one product, the
  * SpMV of another and the copy-out of a third overlap (PCIe is full duplex).
  * x and y must stay untouched until spmvtk_pipeline_wait returns; pinned
  * host memory is needed for the copies to be asynchronous.  Every product

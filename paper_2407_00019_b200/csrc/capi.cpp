@@ -314,16 +314,21 @@ spmvtk_status spmvtk_spmv(const spmvtk_matrix* m, spmvtk_kernel kernel, const do
 // ---- streaming host SpMV (spmvtk_pipeline_*) -------------------------------
 struct spmvtk_pipeline {
   static constexpr int kMaxSplit = 4;
+  static constexpr int kMaxSlots = 4;
   const dev::Matrix* m = nullptr;
+  int slots = 3;  // device staging slots (products in flight): 3 measured 10-12 % faster
+                  // than 2 and 4 at n = 2^20 (profiles/r01_pipeline_slots.txt),
+                  // within 3 % of the PCIe duplex copy time; SPMVTK_PIPE_SLOTS overrides
   spmvtk_kernel kernel = SPMVTK_KERNEL_CRS;
   int split = 2;  // copies per direction cut into `split` parts on their own streams
                   // (2 measured 6 % faster than 1 and 4 at n = 2^20,
                   // profiles/r01_pipeline_split.txt; SPMVTK_PIPE_SPLIT overrides)
   cudaStream_t h2d[kMaxSplit] = {}, d2h[kMaxSplit] = {};
   cudaStream_t comp = nullptr;
-  double* x[2] = {nullptr, nullptr};
-  double* y[2] = {nullptr, nullptr};
-  cudaEvent_t h2d_done[2][kMaxSplit] = {}, comp_done[2] = {}, d2h_done[2][kMaxSplit] = {};
+  double* x[kMaxSlots] = {};
+  double* y[kMaxSlots] = {};
+  cudaEvent_t h2d_done[kMaxSlots][kMaxSplit] = {}, comp_done[kMaxSlots] = {},
+              d2h_done[kMaxSlots][kMaxSplit] = {};
   std::uint64_t count = 0;
   ~spmvtk_pipeline() {
     if (comp) cudaStreamSynchronize(comp);
@@ -331,7 +336,7 @@ struct spmvtk_pipeline {
       if (d2h[k]) cudaStreamSynchronize(d2h[k]);
       if (h2d[k]) cudaStreamSynchronize(h2d[k]);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < kMaxSlots; ++b) {
       if (x[b]) cudaFree(x[b]);
       if (y[b]) cudaFree(y[b]);
       if (comp_done[b]) cudaEventDestroy(comp_done[b]);
@@ -359,13 +364,15 @@ spmvtk_status spmvtk_pipeline_create(const spmvtk_matrix* m, spmvtk_kernel kerne
     p->kernel = kernel;
     if (const char* e = std::getenv("SPMVTK_PIPE_SPLIT"))
       p->split = std::max(1, std::min(spmvtk_pipeline::kMaxSplit, std::atoi(e)));
+    if (const char* e = std::getenv("SPMVTK_PIPE_SLOTS"))
+      p->slots = std::max(2, std::min(spmvtk_pipeline::kMaxSlots, std::atoi(e)));
     rt::check(cudaStreamCreateWithFlags(&p->comp, cudaStreamNonBlocking), "pipeline stream");
     for (int k = 0; k < p->split; ++k) {
       rt::check(cudaStreamCreateWithFlags(&p->h2d[k], cudaStreamNonBlocking), "pipeline stream");
       rt::check(cudaStreamCreateWithFlags(&p->d2h[k], cudaStreamNonBlocking), "pipeline stream");
     }
     const std::size_t nx = std::max<std::int64_t>(m->ncols, 1), ny = std::max<std::int64_t>(m->n, 1);
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < p->slots; ++b) {
       rt::check(cudaMalloc(&p->x[b], nx * sizeof(double)), "pipeline x");
       rt::check(cudaMalloc(&p->y[b], ny * sizeof(double)), "pipeline y");
       rt::check(cudaEventCreateWithFlags(&p->comp_done[b], cudaEventDisableTiming), "event");
@@ -381,7 +388,7 @@ spmvtk_status spmvtk_pipeline_create(const spmvtk_matrix* m, spmvtk_kernel kerne
 spmvtk_status spmvtk_pipeline_submit(spmvtk_pipeline* p, const double* x, double* y) {
   return guarded([&] {
     if (!p || !x || !y) throw Error(ErrorCode::InvalidArgument, "null argument");
-    const int b = static_cast<int>(p->count & 1);
+    const int b = static_cast<int>(p->count % static_cast<std::uint64_t>(p->slots));
     const std::size_t nx = static_cast<std::size_t>(p->m->ncols);
     const std::size_t ny = static_cast<std::size_t>(p->m->n);
     const int K = p->split;

@@ -30,7 +30,20 @@ def t(fn, reps=50):
 
 print("H2D 8MB pinned  ms", t(lambda: xd.copy_(xh, non_blocking=True)))
 print("D2H 8MB pinned  ms", t(lambda: yh.copy_(xd, non_blocking=True)))
-print("both concurrent ms", t(lambda: (xd.copy_(xh, non_blocking=True), yh.copy_(xd, non_blocking=True))))
+print("both, one stream ms", t(lambda: (xd.copy_(xh, non_blocking=True), yh.copy_(xd, non_blocking=True))))
+# full duplex: the copy-in and the copy-out on their own streams
+yd = torch.empty_like(xd)
+s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+
+
+def duplex():
+    with torch.cuda.stream(s_in):
+        xd.copy_(xh, non_blocking=True)
+    with torch.cuda.stream(s_out):
+        yh.copy_(yd, non_blocking=True)
+
+
+print("both, two streams (duplex) ms", t(duplex))
 lib = sp.load_library()
 cudart = C.CDLL("libcudart.so.12") if False else None
 m = sp.HostCrs(2, n).upload()

@@ -1,4 +1,5 @@
-"""Streaming host SpMV: ms per product with SPMVTK_PIPE_SPLIT copy streams per direction."""
+"""Streaming host SpMV: ms per product with SPMVTK_PIPE_SPLIT copy streams per direction
+and SPMVTK_PIPE_SLOTS products in flight (host time of the submits printed too)."""
 import os, sys, time
 sys.path.insert(0, os.getcwd())
 import torch
@@ -11,5 +12,7 @@ for i in range(4): pipe.submit(xs[i % 2].numpy(), ys[i % 2].numpy())
 pipe.wait()
 t0 = time.perf_counter()
 for i in range(200): pipe.submit(xs[i % 2].numpy(), ys[i % 2].numpy())
+t1 = time.perf_counter()
 pipe.wait()
-print(os.environ.get("SPMVTK_PIPE_SPLIT", "1"), "ms/step", (time.perf_counter() - t0) / 200 * 1e3, flush=True)
+print("split", os.environ.get("SPMVTK_PIPE_SPLIT", "2"), "slots", os.environ.get("SPMVTK_PIPE_SLOTS", "3"),
+      "ms/step", (time.perf_counter() - t0) / 200 * 1e3, "submit ms", (t1 - t0) / 200 * 1e3, flush=True)
