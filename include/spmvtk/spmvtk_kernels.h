@@ -27,6 +27,14 @@ extern "C" {
  * acc[0] (validation). */
 int spmvtk_k_row_stats(const int32_t* ptr, int64_t n, unsigned long long* acc,
                        void* stream);
+/* The same reduction published without a copy or a stream synchronisation:
+ * acc = 4 device u64 that start zeroed (the kernel leaves them zeroed), host
+ * = 4 u64 of mapped pinned memory; when the last CTA finishes it writes
+ * {max | bad<<63, sum, sumsq} to host[0..2] and then seq to host[3], so the
+ * caller spins on host[3] == seq.  n must be > 0. */
+int spmvtk_k_row_stats_mapped(const int32_t* ptr, int64_t n, unsigned long long* acc,
+                              unsigned long long* host, unsigned long long seq,
+                              void* stream);
 
 /* dst[i] = (int32)(src[i] - base) ; src int64 (reference layout). */
 int spmvtk_k_narrow_index(const int64_t* src, int32_t* dst, int64_t len,

@@ -36,9 +36,15 @@ __device__ __forceinline__ void stats_add(int32_t a, int32_t b, unsigned long lo
   s2 += c * c;
 }
 
+// acc[0..2] = max | bad<<63, sum, sum of squares.  With `host` (mapped
+// pinned memory) the last CTA to finish also publishes the totals there,
+// then `seq` in host[3], and clears acc[0..3] for the next call: the caller
+// spins on host[3] instead of a memset + copy + stream synchronisation.
 __global__ void __launch_bounds__(kStatsThreads) k_row_stats(const int32_t* __restrict__ ptr,
                                                              int64_t n,
-                                                             unsigned long long* acc) {
+                                                             unsigned long long* acc,
+                                                             volatile unsigned long long* host,
+                                                             unsigned long long seq) {
   __shared__ unsigned long long s_red[3][kStatsThreads / 32];
   __shared__ int s_bad;
   unsigned long long mx = 0, s = 0, s2 = 0;
@@ -89,6 +95,19 @@ __global__ void __launch_bounds__(kStatsThreads) k_row_stats(const int32_t* __re
       atomicMax(acc + 0, mx | (s_bad ? (1ull << 63) : 0ull));
       atomicAdd(acc + 1, s);
       atomicAdd(acc + 2, s2);
+      if (host) {
+        __threadfence();
+        if (atomicAdd(acc + 3, 1ull) == gridDim.x - 1) {  // last CTA: totals are final
+          const unsigned long long t0 = atomicAdd(acc + 0, 0ull), t1 = atomicAdd(acc + 1, 0ull),
+                                   t2 = atomicAdd(acc + 2, 0ull);
+          host[0] = t0;
+          host[1] = t1;
+          host[2] = t2;
+          __threadfence_system();
+          host[3] = seq;
+          acc[0] = acc[1] = acc[2] = acc[3] = 0;
+        }
+      }
     }
   }
 }
@@ -320,7 +339,16 @@ int spmvtk_k_row_stats(const int32_t* ptr, int64_t n, unsigned long long* acc,
   if (cudaMemsetAsync(acc, 0, 3 * sizeof(unsigned long long), s) != cudaSuccess)
     SPMVTK_LAUNCH_RETURN();
   if (n > 0)
-    k_row_stats<<<grid_for((n + 3) / 4, kStatsThreads, 2), kStatsThreads, 0, s>>>(ptr, n, acc);
+    k_row_stats<<<grid_for((n + 3) / 4, kStatsThreads, 2), kStatsThreads, 0, s>>>(ptr, n, acc,
+                                                                                nullptr, 0);
+  SPMVTK_LAUNCH_RETURN();
+}
+
+int spmvtk_k_row_stats_mapped(const int32_t* ptr, int64_t n, unsigned long long* acc,
+                              unsigned long long* host, unsigned long long seq, void* stream) {
+  if (n <= 0) return static_cast<int>(cudaErrorInvalidValue);
+  k_row_stats<<<grid_for((n + 3) / 4, kStatsThreads, 2), kStatsThreads, 0, as_stream(stream)>>>(
+      ptr, n, acc, host, seq);
   SPMVTK_LAUNCH_RETURN();
 }
 

@@ -5,6 +5,8 @@
 #include <cstring>
 
 #include <cmath>
+#include <atomic>
+#include <chrono>
 #include <cstdint>
 #include <mutex>
 
@@ -63,11 +65,13 @@ void free_bytes(void* p) { cudaFreeAsync(p, t_stream); }
 
 namespace {
 // per-thread scratch of the row-statistics round trip: a device accumulator
-// and a pinned host landing slot, allocated once (the conversion timing
+// (zeroed once; the kernel clears it after use) and a mapped pinned landing
+// slot the kernel's last CTA writes, allocated once (the conversion timing
 // t_trans pays this round trip on every CRS -> ELL call)
 struct StatsScratch {
   unsigned long long* dev = nullptr;
   unsigned long long* host = nullptr;
+  unsigned long long seq = 0;
   ~StatsScratch() {
     if (dev) cudaFree(dev);
     if (host) cudaFreeHost(host);
@@ -80,13 +84,38 @@ Moments row_moments(const std::int32_t* ptr, std::int64_t n) {
   init();
   if (!t_stats.dev) {
     check(cudaMalloc(&t_stats.dev, 4 * sizeof(unsigned long long)), "row statistics scratch");
-    check(cudaHostAlloc(&t_stats.host, 4 * sizeof(unsigned long long), cudaHostAllocDefault),
+    check(cudaMemset(t_stats.dev, 0, 4 * sizeof(unsigned long long)), "row statistics scratch");
+    check(cudaHostAlloc(&t_stats.host, 4 * sizeof(unsigned long long), cudaHostAllocMapped),
           "row statistics scratch");
+    std::memset(t_stats.host, 0, 4 * sizeof(unsigned long long));
   }
-  check_launch(spmvtk_k_row_stats(ptr, n, t_stats.dev, t_stream), "row statistics kernel");
-  unsigned long long h[3];
-  copy_to_host(t_stats.host, t_stats.dev, 3 * sizeof(unsigned long long));
-  std::memcpy(h, t_stats.host, sizeof(h));
+  unsigned long long h[3] = {0, 0, 0};
+  if (n > 0) {
+    // the kernel publishes into mapped memory; spin briefly on its sequence
+    // word (no memset, no copy, no stream synchronisation on the fast path),
+    // then fall back to a stream synchronisation, which also surfaces errors
+    const unsigned long long seq = ++t_stats.seq;
+    void* host_dev = nullptr;
+    check(cudaHostGetDevicePointer(&host_dev, t_stats.host, 0), "row statistics scratch");
+    check_launch(spmvtk_k_row_stats_mapped(ptr, n, t_stats.dev,
+                                           static_cast<unsigned long long*>(host_dev), seq,
+                                           t_stream),
+                 "row statistics kernel");
+    volatile unsigned long long* flag = t_stats.host + 3;
+    const auto t0 = std::chrono::steady_clock::now();
+    while (*flag != seq &&
+           std::chrono::steady_clock::now() - t0 < std::chrono::microseconds(200)) {
+    }
+    if (*flag != seq) {
+      sync();
+      if (*flag != seq) throw Error(ErrorCode::Validation, "row statistics did not complete");
+    }
+    std::atomic_thread_fence(std::memory_order_acquire);
+    const volatile unsigned long long* v = t_stats.host;
+    h[0] = v[0];
+    h[1] = v[1];
+    h[2] = v[2];
+  }
   Moments m;
   m.monotone = (h[0] >> 63) == 0;
   m.max = h[0] & ~(1ull << 63);
