@@ -277,6 +277,14 @@ spmvtk_status spmvtk_gen_vector(int64_t n, uint64_t seed, double* out);
 spmvtk_status spmvtk_conversion_bytes(const spmvtk_matrix* m, spmvtk_format to,
                                       uint64_t* reference_estimate, uint64_t* device_bytes);
 
+/* One CRS -> `to` conversion timed as the reference's measure_transformation
+ * (autotune.cpp:122-128): wall clock in the library around the conversion,
+ * the device synchronised before and after, allocation and the max-row
+ * reduction included -- the t_trans of spmvtk_bench for any target format. */
+spmvtk_status spmvtk_matrix_convert_timed(const spmvtk_matrix* m, spmvtk_format to,
+                                          uint64_t max_bytes, spmvtk_matrix** out,
+                                          double* seconds);
+
 /* Median device time (seconds) of the kernels of one CRS -> `to` conversion
  * with outputs preallocated (allocation and host synchronisation excluded;
  * spmvtk_bench's t_trans includes them, as the reference's does). */

@@ -278,6 +278,20 @@ spmvtk_status spmvtk_matrix_convert(const spmvtk_matrix* m, spmvtk_format to,
   });
 }
 
+spmvtk_status spmvtk_matrix_convert_timed(const spmvtk_matrix* m, spmvtk_format to,
+                                          uint64_t max_bytes, spmvtk_matrix** out,
+                                          double* seconds) {
+  return guarded([&] {
+    need(out, "null output");
+    need(seconds, "null output");
+    const dev::Matrix& a = crs_of(m);
+    if (!valid_format(to)) throw Error(ErrorCode::InvalidArgument, "unknown target format");
+    auto [conv, secs] = at::measure_transformation(a, to, max_bytes);
+    *out = conv;
+    *seconds = secs;
+  });
+}
+
 spmvtk_status spmvtk_spmv(const spmvtk_matrix* m, spmvtk_kernel kernel, const double* x,
                           int64_t len, int lanes, double* y, double* elapsed_seconds) {
   return guarded([&] {

@@ -163,6 +163,7 @@ SIGNATURES = {
     "spmvtk_matrix_get_format": (C.c_int, [_P]),
     "spmvtk_matrix_get_info": (C.c_int, [_P, C.POINTER(MatrixInfo)]),
     "spmvtk_matrix_convert": (C.c_int, [_P, C.c_int, _u64, _PP]),
+    "spmvtk_matrix_convert_timed": (C.c_int, [_P, C.c_int, _u64, _PP, _pd]),
     "spmvtk_spmv": (C.c_int, [_P, C.c_int, _P, _i64, C.c_int, _P, _pd]),
     "spmvtk_bench": (C.c_int, [_P, C.c_int, C.c_int, C.c_int, _u64, C.POINTER(BenchResult)]),
     "spmvtk_profile_build": (C.c_int, [C.POINTER(_P), C.POINTER(C.c_char_p), C.c_size_t, C.c_int,
@@ -403,6 +404,14 @@ class Matrix:
     # ---- operations ---------------------------------------------------
     def convert(self, to: Format, max_bytes: int = 0) -> "Matrix":
         return Matrix._make(self._lib.spmvtk_matrix_convert, self._h, int(to), max_bytes)
+
+    def convert_timed(self, to: Format, max_bytes: int = 0) -> tuple["Matrix", float]:
+        """convert() timed inside the library as the reference's
+        measure_transformation: (handle, t_trans seconds)."""
+        out, s = C.c_void_p(), C.c_double()
+        _check(self._lib.spmvtk_matrix_convert_timed(self._h, int(to), max_bytes, C.byref(out),
+                                                     C.byref(s)))
+        return Matrix(out), s.value
 
     def to_crs(self) -> "Matrix":
         """Canonical CRS rebuilt on the device (inverse conversions)."""
