@@ -1,10 +1,13 @@
 """Summarises an ncu --csv launch list (gpu__time_duration, dram bytes) per
-kernel: count, mean time, DRAM bytes per launch, achieved DRAM GB/s."""
+kernel: count, mean time, DRAM bytes per launch, achieved DRAM GB/s.
+With --by-grid, launches are keyed by (kernel, grid size), which separates
+the same kernel on different matrices (configs)."""
 import csv
 import sys
 from collections import OrderedDict
 
-rows = list(csv.reader(open(sys.argv[1])))
+by_grid = "--by-grid" in sys.argv
+rows = list(csv.reader(open([a for a in sys.argv[1:] if not a.startswith("--")][0])))
 hi = [i for i, r in enumerate(rows) if r and r[0] == "ID"][0]
 h = rows[hi]
 ix = {k: i for i, k in enumerate(h)}
@@ -12,7 +15,10 @@ launch = OrderedDict()
 for r in rows[hi + 1:]:
     if len(r) < len(h):
         continue
-    key = (r[ix["ID"]], r[ix["Kernel Name"]].split("(")[0].replace("<unnamed>::", "")[:48])
+    name = r[ix["Kernel Name"]].split("(")[0].replace("<unnamed>::", "")
+    if by_grid and "Grid Size" in ix:
+        name = name[:38] + " " + r[ix["Grid Size"]].replace('"', "")
+    key = (r[ix["ID"]], name[:48])
     d = launch.setdefault(key, {})
     v = float(r[ix["Metric Value"]].replace(",", ""))
     unit = r[ix["Metric Unit"]]
