@@ -680,3 +680,68 @@ def test_inverse_conversions_on_device(gpu, golden):
         coo.to_crs()
     assert e.value.status == sp.Status.ERR_DATA and "duplicate (row, col) pair (1, 2)" in \
         e.value.message
+
+
+def test_lower_abi_phase1_phase2_and_statistics(gpu, port):
+    """The lower C ABI (spmvtk_kernels.h) called directly on device buffers:
+    spmvtk_k_crs_to_coo_col (Phase I with Phase II fused), spmvtk_k_expand_ptr
+    (Phase II alone, on the col_ptr of spmvtk_k_crs_to_ccs) and
+    spmvtk_k_row_stats_mapped (max/sum/sumsq published into mapped memory,
+    accumulator left zeroed for the next call) -- against the C port."""
+    import ctypes as C
+
+    import torch
+    sp = gpu
+    lib = sp.load_library()
+    P, I64, U64 = C.c_void_p, C.c_int64, C.c_uint64
+    lib.spmvtk_k_ccs_scratch_bytes.restype = C.c_size_t
+    lib.spmvtk_k_ccs_scratch_bytes.argtypes = [I64, I64]
+    lib.spmvtk_k_crs_to_ccs.argtypes = [I64, I64, P, P, P, P, P, P, P, P]
+    lib.spmvtk_k_crs_to_coo_col.argtypes = [I64, I64, P, P, P, P, P, P, P, P, P]
+    lib.spmvtk_k_expand_ptr.argtypes = [P, I64, I64, P, P]
+    lib.spmvtk_k_row_stats_mapped.argtypes = [P, I64, P, P, U64, P]
+    rng = np.random.default_rng(5)
+    n = 40_000
+    lens = rng.integers(0, 30, size=n)
+    rows = [np.sort(rng.choice(n, size=int(ln), replace=False)) for ln in lens]
+    ci = np.concatenate(rows)
+    rp = np.concatenate([[0], np.cumsum(lens)])
+    v = rng.standard_normal(ci.shape[0])
+    nnz = int(rp[-1])
+    dev = lambda a, dt: torch.as_tensor(np.asarray(a, dt), device="cuda")  # noqa: E731
+    irp, icol, val = dev(rp, np.int32), dev(ci, np.int32), dev(v, np.float64)
+    stream = torch.cuda.current_stream().cuda_stream
+    scratch = torch.empty(lib.spmvtk_k_ccs_scratch_bytes(n, nnz), dtype=torch.uint8, device="cuda")
+    cp = torch.empty(n + 1, dtype=torch.int32, device="cuda")
+    ri = torch.empty(nnz, dtype=torch.int32, device="cuda")
+    cc = torch.empty(nnz, dtype=torch.int32, device="cuda")
+    cv = torch.empty(nnz, dtype=torch.float64, device="cuda")
+    assert lib.spmvtk_k_crs_to_coo_col(n, nnz, irp.data_ptr(), icol.data_ptr(), val.data_ptr(),
+                                       cp.data_ptr(), ri.data_ptr(), cc.data_ptr(),
+                                       cv.data_ptr(), scratch.data_ptr(), stream) == 0
+    want_r, want_c, want_v = port.crs_to_coo_col(n, rp + 1, ci + 1, v)
+    np.testing.assert_array_equal(ri.cpu().numpy() + 1, want_r)
+    np.testing.assert_array_equal(cc.cpu().numpy() + 1, want_c)
+    assert cv.cpu().numpy().tobytes() == want_v.tobytes()
+    # Phase I alone, then Phase II from its col_ptr
+    ri2 = torch.empty_like(ri)
+    cv2 = torch.empty_like(cv)
+    assert lib.spmvtk_k_crs_to_ccs(n, nnz, irp.data_ptr(), icol.data_ptr(), val.data_ptr(),
+                                   cp.data_ptr(), ri2.data_ptr(), cv2.data_ptr(),
+                                   scratch.data_ptr(), stream) == 0
+    cc2 = torch.empty_like(cc)
+    assert lib.spmvtk_k_expand_ptr(cp.data_ptr(), n, nnz, cc2.data_ptr(), stream) == 0
+    assert torch.equal(ri2, ri) and torch.equal(cc2, cc) and torch.equal(cv2, cv)
+    # row statistics through mapped memory, twice (the accumulator resets)
+    acc = torch.zeros(4, dtype=torch.int64, device="cuda")
+    host = torch.zeros(4, dtype=torch.int64).pin_memory()
+    for seq in (1, 2):
+        assert lib.spmvtk_k_row_stats_mapped(irp.data_ptr(), n, acc.data_ptr(), host.data_ptr(),
+                                             seq, stream) == 0
+        torch.cuda.synchronize()
+        h = host.numpy()
+        assert int(h[3]) == seq
+        assert int(h[0]) == int(lens.max())
+        assert int(h[1]) == int(lens.sum())
+        assert int(h[2]) == int((lens.astype(np.int64) ** 2).sum())
+        assert int(acc.abs().sum().item()) == 0
