@@ -559,50 +559,55 @@ __global__ void __launch_bounds__(kRefineThreads) k_bkt_refine(
     const int4* __restrict__ rec, int64_t nnz, int shift, int fshift,
     const int32_t* __restrict__ Toff, int ns, int32_t* __restrict__ fcur,
     int4* __restrict__ rec2, const int32_t* runs) {
+  // persistent CTAs walk the chunks, so in single-pass mode the launch
+  // costs a few hundred CTAs that exit at once, not one per chunk
   if (!two_pass(runs)) return;
   __shared__ int32_t s_cnt[kRefineWin];
-  const int64_t q0 = static_cast<int64_t>(blockIdx.x) * kRefineItems;
-  const int32_t len = static_cast<int32_t>(min(static_cast<int64_t>(kRefineItems), nnz - q0));
-  int4 r[kRefinePer];
-#pragma unroll
-  for (int k = 0; k < kRefinePer; ++k) {
-    const int32_t q = static_cast<int32_t>(threadIdx.x) + k * kRefineThreads;
-    if (q < len) r[k] = ld_stream4(rec + q0 + q);
-  }
-  const int32_t b_lo = ((__ldg(&rec[q0].x) >> shift) >> fshift) << fshift;
-  const int32_t b_hi = (((__ldg(&rec[q0 + len - 1].x) >> shift) >> fshift) + 1) << fshift;
-  const int32_t win = b_hi - b_lo;
-  if (win > kRefineWin) {  // many tiny coarse buckets: global cursors
+  for (int64_t q0 = static_cast<int64_t>(blockIdx.x) * kRefineItems; q0 < nnz;
+       q0 += static_cast<int64_t>(gridDim.x) * kRefineItems) {
+    const int32_t len = static_cast<int32_t>(min(static_cast<int64_t>(kRefineItems), nnz - q0));
+    int4 r[kRefinePer];
 #pragma unroll
     for (int k = 0; k < kRefinePer; ++k) {
       const int32_t q = static_cast<int32_t>(threadIdx.x) + k * kRefineThreads;
-      if (q < len) {
-        const int32_t b = r[k].x >> shift;
-        rec2[Toff[static_cast<int64_t>(b) * ns] + atomicAdd(&fcur[b], 1)] = r[k];
+      if (q < len) r[k] = ld_stream4(rec + q0 + q);
+    }
+    const int32_t b_lo = ((__ldg(&rec[q0].x) >> shift) >> fshift) << fshift;
+    const int32_t b_hi = (((__ldg(&rec[q0 + len - 1].x) >> shift) >> fshift) + 1) << fshift;
+    const int32_t win = b_hi - b_lo;
+    if (win > kRefineWin) {  // many tiny coarse buckets: global cursors
+#pragma unroll
+      for (int k = 0; k < kRefinePer; ++k) {
+        const int32_t q = static_cast<int32_t>(threadIdx.x) + k * kRefineThreads;
+        if (q < len) {
+          const int32_t b = r[k].x >> shift;
+          rec2[Toff[static_cast<int64_t>(b) * ns] + atomicAdd(&fcur[b], 1)] = r[k];
+        }
+      }
+      continue;  // win is CTA-uniform: every thread takes this branch
+    }
+    for (int i = threadIdx.x; i < win; i += blockDim.x) s_cnt[i] = 0;
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kRefinePer; ++k) {
+      const int32_t q = static_cast<int32_t>(threadIdx.x) + k * kRefineThreads;
+      if (q < len) atomicAdd(&s_cnt[(r[k].x >> shift) - b_lo], 1);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < win; i += blockDim.x) {
+      const int32_t c = s_cnt[i];
+      if (c) {
+        const int64_t b = b_lo + i;
+        s_cnt[i] = Toff[b * ns] + atomicAdd(&fcur[b], c);
       }
     }
-    return;
-  }
-  for (int i = threadIdx.x; i < win; i += blockDim.x) s_cnt[i] = 0;
-  __syncthreads();
+    __syncthreads();
 #pragma unroll
-  for (int k = 0; k < kRefinePer; ++k) {
-    const int32_t q = static_cast<int32_t>(threadIdx.x) + k * kRefineThreads;
-    if (q < len) atomicAdd(&s_cnt[(r[k].x >> shift) - b_lo], 1);
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < win; i += blockDim.x) {
-    const int32_t c = s_cnt[i];
-    if (c) {
-      const int64_t b = b_lo + i;
-      s_cnt[i] = Toff[b * ns] + atomicAdd(&fcur[b], c);
+    for (int k = 0; k < kRefinePer; ++k) {
+      const int32_t q = static_cast<int32_t>(threadIdx.x) + k * kRefineThreads;
+      if (q < len) rec2[atomicAdd(&s_cnt[(r[k].x >> shift) - b_lo], 1)] = r[k];
     }
-  }
-  __syncthreads();
-#pragma unroll
-  for (int k = 0; k < kRefinePer; ++k) {
-    const int32_t q = static_cast<int32_t>(threadIdx.x) + k * kRefineThreads;
-    if (q < len) rec2[atomicAdd(&s_cnt[(r[k].x >> shift) - b_lo], 1)] = r[k];
+    __syncthreads();  // s_cnt is reused by the next chunk
   }
 }
 
@@ -1153,7 +1158,8 @@ int crs_to_ccs_impl(int64_t n, int64_t nnz, const int32_t* irp, const int32_t* i
     else
       k_bkt_scatter<<<ns, nt, static_cast<size_t>(bp.nc) * 4, s>>>(
           irp, icol, val, slice_row, bp.shift + bp.fshift, bp.nc, Tcoff, rec, runs, true);
-    k_bkt_refine<<<static_cast<unsigned>((nnz + kRefineItems - 1) / kRefineItems),
+    k_bkt_refine<<<static_cast<unsigned>(std::min<int64_t>(
+                       (nnz + kRefineItems - 1) / kRefineItems, int64_t(kSMs) * 2)),
                    kRefineThreads, 0, s>>>(rec, nnz, bp.shift, bp.fshift, Toff, ns, fcur, rec2,
                                            runs);
     // single pass: per slice, staged over its bucket window or cursor
