@@ -1,6 +1,7 @@
 """BASELINE.json workloads on the GPU (tests against the C oracle).
 
-* configs 1-3 at FULL size: every transform bit-exact, every SpMV within
+* configs 1-3 at FULL size: every transform bit-exact (COO-col included,
+  and its inverse conversion back to the input CRS), every SpMV within
   1e-12 max-norm relative, D_mat as measured in SURVEY.md §0.15;
 * config 4 (power-law, n = 2^22): statistics, the ELL memory guard refusal
   (≈160 GB in GPU layout), CRS/COO parity;
@@ -47,6 +48,18 @@ def check_all(sp, port, h, n, rp, ci, v, x, ell=True):
     del cp, ri, cv
     cc = m.convert(sp.Format.COO_COL)
     assert max_rel_error(cc.spmv(x, sp.Kernel.COO_COL_OUTER)[0], want) <= TOL
+    # COO-col arrays (Phase II fused into the CCS sort) bit-exact, and the
+    # inverse conversion back to the (sorted) input CRS on the device
+    kr, kc, kv = port.crs_to_coo_col(n, rp, ci, v)
+    assert np.array_equal(cc.array(sp.Array.ROW_IDX), kr)
+    assert np.array_equal(cc.array(sp.Array.COL_IDX), kc)
+    assert cc.array(sp.Array.VALUES).tobytes() == kv.tobytes()
+    del kr, kc, kv
+    back = cc.to_crs()
+    assert np.array_equal(back.array(sp.Array.POINTER), rp)
+    assert np.array_equal(back.array(sp.Array.COL_IDX), ci)
+    assert back.array(sp.Array.VALUES).tobytes() == v.tobytes()
+    back.free()
     cc.free()
     if ell:
         bc, ev, ec, cnt = port.crs_to_ell(n, rp, ci, v)
