@@ -147,3 +147,21 @@ def test_config_5_full_size_properties(gpu, d):
     e.free()
     c = m.convert(sp.Format.COO_COL)
     assert max_rel_error(c.spmv(x, sp.Kernel.COO_COL_OUTER)[0], y0) <= TOL
+    c.free()
+    # CCS at full size (single pass; D = 0 takes the windowed staged scatter):
+    # col_ptr = column counts, rows ascending inside every column, and the
+    # transpose back reproduces the input CRS bit for bit
+    ccs = m.convert(sp.Format.CCS)
+    ci = m.array(sp.Array.COL_IDX, 8, 0)
+    cp = ccs.array(sp.Array.POINTER, 8, 0)
+    assert np.array_equal(np.diff(cp), np.bincount(ci, minlength=n))
+    ri = ccs.array(sp.Array.ROW_IDX, 8, 0)
+    col_of = np.repeat(np.arange(n), np.diff(cp))
+    assert not np.any((np.diff(ri) <= 0) & (col_of[1:] == col_of[:-1]))
+    del ri, col_of
+    back = ccs.to_crs()
+    assert np.array_equal(back.array(sp.Array.POINTER, 8, 0), rp)
+    assert np.array_equal(back.array(sp.Array.COL_IDX, 8, 0), ci)
+    assert back.array(sp.Array.VALUES).tobytes() == m.array(sp.Array.VALUES).tobytes()
+    back.free()
+    ccs.free()
