@@ -142,7 +142,8 @@ __device__ void block_bitonic(KeyPtr key, ValPtr val, int32_t len) {
 // (~4k entries per bucket).  The CRS is split into kSlices row ranges of
 // equal entry counts (one per SM).
 //   1. k_bkt_count   slice-local bucket histograms in shared memory ->
-//                    T[b * kSlices + slice]
+//                    T[b * kSlices + slice]; also the number of non-empty
+//                    runs (two-pass choice) and each slice's bucket window
 //   2. exclusive scan of T (bucket-major) -> each (bucket, slice) owns a run
 //   3. k_bkt_scatter each slice re-reads its rows and appends 16-byte
 //                    records (col, row, value) to its runs with shared-memory
@@ -152,10 +153,11 @@ __device__ void block_bitonic(KeyPtr key, ValPtr val, int32_t len) {
 //                    when columns scatter over many runs, or per slice over a
 //                    banded matrix's bucket window, k_bkt_scatter_single)
 //   4. k_bkt_sort    one CTA per bucket: counting sort by column in shared
-//                    memory, per-column sort by row (rows are distinct within
-//                    a column, so this restores the reference's order,
-//                    convert.cpp:43-51), col_ptr and the final row_idx /
-//                    values written fully coalesced.
+//                    memory, then each entry goes to its rank by row inside
+//                    its column (rows are distinct within a column, so this
+//                    restores the reference's order, convert.cpp:43-51);
+//                    col_ptr, row_idx, values (and for COO-col the column,
+//                    Phase II fused) written from there.
 // Buckets too large for shared memory take a global-memory path.
 constexpr int kSlices = 3 * 148;  // max slices (3 CTAs per SM, 64 KB histograms)
 int g_ccs_slices = 148;           // tuning: slices actually used (one per SM)
