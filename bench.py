@@ -302,11 +302,13 @@ def impl_reference(args):
     value = b / dt / 1e9
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "n_gpus": args.gpus, "steps": args.steps, "steps_requested": args.steps_requested,
+        "warmup": args.warmup,
         "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"baseline config {args.config}", "n": n, "nnz": nnz,
-                   "best_format": best},
+                   "best_format": best,
+                   "bounded_sample": "steps capped at ~60 s of CPU work"},
         "cpu_baseline": {"value": value, "unit": "GB/s", "cores": lanes, "kind": "reference",
                          "sample": f"{args.steps} SpMVs ({best}, {lanes} lanes) of the full "
                                    f"config-{args.config} matrix; oracle/_ref = reference "
