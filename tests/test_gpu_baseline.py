@@ -4,7 +4,7 @@
   and its inverse conversion back to the input CRS), every SpMV within
   1e-12 max-norm relative, D_mat as measured in SURVEY.md §0.15;
 * config 4 (power-law, n = 2^22): statistics, the ELL memory guard refusal
-  (≈160 GB in GPU layout), CRS/COO parity;
+  (≈160 GB in GPU layout), CRS/COO parity, the CCS bit-exact at full size;
 * config 5 (D_mat sweep) at reduced n for oracle parity, and at full size
   for D in {0, 1, 2}: size-independent properties (ELL and COO SpMV equal
   CRS SpMV to 1e-12, band count = max row length, exported row counts = row
@@ -116,6 +116,19 @@ def test_config_4_power_law(gpu, port):
     assert max_rel_error(m.spmv(x, sp.Kernel.CRS)[0], want) <= TOL
     coo = m.convert(sp.Format.COO_ROW)
     assert max_rel_error(coo.spmv(x, sp.Kernel.COO_ROW_OUTER)[0], want) <= TOL
+    coo.free()
+    # CCS at full size through the two-pass partition (coarse staged scatter,
+    # persistent refine, sort), bit-exact against the port; COO-col SpMV
+    cp, ri, cv = port.crs_to_ccs(n, rp, ci, v)
+    ccs = m.convert(sp.Format.CCS)
+    assert np.array_equal(ccs.array(sp.Array.POINTER), cp)
+    assert np.array_equal(ccs.array(sp.Array.ROW_IDX), ri)
+    assert ccs.array(sp.Array.VALUES).tobytes() == cv.tobytes()
+    ccs.free()
+    del cp, ri, cv
+    cc = m.convert(sp.Format.COO_COL)
+    assert max_rel_error(cc.spmv(x, sp.Kernel.COO_COL_OUTER)[0], want) <= TOL
+    cc.free()
 
 
 @pytest.mark.parametrize("d", [0.0, 0.3, 1.0, 2.0])
