@@ -1,8 +1,8 @@
 // convert.hpp -- C++ transform entry points (drop-in for
 // /root/reference/proj/include/spmvtk/convert.hpp:9-33).  The forward
 // transforms run on the GPU (upload, sm_100a kernels, download); results are
-// bit-identical to the reference.  coo_to_crs / ell_to_crs rebuild canonical
-// CRS on the host (device versions are "next").
+// bit-identical to the reference.  coo_to_crs / ell_to_crs / canonicalize
+// rebuild canonical CRS on the device too (kernels_inverse.cu).
 #pragma once
 
 #include <cstdint>

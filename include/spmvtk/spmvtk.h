@@ -291,8 +291,10 @@ spmvtk_status spmvtk_matrix_convert_timed(const spmvtk_matrix* m, spmvtk_format 
 spmvtk_status spmvtk_transform_kernel_seconds(const spmvtk_matrix* m, spmvtk_format to,
                                               int repeats, double* seconds);
 
-/* Grows the device memory pool by `bytes` once (allocate + free), so later
- * stream-ordered allocations of handles are sub-allocations. */
+/* Grows the device memory pool by `bytes` once (allocate + free) and keeps
+ * up to that many bytes cached after frees (the pool's release threshold;
+ * default 2 GiB), so later stream-ordered allocations of handles are
+ * sub-allocations. */
 spmvtk_status spmvtk_reserve_device_memory(uint64_t bytes);
 
 /* Compute metrics / amortization / D* helpers (autotune.cpp:36-60, :130-158). */

@@ -134,6 +134,24 @@ int spmvtk_k_spmv_crs(int64_t n, const int32_t* irp, const int32_t* icol,
                       const double* val, const double* x, double* y,
                       double mean_row, int32_t max_row, int32_t* long_rows,
                       void* stream);
+/* ---- entry-balanced ("segmented") CRS SpMV (kernels_spmv_seg.cu)
+ * A plan assigns warp w the rows whose first entry lies in [w*chunk,
+ * (w+1)*chunk): plan[w] = first row r with irp[r] >= w*chunk, plan[nwarps]
+ * = n (nwarps + 1 int32 entries; chunk <= 0 = SPMVTK_SEG_CHUNK). */
+#define SPMVTK_SEG_CHUNK 2048
+int32_t spmvtk_k_seg_plan_warps(int64_t nnz, int32_t chunk);
+/* The chunk the library's plans use (SPMVTK_SEG_CHUNK unless tuned). */
+int32_t spmvtk_k_seg_chunk(void);
+int spmvtk_k_seg_plan(int64_t n, int64_t nnz, const int32_t* irp, int32_t chunk,
+                      int32_t* plan, void* stream);
+/* y[r] for the rows of warps [w_base, w_end) clipped to [row_lo, row_hi);
+ * every row of that range is written. */
+int spmvtk_k_spmv_crs_seg(const int32_t* irp, const int32_t* icol, const double* val,
+                          const double* x, double* y, const int32_t* plan,
+                          int32_t w_base, int32_t w_end, int64_t row_lo, int64_t row_hi,
+                          void* stream);
+/* The CRS kernel choice: 1 = segmented (plan needed), 0 = sub-warp per row. */
+int spmvtk_k_crs_use_seg(double mean_row, int64_t max_row);
 /* Row length above which spmvtk_k_spmv_crs hands a row to the block-per-row
  * pass (long_rows must then be non-NULL when max_row exceeds it). */
 int64_t spmvtk_k_crs_long_limit(double mean_row);
@@ -176,6 +194,10 @@ int spmvtk_k_spmv_crs_push(int64_t n, const int32_t* irp, const int32_t* icol,
                            const struct spmvtk_push* push,
                            const struct spmvtk_push_sync* sync, double mean_row,
                            int32_t max_row, int32_t* long_rows, void* stream);
+int spmvtk_k_spmv_crs_seg_push(const int32_t* irp, const int32_t* icol, const double* val,
+                               const double* x, const struct spmvtk_push* push,
+                               const struct spmvtk_push_sync* sync, const int32_t* plan,
+                               int32_t nwarps, int64_t n, void* stream);
 int spmvtk_k_spmv_ell_cm_push(int64_t n, int32_t nz, int64_t ld, const double* val,
                               const int32_t* col, const double* x,
                               const struct spmvtk_push* push,

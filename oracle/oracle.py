@@ -168,6 +168,20 @@ class Port:
         return y
 
     # ---- autotune arithmetic -------------------------------------------------
+    def gen_baseline(self, config: int, param: int, dparam: float = 0.0, seed: int = 2407):
+        """A BASELINE workload as a reference CRS handle (the product's
+        generator compiled into this library: no product .so is loaded)."""
+        h = C.c_void_p()
+        if self.lib.ref_gen_baseline(config, param, float(dparam), seed, C.byref(h)):
+            raise RuntimeError(self.err())
+        return h
+
+    def gen_vector(self, n: int, seed: int) -> np.ndarray:
+        out = np.empty(n, np.float64)
+        if self.lib.ref_gen_vector(n, seed, _p(out)):
+            raise RuntimeError(self.err())
+        return out
+
     def partition_range(self, length, lanes):
         s, e = np.empty(max(lanes, 1), np.int64), np.empty(max(lanes, 1), np.int64)
         if self.lib.or_partition_range(length, lanes, _p(s), _p(e)):
@@ -217,6 +231,8 @@ class Ref:
         L.ref_amortization.argtypes = [C.c_double] * 3
         L.ref_amortization.restype = C.c_int64
         L.ref_partition_range.argtypes = [_i64, C.c_int, _P, _P]
+        L.ref_gen_baseline.argtypes = [C.c_int, _i64, C.c_double, C.c_uint64, C.POINTER(_P)]
+        L.ref_gen_vector.argtypes = [_i64, C.c_uint64, _P]
         L.spmvtk_matrix_free.argtypes = [_P]
         L.spmvtk_matrix_convert.argtypes = [_P, C.c_int, C.c_uint64, C.POINTER(_P)]
         L.spmvtk_spmv.argtypes = [_P, C.c_int, _P, _i64, C.c_int, _P, _pd]
@@ -319,6 +335,20 @@ class Ref:
     def amortization(self, t_crs, t_ell, t_trans):
         k = self.lib.ref_amortization(t_crs, t_ell, t_trans)
         return None if k == -1 else k
+
+    def gen_baseline(self, config: int, param: int, dparam: float = 0.0, seed: int = 2407):
+        """A BASELINE workload as a reference CRS handle (the product's
+        generator compiled into this library: no product .so is loaded)."""
+        h = C.c_void_p()
+        if self.lib.ref_gen_baseline(config, param, float(dparam), seed, C.byref(h)):
+            raise RuntimeError(self.err())
+        return h
+
+    def gen_vector(self, n: int, seed: int) -> np.ndarray:
+        out = np.empty(n, np.float64)
+        if self.lib.ref_gen_vector(n, seed, _p(out)):
+            raise RuntimeError(self.err())
+        return out
 
     def partition_range(self, length, lanes):
         s, e = np.empty(max(lanes, 1), np.int64), np.empty(max(lanes, 1), np.int64)

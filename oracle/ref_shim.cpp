@@ -24,6 +24,7 @@
 #include "spmvtk/spmv.hpp"
 #include "spmvtk/spmvtk.h"
 #include "spmvtk/stats.hpp"
+#include "../paper_2407_00019_b200/csrc/generators.hpp"
 
 using namespace spmvtk;  // -> spmvtk_ref
 
@@ -228,6 +229,32 @@ int64_t ref_amortization(double t_crs, double t_ell, double t_trans) {
     out = k ? *k : -1;
   });
   return out;
+}
+
+// A BASELINE workload (gen::baseline, int32 0-based) as a reference CRS
+// handle (int64 1-based), for bench.py's reference arm.
+int ref_gen_baseline(int config, int64_t param, double dparam, uint64_t seed,
+                     spmvtk_matrix** out) {
+  return guard([&] {
+    gen::HostCrs h = gen::baseline(config, param, dparam, seed);
+    CrsMatrix m;
+    m.n = h.n;
+    m.row_ptr.resize(static_cast<std::size_t>(h.n) + 1);
+    m.col_idx.resize(h.values.size());
+    if (h.wide()) {
+      for (std::size_t i = 0; i < m.row_ptr.size(); ++i) m.row_ptr[i] = h.row_ptr[i] - h.base + 1;
+      for (std::size_t p = 0; p < m.col_idx.size(); ++p) m.col_idx[p] = h.col_idx[p] - h.base + 1;
+    } else {
+      for (std::size_t i = 0; i < m.row_ptr.size(); ++i) m.row_ptr[i] = h.row_ptr32[i] - h.base + 1;
+      for (std::size_t p = 0; p < m.col_idx.size(); ++p) m.col_idx[p] = h.col32[p] - h.base + 1;
+    }
+    m.values = std::move(h.values);
+    *out = new spmvtk_matrix{std::move(m)};
+  });
+}
+
+int ref_gen_vector(int64_t n, uint64_t seed, double* out) {
+  return guard([&] { gen::vector_u11(n, seed, out); });
 }
 
 int ref_partition_range(int64_t len, int lanes, int64_t* istart, int64_t* iend) {

@@ -82,9 +82,12 @@ void fill_ones(double* d, std::int64_t n) {
 
 double measure_spmv(const dev::Matrix& m, spmvtk_kernel k, int repeats) {
   if (repeats < 1) throw Error(ErrorCode::InvalidArgument, "repeats must be at least 1");
-  rt::DevArray<double> x(static_cast<std::size_t>(std::max<std::int64_t>(m.n, 1)), "x");
+  // x spans the columns (a row-block shard reads global columns in
+  // [0, ncols)), y the rows
+  const std::int64_t nx = std::max<std::int64_t>(std::max(m.ncols, m.n), 1);
+  rt::DevArray<double> x(static_cast<std::size_t>(nx), "x");
   rt::DevArray<double> y(static_cast<std::size_t>(std::max<std::int64_t>(m.n, 1)), "y");
-  fill_ones(x.get(), m.n);
+  fill_ones(x.get(), nx);
   dev::spmv_device(m, k, x.get(), y.get());  // warm-up, untimed
   rt::sync();
   std::vector<double> samples;

@@ -192,8 +192,10 @@ const char* spmvtk_last_error(void) { return t_error.c_str(); }
 
 void spmvtk_matrix_free(spmvtk_matrix* m) {
   if (!m) return;
-  // buffers may still be in use by work queued on any stream of this thread
-  cudaDeviceSynchronize();
+  // stream-ordered: the buffers go back to the pool once the work already
+  // queued on the calling thread's stream has finished with them (no device
+  // synchronisation).  Work the caller queued on OTHER streams must be
+  // complete first, as with any freed buffer.
   delete m;
 }
 
@@ -827,6 +829,7 @@ spmvtk_status spmvtk_flags_wait(const uint64_t* flags, int32_t n, uint64_t value
 
 spmvtk_status spmvtk_reserve_device_memory(uint64_t bytes) {
   return guarded([&] {
+    rt::set_pool_keep(bytes);
     rt::DevArray<unsigned char> block(static_cast<std::size_t>(bytes), "pool reservation");
     block.release();
     rt::sync();

@@ -51,53 +51,6 @@ __device__ __forceinline__ int4 ld_stream4(const int4* p) {
                : "l"(p));
   return v;
 }
-// L2 eviction-priority policies (createpolicy): the matrix streams through
-// once per SpMV (evict_first) while x is re-gathered nnz times (evict_last),
-// so x stays L2-resident even when the matrix is several times the L2.
-__device__ __forceinline__ uint64_t policy_evict_first() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ uint64_t policy_evict_last() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ double ld_stream_hint(const double* p, uint64_t pol) {
-  double v;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
-               : "=d"(v)
-               : "l"(p), "l"(pol));
-  return v;
-}
-__device__ __forceinline__ int ld_stream_hint(const int* p, uint64_t pol) {
-  int v;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;"
-               : "=r"(v)
-               : "l"(p), "l"(pol));
-  return v;
-}
-__device__ __forceinline__ double2 ld_stream2_hint(const double2* p, uint64_t pol) {
-  double2 v;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
-               : "=d"(v.x), "=d"(v.y)
-               : "l"(p), "l"(pol));
-  return v;
-}
-__device__ __forceinline__ int2 ld_stream2_hint(const int2* p, uint64_t pol) {
-  int2 v;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.s32 {%0, %1}, [%2], %3;"
-               : "=r"(v.x), "=r"(v.y)
-               : "l"(p), "l"(pol));
-  return v;
-}
-__device__ __forceinline__ double ld_x_hint(const double* p, uint64_t pol) {
-  double v;
-  asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
-  return v;
-}
-
 // x gathers: keep them cacheable (x is small and reused)
 __device__ __forceinline__ double ld_x(const double* p) { return __ldg(p); }
 
@@ -222,5 +175,6 @@ __device__ __forceinline__ void resolve_segments(SegWindow& w, const int32_t* pt
 void preload_convert();
 void preload_util();
 void preload_inverse();
+void preload_seg();
 
 }  // namespace spmvtk_dev

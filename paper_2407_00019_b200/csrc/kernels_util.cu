@@ -38,7 +38,7 @@ __device__ __forceinline__ void stats_add(int32_t a, int32_t b, unsigned long lo
 
 // acc[0..2] = max | bad<<63, sum, sum of squares.  With `host` (mapped
 // pinned memory) the last CTA to finish also publishes the totals there,
-// then `seq` in host[3], and clears acc[0..3] for the next call: the caller
+// clears acc[0..3] for the next call, then publishes `seq` in host[3]: the caller
 // spins on host[3] instead of a memset + copy + stream synchronisation.
 __global__ void __launch_bounds__(kStatsThreads) k_row_stats(const int32_t* __restrict__ ptr,
                                                              int64_t n,
@@ -100,12 +100,16 @@ __global__ void __launch_bounds__(kStatsThreads) k_row_stats(const int32_t* __re
         if (atomicAdd(acc + 3, 1ull) == gridDim.x - 1) {  // last CTA: totals are final
           const unsigned long long t0 = atomicAdd(acc + 0, 0ull), t1 = atomicAdd(acc + 1, 0ull),
                                    t2 = atomicAdd(acc + 2, 0ull);
+          // clear the accumulators BEFORE publishing seq: the caller may
+          // launch the next reduction (on another stream) as soon as it
+          // sees seq, and its atomics must not race with this reset
+          acc[0] = acc[1] = acc[2] = acc[3] = 0;
+          __threadfence();
           host[0] = t0;
           host[1] = t1;
           host[2] = t2;
           __threadfence_system();
           host[3] = seq;
-          acc[0] = acc[1] = acc[2] = acc[3] = 0;
         }
       }
     }

@@ -111,6 +111,65 @@ rt::Moments crs_moments(const Matrix& m) {
   return *m.moments;
 }
 
+const std::vector<std::int32_t>& crs_seg_plan(const Matrix& m, const std::int32_t** dev) {
+  std::lock_guard<std::mutex> lk(m.mu);
+  const std::int32_t chunk = spmvtk_k_seg_chunk();
+  if (m.seg_plan_host.empty() || m.seg_plan_chunk != chunk) {
+    const std::int32_t nw = spmvtk_k_seg_plan_warps(m.nnz, chunk);
+    DevArray<std::int32_t> plan(static_cast<std::size_t>(nw) + 1, "SpMV plan");
+    rt::check_launch(spmvtk_k_seg_plan(m.n, m.nnz, m.ptr.get(), chunk, plan.get(),
+                                       rt::stream()),
+                     "SpMV plan");
+    std::vector<std::int32_t> host(static_cast<std::size_t>(nw) + 1);
+    rt::copy_to_host(host.data(), plan.get(), host.size() * sizeof(std::int32_t));  // synchronises
+    m.seg_plan = std::move(plan);
+    m.seg_plan_host = std::move(host);
+    m.seg_plan_chunk = chunk;
+  }
+  *dev = m.seg_plan.get();
+  return m.seg_plan_host;
+}
+
+namespace {
+// warps whose rows intersect [r0, r1): plan[w] < r1 and plan[w+1] > r0
+std::pair<std::int32_t, std::int32_t> plan_warps_for(const std::vector<std::int32_t>& plan,
+                                                     std::int64_t r0, std::int64_t r1) {
+  const std::int32_t nw = static_cast<std::int32_t>(plan.size()) - 1;
+  // first w with plan[w+1] > r0
+  const auto lo = std::upper_bound(plan.begin() + 1, plan.end(), static_cast<std::int32_t>(r0));
+  const std::int32_t w0 = static_cast<std::int32_t>(lo - (plan.begin() + 1));
+  // first w with plan[w] >= r1
+  const auto hi = std::lower_bound(plan.begin(), plan.begin() + nw, static_cast<std::int32_t>(r1));
+  const std::int32_t w1 = static_cast<std::int32_t>(hi - plan.begin());
+  return {w0, std::max(w0, w1)};
+}
+
+void spmv_crs_rows(const Matrix& m, const double* x, double* y, std::int64_t r0, std::int64_t r1,
+                   cudaStream_t st) {
+  rt::Moments mo = crs_moments(m);
+  const double mean = m.n > 0 ? static_cast<double>(mo.sum) / static_cast<double>(m.n) : 0;
+  if (spmvtk_k_crs_use_seg(mean, static_cast<std::int64_t>(mo.max))) {
+    const std::int32_t* plan = nullptr;
+    const auto& hp = crs_seg_plan(m, &plan);
+    auto [w0, w1] = plan_warps_for(hp, r0, r1);
+    rt::check_launch(spmvtk_k_spmv_crs_seg(m.ptr.get(), m.col.get(), m.val.get(), x, y, plan, w0,
+                                           w1, r0, r1, st),
+                     "spmv crs");
+    return;
+  }
+  const std::int64_t rows = r1 - r0;
+  DevArray<std::int32_t> long_rows;
+  if (static_cast<std::int64_t>(mo.max) > spmvtk_k_crs_long_limit(mean))
+    long_rows.reset(rows + 1, "CRS long-row queue");
+  // row pointers stay absolute, so offsetting irp and y is enough
+  rt::check_launch(spmvtk_k_spmv_crs(rows, m.ptr.get() + r0, m.col.get(), m.val.get(), x, y + r0,
+                                     mean,
+                                     static_cast<std::int32_t>(std::min<std::uint64_t>(mo.max, INT32_MAX)),
+                                     long_rows.get(), st),
+                   "spmv crs");
+}
+}  // namespace
+
 Matrix* crs_from_arrays(std::int64_t n, std::int64_t nnz, const void* row_ptr,
                         const void* col_idx, const double* values, int index_width,
                         int index_base, bool on_device) {
@@ -504,20 +563,9 @@ void spmv_device_rows(const Matrix& m, spmvtk_kernel kernel, const double* x, do
   if (rows == 0) return;
   cudaStream_t st = rt::stream();
   switch (kernel) {
-    case SPMVTK_KERNEL_CRS: {
-      rt::Moments mo = crs_moments(m);
-      const double mean = m.n > 0 ? static_cast<double>(mo.sum) / static_cast<double>(m.n) : 0;
-      DevArray<std::int32_t> long_rows;
-      if (static_cast<std::int64_t>(mo.max) > spmvtk_k_crs_long_limit(mean))
-        long_rows.reset(rows + 1, "CRS long-row queue");
-      // row pointers stay absolute, so offsetting irp and y is enough
-      rt::check_launch(spmvtk_k_spmv_crs(rows, m.ptr.get() + r0, m.col.get(), m.val.get(), x,
-                                         y + r0, mean,
-                                         static_cast<std::int32_t>(std::min<std::uint64_t>(mo.max, INT32_MAX)),
-                                         long_rows.get(), st),
-                       "spmv crs");
+    case SPMVTK_KERNEL_CRS:
+      spmv_crs_rows(m, x, y, r0, r1, st);
       return;
-    }
     case SPMVTK_KERNEL_ELL_INNER:
       rt::check_launch(spmvtk_k_spmv_ell_cm(rows, m.band_count, m.ld, m.val.get() + r0,
                                             m.col.get() + r0, x, y + r0, st),
@@ -539,15 +587,7 @@ void spmv_device(const Matrix& m, spmvtk_kernel kernel, const double* x, double*
     case SPMVTK_KERNEL_CRS: {
       if (m.format != SPMVTK_FORMAT_CRS)
         throw Error(ErrorCode::InvalidArgument, "operation requires a CRS handle");
-      rt::Moments mo = crs_moments(m);
-      const double mean = m.n > 0 ? static_cast<double>(mo.sum) / static_cast<double>(m.n) : 0;
-      DevArray<std::int32_t> long_rows;
-      if (static_cast<std::int64_t>(mo.max) > spmvtk_k_crs_long_limit(mean))
-        long_rows.reset(m.n + 1, "CRS long-row queue");
-      rt::check_launch(spmvtk_k_spmv_crs(m.n, m.ptr.get(), m.col.get(), m.val.get(), x, y, mean,
-                                         static_cast<std::int32_t>(std::min<std::uint64_t>(mo.max, INT32_MAX)),
-                                         long_rows.get(), st),
-                       "spmv crs");
+      if (m.n > 0) spmv_crs_rows(m, x, y, 0, m.n, st);
       return;
     }
     case SPMVTK_KERNEL_COO_ROW_OUTER:
@@ -619,6 +659,15 @@ void spmv_device_push(const Matrix& m, spmvtk_kernel kernel, const double* x,
       throw Error(ErrorCode::InvalidArgument, "operation requires a CRS handle");
     rt::Moments mo = crs_moments(m);
     const double mean = m.n > 0 ? static_cast<double>(mo.sum) / static_cast<double>(m.n) : 0;
+    if (m.n > 0 && spmvtk_k_crs_use_seg(mean, static_cast<std::int64_t>(mo.max))) {
+      const std::int32_t* plan = nullptr;
+      const auto& hp = crs_seg_plan(m, &plan);
+      rt::check_launch(spmvtk_k_spmv_crs_seg_push(m.ptr.get(), m.col.get(), m.val.get(), x, &push,
+                                                  sync, plan,
+                                                  static_cast<std::int32_t>(hp.size()) - 1, m.n, st),
+                       "spmv crs (push)");
+      return;
+    }
     DevArray<std::int32_t> long_rows;
     if (static_cast<std::int64_t>(mo.max) > spmvtk_k_crs_long_limit(mean))
       long_rows.reset(m.n + 1, "CRS long-row queue");

@@ -12,6 +12,7 @@
 #include <cstdint>
 #include <mutex>
 #include <optional>
+#include <vector>
 
 #include "runtime.hpp"
 #include "spmvtk/spmvtk.h"
@@ -36,6 +37,11 @@ struct spmvtk_matrix {
 
   mutable std::mutex mu;
   mutable std::optional<spmvtk::rt::Moments> moments;  // CRS row moments
+  // CRS: entry-balanced SpMV plan (warp -> first row), built at the first
+  // segmented SpMV; host copy for row-range launches
+  mutable spmvtk::rt::DevArray<std::int32_t> seg_plan;
+  mutable std::vector<std::int32_t> seg_plan_host;
+  mutable std::int32_t seg_plan_chunk = 0;
 
   std::uint64_t device_bytes() const {
     return val.bytes() + ptr.bytes() + row.bytes() + col.bytes() + count.bytes();
@@ -48,6 +54,8 @@ using Matrix = spmvtk_matrix;
 
 // Exact row moments of a CRS handle (cached after the first GPU reduction).
 rt::Moments crs_moments(const Matrix& m);
+// The segmented-SpMV plan of a CRS handle (cached; nwarps + 1 entries).
+const std::vector<std::int32_t>& crs_seg_plan(const Matrix& m, const std::int32_t** dev);
 
 // CRS from caller arrays; see spmvtk_matrix_from_crs.
 Matrix* crs_from_arrays(std::int64_t n, std::int64_t nnz, const void* row_ptr,

@@ -4,6 +4,7 @@
 #include <cstdlib>
 #include <cstring>
 
+#include <algorithm>
 #include <cmath>
 #include <atomic>
 #include <chrono>
@@ -38,13 +39,28 @@ void init() {
     check(cudaGetDevice(&dev), "cudaGetDevice");
     cudaMemPool_t pool;
     check(cudaDeviceGetDefaultMemPool(&pool, dev), "cudaDeviceGetDefaultMemPool");
-    uint64_t threshold = UINT64_MAX;
+    // keep up to kPoolKeepDefault bytes cached between conversions (so a
+    // timed conversion of a mid-sized matrix sub-allocates instead of paying
+    // cudaMalloc); anything above is returned to the driver at the next
+    // synchronisation.  spmvtk_reserve_device_memory() raises the figure.
+    uint64_t threshold = kPoolKeepDefault;
     check(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold),
           "cudaMemPoolSetAttribute");
     check(static_cast<cudaError_t>(spmvtk_k_preload()), "kernel preload");
     // test hook: force a CRS kernel variant for a whole process
     if (const char* v = std::getenv("SPMVTK_CRS_VARIANT")) spmvtk_k_tune("crs_variant", std::atoi(v));
   });
+}
+
+void set_pool_keep(std::uint64_t bytes) {
+  init();
+  int dev = 0;
+  check(cudaGetDevice(&dev), "cudaGetDevice");
+  cudaMemPool_t pool;
+  check(cudaDeviceGetDefaultMemPool(&pool, dev), "cudaDeviceGetDefaultMemPool");
+  uint64_t threshold = std::max<std::uint64_t>(bytes, kPoolKeepDefault);
+  check(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold),
+        "cudaMemPoolSetAttribute");
 }
 
 void* alloc_bytes(std::size_t bytes, const char* what) {

@@ -29,6 +29,11 @@ void set_stream(cudaStream_t s);
 // module preload so no timed call pays lazy kernel loading.
 void init();
 
+// Bytes the stream-ordered pool keeps cached after frees (the release
+// threshold); set_pool_keep() raises it (spmvtk_reserve_device_memory).
+inline constexpr std::uint64_t kPoolKeepDefault = 2ull << 30;
+void set_pool_keep(std::uint64_t bytes);
+
 void* alloc_bytes(std::size_t bytes, const char* what);
 void free_bytes(void* p);
 

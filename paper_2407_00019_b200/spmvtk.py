@@ -421,7 +421,14 @@ class Matrix:
              out: np.ndarray | None = None) -> tuple[np.ndarray, float]:
         xs = np.ascontiguousarray(x, dtype=np.float64)
         # y has one entry per row (== len(x) except for row-block shards)
-        y = out if out is not None else np.empty(self.describe().n, dtype=np.float64)
+        nrows = self.describe().n
+        if out is not None:
+            if not (isinstance(out, np.ndarray) and out.dtype == np.float64
+                    and out.flags.c_contiguous and out.shape == (nrows,)):
+                raise ValueError(f"out must be a contiguous float64 array of {nrows} rows")
+            y = out
+        else:
+            y = np.empty(nrows, dtype=np.float64)
         el = C.c_double()
         _check(self._lib.spmvtk_spmv(self._h, int(kernel), _ptr(xs), xs.shape[0], lanes,
                                      _ptr(y), C.byref(el)))
@@ -464,11 +471,18 @@ class Pipeline:
         h = C.c_void_p()
         _check(self._lib.spmvtk_pipeline_create(m.handle, int(kernel), C.byref(h)))
         self._h = h.value
+        self._m = m  # the C pipeline borrows the handle: keep it alive
+        d = m.describe()
+        self._ncols, self._nrows = d.ncols, d.n
         self._keep = []
 
     def submit(self, x: np.ndarray, y: np.ndarray) -> None:
-        assert x.dtype == np.float64 and y.dtype == np.float64
-        assert x.flags.c_contiguous and y.flags.c_contiguous
+        # the C side takes bare pointers (no lengths): a short buffer would
+        # be read / written past its end by the asynchronous copies
+        for a, want, name in ((x, self._ncols, "x"), (y, self._nrows, "y")):
+            if not (isinstance(a, np.ndarray) and a.dtype == np.float64
+                    and a.flags.c_contiguous and a.shape == (want,)):
+                raise ValueError(f"{name} must be a contiguous float64 array of length {want}")
         self._keep.append((x, y))
         _check(self._lib.spmvtk_pipeline_submit(self._h, x.ctypes.data, y.ctypes.data))
 

@@ -22,7 +22,11 @@ ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--only", default="")
 ap.add_argument("--transforms", action="store_true")
 ap.add_argument("--formats", default="", help="comma list of formats to convert to")
+ap.add_argument("--tune", default="", help="comma list of key=value tuning knobs")
 a = ap.parse_args()
+for kv in filter(None, a.tune.split(",")):
+    k, v = kv.split("=")
+    assert sp.load_library().spmvtk_k_tune(k.encode(), int(v)) == 0, kv
 param = a.param or {1: 256, 2: 1 << 20, 3: 128, 4: 1 << 22, 5: 1 << 21}[a.config]
 only = set(a.only.split(",")) if a.only else None
 sp.set_stream(torch.cuda.current_stream().cuda_stream)
