@@ -1,20 +1,29 @@
 """Benchmark of the hot path on BASELINE.json's workload.
 
 Metric (BASELINE.json): "SpMV GB/s & GFLOP/s per format; CRS->ELL/COO
-transform time in CRS-SpMV units".  Workload: config 2 (random rows, n=2^20,
-row lengths U{8..24}, columns uniform in [0,n), values N(0,1), seeded
-synthetic data -- the paper's SuiteSparse set is not available).
+transform time in CRS-SpMV units".  Workload (default): BASELINE config 4,
+the largest configuration that fits one GPU -- power-law rows (n = 2^22,
+log-normal row lengths with mean 16 and sigma_log 1.2 capped at 4096,
+uniform distinct sorted columns, N(0,1) values), seeded synthetic data (the
+paper's SuiteSparse set is not available).  Its ELL is refused by the
+reference's memory guard (~206 GB), so CRS and COO decide.  Configs 2 and 3
+are measured in the same run under `also`.
 
 A step = one SpMV y = A x in the best format for the matrix (every format is
 measured; the per-format table, the transform times in CRS-SpMV units and
 the AT decision are reported beside the headline).  `value` = algorithmic
-bytes of one SpMV (GPU layout, DESIGN.md §4) x steps / device time, inputs
-resident in HBM (the matrix, 222 MB, is larger than the 126 MB L2, so no
+bytes of one SpMV (GPU layout, DESIGN.md §3) x steps / device time, inputs
+resident in HBM (the matrix, 0.89 GB, is larger than the 126 MB L2, so no
 flush is needed between steps).  `e2e` = the same metric through the C ABI
 with pinned HOST x / y, every step's copy-in and copy-out inside the timed
 region: the streaming spmvtk_pipeline_* calls (products overlap each
 other's copies), and under e2e.sync the reference's synchronous
 spmvtk_spmv().
+
+`--impl reference` runs the reference's own CPU implementation
+(oracle/_ref/libspmvtk_ref.so, compiled from its sources) on the same
+matrix -- generated inside that library, so the product library is never
+loaded -- with the same `config` dict.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 """
@@ -41,15 +50,16 @@ FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback
 
 
 def ncu_traffic(config: int, kernel: str):
-    """DRAM read+write bytes per launch of `kernel` on this config, from the
-    committed ncu launch list (profiles/traffic_*.json), or None."""
+    """(DRAM read+write bytes per launch of `kernel` on this config, source
+    file) from the committed ncu captures (profiles/traffic_r*.json, newest
+    round first), or None."""
     import glob
     for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "traffic_r*.json")), reverse=True):
         try:
             with open(path) as f:
                 v = json.load(f).get(f"config{config}", {}).get(kernel)
             if v:
-                return float(v)
+                return float(v), os.path.relpath(path, ROOT)
         except Exception:
             continue
     return None
@@ -66,6 +76,8 @@ def hbm_peak():
 # the reference's ELL memory guard as its own bench uses it (SURVEY.md 8d:
 # config 4's ELL, ~206 GB in the GPU layout, is refused, not attempted)
 ELL_GUARD_BYTES = 48 << 30
+DEFAULT_CONFIG = 4  # the largest BASELINE configuration that fits one GPU
+DEFAULT_PARAM = {1: 256, 2: 1 << 20, 3: 128, 4: 1 << 22, 5: 1 << 21}
 
 
 def spmv_bytes(fmt: str, n: int, nnz: int, nz: int = 0) -> int:
@@ -230,30 +242,66 @@ def cpu_model() -> str:
     return "unknown"
 
 
-def cpu_reference_run(host, n, nnz, nz, per_call_repeats=3):
+WORKLOADS = {
+    1: "2-D 5-point Laplacian 256x256",
+    2: "random rows U{8..24}, uniform distinct sorted columns",
+    3: "27-point stencil 128^3 (non-periodic)",
+    4: "power-law rows (log-normal, mean 16, sigma_log 1.2, cap 4096), uniform columns",
+    5: "D_mat sweep (Gamma row lengths, mean 32, columns within +-n/64)",
+}
+
+
+def workload_config(cfg: int, param: int, dparam: float, seed: int, n: int, nnz: int,
+                    max_row: int, d_mat: float) -> dict:
+    """The `config` dict: identical in both arms (the driver compares them)."""
+    crs_bytes = spmv_bytes("crs", n, nnz)
+    return {"workload": f"BASELINE config {cfg}: {WORKLOADS[cfg]}", "param": param,
+            "dparam": dparam, "seed": seed, "n": n, "nnz": nnz, "max_row": max_row,
+            "d_mat": round(d_mat, 4),
+            "l2": ("inputs larger than L2 (no flush)" if crs_bytes > (126 << 20)
+                   else "L2-resident matrix (no flush)")}
+
+
+def ell_splits(n: int, nz: int) -> int:
+    """Band chunks the GPU ell-outer kernel uses (matrix.cpp ell_splits): the
+    band split only pays when row pairs alone cannot fill 148 SMs x 2048."""
+    want, pairs = 148 * 2048, (n + 1) // 2
+    if nz <= 1 or pairs >= want:
+        return 1
+    return min(-(-want // pairs), nz)
+
+
+REF_KERNELS = {"crs": 0, "coo-row": 1, "ell-inner": 3, "ell-outer": 4}
+
+
+def cpu_reference_run(ref, h, n, nnz, nz, per_call_repeats=3):
     """The reference's own CPU path (oracle/_ref, compiled from the reference
-    sources) on this host's cores, on the same matrix."""
-    from oracle.oracle import Ref
-    ref = Ref()
+    sources) on this host's cores: its measure_spmv / measure_transformation
+    protocol (autotune.cpp:95-128) for every format its memory guard admits."""
     cores = os.cpu_count() or 1
-    rp, ci, v = host.arrays(index_base=1)
-    h = ref.matrix(n, rp, ci, v)
-    del rp, ci, v
-    res = {}
-    # transforms: one cold conversion each (autotune.cpp:122-128, :197-214)
-    t_ell, ell = ref.measure_transformation(h, 4, 0)
-    t_coo, coo = ref.measure_transformation(h, 2, 0)
+    res, transforms, handles = {}, {}, {"crs": h}
+    # transforms: one cold conversion each (autotune.cpp:122-128, :197-214);
+    # the ELL guard as the reference's own bench applies it (SURVEY.md §8d)
+    for name, fmt, cap in (("ell", 4, ELL_GUARD_BYTES), ("coo-row", 2, 0)):
+        try:
+            t, out = ref.measure_transformation(h, fmt, cap)
+            transforms[name] = {"ms": t * 1e3}
+            handles[name] = out
+        except RuntimeError as e:
+            transforms[name] = {"refused": str(e)[:160]}
     # SpMV: warm-up + median of repeats (autotune.cpp:95-120); CRS is
     # sequential in the reference (autotune.cpp:186), the others use lanes
     t_crs = ref.measure_spmv(h, 0, 1, per_call_repeats)
     res["crs"] = (t_crs, 1)
-    res["ell-inner"] = (ref.measure_spmv(ell, 3, cores, per_call_repeats), cores)
-    res["ell-outer"] = (ref.measure_spmv(ell, 4, cores, per_call_repeats), cores)
-    res["coo-row"] = (ref.measure_spmv(coo, 1, cores, per_call_repeats), cores)
-    # the lane-parallel kernels also at one lane (SURVEY.md §8d)
-    one = {"ell-inner@1": ref.measure_spmv(ell, 3, 1, per_call_repeats),
-           "ell-outer@1": ref.measure_spmv(ell, 4, 1, per_call_repeats),
-           "coo-row@1": ref.measure_spmv(coo, 1, 1, per_call_repeats)}
+    one = {}
+    if "coo-row" in handles:
+        res["coo-row"] = (ref.measure_spmv(handles["coo-row"], 1, cores, per_call_repeats), cores)
+        one["coo-row@1"] = ref.measure_spmv(handles["coo-row"], 1, 1, per_call_repeats)
+    if "ell" in handles:
+        res["ell-inner"] = (ref.measure_spmv(handles["ell"], 3, cores, per_call_repeats), cores)
+        res["ell-outer"] = (ref.measure_spmv(handles["ell"], 4, cores, per_call_repeats), cores)
+        one["ell-inner@1"] = ref.measure_spmv(handles["ell"], 3, 1, per_call_repeats)
+        one["ell-outer@1"] = ref.measure_spmv(handles["ell"], 4, 1, per_call_repeats)
     table = {}
     for k, (t, lanes) in res.items():
         b = spmv_bytes(k, n, nnz, nz)
@@ -262,40 +310,47 @@ def cpu_reference_run(host, n, nnz, nz, per_call_repeats=3):
     for k, t in one.items():
         b = spmv_bytes(k.split("@")[0], n, nnz, nz)
         table[k] = {"gbs": b / t / 1e9, "gflops": 2 * nnz / t / 1e9, "ms": t * 1e3, "lanes": 1}
-    out = {"table": table, "best": best, "cores": cores, "cpu_model": cpu_model(),
-           "transforms": {"ell": {"ms": t_ell * 1e3, "tt": t_ell / t_crs},
-                          "coo-row": {"ms": t_coo * 1e3, "tt": t_coo / t_crs}},
-           "handles": (ref, h, ell, coo)}
-    return out
+    for tr in transforms.values():
+        if "ms" in tr:
+            tr["tt"] = tr["ms"] * 1e-3 / t_crs
+    return {"table": table, "best": best, "cores": cores, "cpu_model": cpu_model(),
+            "transforms": transforms, "handles": handles}
+
+
+def ref_handle_stats(ref, h):
+    """n, nnz, max row and D_mat of a reference CRS handle (reference code)."""
+    meta = ref.meta(h)
+    rp = ref.array(h, 1)
+    nz = int(np.max(np.diff(rp))) if meta["n"] else 0
+    _, _, d_mat = ref.row_stats(h)
+    return meta["n"], meta["nnz"], nz, d_mat
 
 
 def impl_reference(args):
     rank, world, _ = dist_env()
     if world > 1 and rank != 0:
         return 0
-    from paper_2407_00019_b200 import spmvtk as sp
-    # host-side generation only: this arm never touches the GPU
-    host = sp.HostCrs(args.config, args.param, 0.0, args.seed)
-    n, nnz = host.n, host.nnz
-    rp, _, _ = host.arrays(index_base=0)
-    nz = int(np.max(np.diff(rp))) if n else 0
-    del rp
-    r = cpu_reference_run(host, n, nnz, nz)
-    ref, h, ell, coo = r.pop("handles")
+    # the reference library alone: the matrix is generated inside it (the
+    # product's generator compiled into oracle/_ref), never by the product
+    from oracle.oracle import Ref
+    ref = Ref()
+    h = ref.gen_baseline(args.config, args.param, 0.0, args.seed)
+    n, nnz, nz, d_mat = ref_handle_stats(ref, h)
+    r = cpu_reference_run(ref, h, n, nnz, nz)
+    handles = r.pop("handles")
     best = r["best"]
-    kern = {"crs": 0, "coo-row": 1, "ell-inner": 3, "ell-outer": 4}[best]
-    handle = {"crs": h, "coo-row": coo, "ell-inner": ell, "ell-outer": ell}[best]
+    handle = handles["crs" if best == "crs" else "coo-row" if best == "coo-row" else "ell"]
     lanes = r["table"][best]["lanes"]
-    x = np.ones(n)
+    x = ref.gen_vector(n, args.seed + 1)
     tw = time.perf_counter()
     for _ in range(args.warmup):
-        ref.spmv(handle, kern, x, lanes)
+        ref.spmv(handle, REF_KERNELS[best], x, lanes)
     t_one = (time.perf_counter() - tw) / max(1, args.warmup)
     # bounded sample: at most ~60 s of CPU work whatever K is
     steps = int(max(3, min(args.steps, 60.0 / max(t_one, 1e-9))))
     t0 = time.perf_counter()
     for _ in range(steps):
-        ref.spmv(handle, kern, x, lanes)
+        ref.spmv(handle, REF_KERNELS[best], x, lanes)
     dt = (time.perf_counter() - t0) / steps
     args.steps_requested, args.steps = args.steps, steps
     b = spmv_bytes(best, n, nnz, nz)
@@ -306,9 +361,9 @@ def impl_reference(args):
         "warmup": args.warmup,
         "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"baseline config {args.config}", "n": n, "nnz": nnz,
-                   "best_format": best,
-                   "bounded_sample": "steps capped at ~60 s of CPU work"},
+        "config": workload_config(args.config, args.param, 0.0, args.seed, n, nnz, nz, d_mat),
+        "format": best,
+        "bounded_sample": "steps capped at ~60 s of CPU work",
         "cpu_baseline": {"value": value, "unit": "GB/s", "cores": lanes, "kind": "reference",
                          "sample": f"{args.steps} SpMVs ({best}, {lanes} lanes) of the full "
                                    f"config-{args.config} matrix; oracle/_ref = reference "
@@ -322,6 +377,91 @@ def impl_reference(args):
 
 
 # --------------------------------------------------------------------------
+SPMV_KINDS = (("crs", "crs", "CRS"), ("coo-row", "coo-row", "COO_ROW_OUTER"),
+              ("coo-col", "coo-col", "COO_COL_OUTER"), ("ell-inner", "ell", "ELL_INNER"),
+              ("ell-outer", "ell", "ELL_OUTER"), ("ell-row", "ell-row", "ELL_ROWMAJOR"))
+TRANSFORMS = (("coo-row", "COO_ROW"), ("ccs", "CCS"), ("coo-col", "COO_COL"), ("ell", "ELL"),
+              ("ell-row", "ELL_ROWMAJOR"))
+
+
+def measure_matrix(sp, torch, m, seed, peak, reps, warmup, with_transforms=True):
+    """Every transform of one CRS handle (t_trans through the API, kernel-only
+    time) and every SpMV format (device time, CUDA events on the launching
+    stream, `reps` back-to-back launches).  Returns (table, transforms,
+    handles, kernels)."""
+    d = m.describe()
+    n, nnz = d.n, d.nnz
+    nz = m.row_stats().max_row
+    handles, transforms = {"crs": m}, {}
+    for name, fmt_name in TRANSFORMS:
+        fmt = getattr(sp.Format, fmt_name)
+        guard = ELL_GUARD_BYTES if name.startswith("ell") else 0
+        try:
+            if with_transforms:
+                # t_trans = one conversion timed as the reference's
+                # measure_transformation (autotune.cpp:122-128): wall clock
+                # inside the library around the conversion with the device
+                # synchronised on both sides, allocation (from the
+                # stream-ordered pool, grown once up front) and the band-count
+                # reduction's host round trip included; median of 3 such
+                # conversions (nothing of a conversion is cached on the handle)
+                samples = []
+                for rep in range(3):
+                    h, t_one = m.convert_timed(fmt, max_bytes=guard)
+                    samples.append(t_one)
+                    if rep < 2:
+                        h.free()
+                t_trans = sorted(samples)[1]
+                k = m.transform_kernel_seconds(fmt, 5)
+                transforms[name] = {"t_trans_ms": t_trans * 1e3, "kernel_ms": k * 1e3,
+                                    "gbs_kernel": transform_bytes(name, n, nnz, nz) / k / 1e9,
+                                    "bytes": transform_bytes(name, n, nnz, nz)}
+            else:
+                h = m.convert(fmt, max_bytes=guard)
+        except sp.SpmvtkError as e:  # the reference's guard (config 4's ELL)
+            if e.status != sp.Status.ERR_MEMORY_LIMIT:
+                raise
+            transforms[name] = {"refused": e.message}
+            continue
+        handles[name] = h
+    x = torch.from_numpy(sp.gen_vector(n, seed + 1)).cuda()
+    y = torch.empty(n, dtype=torch.float64, device="cuda")
+    kernels = {name: (handles[h], getattr(sp.Kernel, k)) for name, h, k in SPMV_KINDS
+               if h in handles}
+    table = {}
+    for name, (h, k) in kernels.items():
+        for _ in range(max(3, warmup)):
+            h.spmv_device(k, x.data_ptr(), y.data_ptr())
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        ev0.record()
+        for _ in range(reps):
+            h.spmv_device(k, x.data_ptr(), y.data_ptr())
+        ev1.record()
+        torch.cuda.synchronize()
+        t = ev0.elapsed_time(ev1) * 1e-3 / reps
+        b = spmv_bytes(name, n, nnz, nz)
+        table[name] = {"gbs": b / t / 1e9, "gflops": 2 * nnz / t / 1e9, "us": t * 1e6,
+                       "bytes": b, "frac": b / t / 1e9 / peak}
+    if "ell-outer" in table:
+        sps = ell_splits(n, nz)
+        table["ell-outer"]["band_chunks"] = sps
+        if sps == 1:
+            table["ell-outer"]["note"] = ("one band chunk at this n: the same kernel as "
+                                          "ell-inner (not a separate candidate)")
+    t_crs = table["crs"]["us"] * 1e-6
+    for tr in transforms.values():
+        if "t_trans_ms" in tr:
+            tr["tt"] = tr["t_trans_ms"] * 1e-3 / t_crs       # in CRS-SpMV units
+            tr["tt_kernel"] = tr["kernel_ms"] * 1e-3 / t_crs
+    return table, transforms, handles, kernels, x, y
+
+
+def best_format(table):
+    cands = {k: v for k, v in table.items() if v.get("band_chunks", 2) != 1}
+    return max(cands, key=lambda k: cands[k]["gbs"])
+
+
 def impl_ours(args):
     import torch
 
@@ -335,6 +475,7 @@ def impl_ours(args):
     torch.cuda.set_device(0)
     stream = torch.cuda.current_stream()
     sp.set_stream(stream.cuda_stream)
+    lib = sp.load_library()
     peak, peak_kind = hbm_peak()
 
     host = sp.HostCrs(args.config, args.param, 0.0, args.seed)
@@ -344,110 +485,50 @@ def impl_ours(args):
     st = m.row_stats()
     nz = st.max_row
 
-    # ---- transforms.  t_trans = one conversion timed as the reference's
-    # measure_transformation (autotune.cpp:122-128): wall clock inside the
-    # library around the conversion with the device synchronised on both
-    # sides (spmvtk_matrix_convert_timed), allocation -- from the
-    # stream-ordered pool, grown once up front -- and the band-count
-    # reduction's host round trip included (median of 3 conversions); kernel =
-    # median device time of the transform's kernels alone with outputs
-    # preallocated.
     sp.reserve_device_memory(8 << 30)
     # process warm-up (first-call costs of the ctypes bindings and the
     # conversion paths) on a small unrelated matrix, never on the one timed
     warm = sp.HostCrs(1, 256, 0.0, args.seed).upload()
-    for fmt in (sp.Format.COO_ROW, sp.Format.CCS, sp.Format.COO_COL, sp.Format.ELL,
-                sp.Format.ELL_ROWMAJOR):
-        warm.convert(fmt).free()
+    for _, fmt_name in TRANSFORMS:
+        warm.convert(getattr(sp.Format, fmt_name)).free()
     warm.free()
     torch.cuda.synchronize()
-    handles = {"crs": m}
-    transforms = {}
-    for name, fmt in (("coo-row", sp.Format.COO_ROW), ("ccs", sp.Format.CCS),
-                      ("coo-col", sp.Format.COO_COL), ("ell", sp.Format.ELL),
-                      ("ell-row", sp.Format.ELL_ROWMAJOR)):
-        torch.cuda.synchronize()
-        try:
-            # median of 3 such conversions (each recomputes everything:
-            # nothing of a conversion is cached on the handle), for a stable
-            # single-conversion time
-            samples = []
-            for rep in range(3):
-                h, t_one = m.convert_timed(
-                    fmt, max_bytes=ELL_GUARD_BYTES if name.startswith("ell") else 0)
-                samples.append(t_one)
-                if rep < 2:
-                    h.free()
-            t_trans = sorted(samples)[1]
-        except sp.SpmvtkError as e:  # the reference's guard (config 4's ELL)
-            if e.status != sp.Status.ERR_MEMORY_LIMIT:
-                raise
-            transforms[name] = {"refused": e.message}
-            continue
-        k = m.transform_kernel_seconds(fmt, 5)
-        transforms[name] = {"t_trans_ms": t_trans * 1e3, "kernel_ms": k * 1e3,
-                            "gbs_kernel": transform_bytes(name, n, nnz, nz) / k / 1e9,
-                            "bytes": transform_bytes(name, n, nnz, nz)}
-        handles[name] = h
-
-    x = torch.from_numpy(sp.gen_vector(n, args.seed + 1)).cuda()
-    y = torch.empty(n, dtype=torch.float64, device="cuda")
-    kernels = {name: (handles[h], k) for name, h, k in (
-        ("crs", "crs", sp.Kernel.CRS), ("coo-row", "coo-row", sp.Kernel.COO_ROW_OUTER),
-        ("coo-col", "coo-col", sp.Kernel.COO_COL_OUTER), ("ell-inner", "ell", sp.Kernel.ELL_INNER),
-        ("ell-outer", "ell", sp.Kernel.ELL_OUTER), ("ell-row", "ell-row", sp.Kernel.ELL_ROWMAJOR))
-        if h in handles}
-
-    def run(name, count):
-        h, k = kernels[name]
-        for _ in range(count):
-            h.spmv_device(k, x.data_ptr(), y.data_ptr())
-
-    def timed(name, count):
-        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        torch.cuda.synchronize()
-        ev0.record()
-        run(name, count)
-        ev1.record()
-        torch.cuda.synchronize()
-        return ev0.elapsed_time(ev1) * 1e-3 / count
-
-    table = {}
-    per_fmt_steps = max(20, min(args.steps, 500))
-    for name in kernels:
-        run(name, max(3, args.warmup))
-        t = timed(name, per_fmt_steps)
-        b = spmv_bytes(name, n, nnz, nz)
-        table[name] = {"gbs": b / t / 1e9, "gflops": 2 * nnz / t / 1e9, "ms": t * 1e3,
-                       "bytes": b, "frac": b / t / 1e9 / peak}
-    t_crs = table["crs"]["ms"] * 1e-3
-    for name, tr in transforms.items():
-        if "refused" in tr:
-            continue
-        tr["tt"] = tr["t_trans_ms"] * 1e-3 / t_crs       # in CRS-SpMV units
-        tr["tt_kernel"] = tr["kernel_ms"] * 1e-3 / t_crs
+    table, transforms, handles, kernels, x, y = measure_matrix(
+        sp, torch, m, args.seed, peak, max(20, min(args.steps, 500)), args.warmup)
+    t_crs = table["crs"]["us"] * 1e-6
     # AT model on GPU timings, ELL-inner variant (Eq. 1-3 as implemented);
     # a guarded ELL is an excluded record, as in the reference's profile
     if "ell-inner" in table:
-        t_ell = table["ell-inner"]["ms"] * 1e-3
+        t_ell = table["ell-inner"]["us"] * 1e-6
         t_trans = transforms["ell"]["t_trans_ms"] * 1e-3
         sp_, tt_, r_ = sp.compute_metrics(t_crs, t_ell, t_trans)
-    else:
-        sp_ = tt_ = r_ = None
+        at = {"variant": "ell-inner", "sp": sp_, "tt": tt_, "r": r_}
+    else:  # an excluded record of the off-line profile (autotune.cpp:197-214)
+        at = {"variant": "ell-inner", "excluded": transforms["ell"].get("refused")}
 
-    best = max(table, key=lambda k: table[k]["gbs"])
-    launches_per_step = 1 if best != "ell-outer" else 2
+    best = best_format(table)
+    h, k = kernels[best]
 
     # ---- headline: K steps of the best format, device time, inputs in HBM
-    run(best, args.warmup)
+    for _ in range(args.warmup):
+        h.spmv_device(k, x.data_ptr(), y.data_ptr())
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    launches0 = lib.spmvtk_k_launch_count()
     with ClockSampler(0) as clk:
-        t_step = timed(best, args.steps)
+        ev0.record()
+        for _ in range(args.steps):
+            h.spmv_device(k, x.data_ptr(), y.data_ptr())
+        ev1.record()
+        torch.cuda.synchronize()
+    gpu_launches = lib.spmvtk_k_launch_count() - launches0
+    t_step = ev0.elapsed_time(ev1) * 1e-3 / args.steps
     bytes_step = spmv_bytes(best, n, nnz, nz)
     value = bytes_step / t_step / 1e9
     # second roofline: the x gathers.  Random columns make every x load an
-    # L2 sector fetch; their rate, not HBM bandwidth, bounds config 2
-    # (DESIGN.md §3).  Gathers per step = nnz (padding slots read the own
-    # row's x, coalesced); peak = the measured random-gather rate.
+    # L2 sector request; the SM's L1->L2 request rate, not HBM bandwidth,
+    # bounds these matrices.  Gathers per step = nnz; peak =
+    # the random-gather rate measured live.
     try:
         gpk = gather_peak(sp, torch)
         gather_roofline = {"bound": "l2-gather", "achieved": nnz / t_step / 1e9,
@@ -457,12 +538,11 @@ def impl_ours(args):
     except Exception as e:  # noqa: BLE001 -- reported, not fatal
         gather_roofline = {"error": f"{type(e).__name__}: {e}"[:200]}
 
-    # ---- e2e: through spmvtk_spmv() with pinned host buffers
+    # ---- e2e: through the C ABI with pinned host buffers
     xh = torch.from_numpy(sp.gen_vector(n, args.seed + 1)).pin_memory()
     yh = torch.empty(n, dtype=torch.float64).pin_memory()
     xn, yn = xh.numpy(), yh.numpy()
-    h, k = kernels[best]
-    e2e_steps = max(10, min(args.steps, 200))
+    e2e_steps = max(10, min(args.steps, 100))
     for _ in range(3):
         h.spmv(xn, k, 1, out=yn)
     torch.cuda.synchronize()
@@ -494,51 +574,19 @@ def impl_ours(args):
         assert np.array_equal(ys[i].numpy(), y.cpu().numpy()), "streaming e2e mismatch"
     pipe.free()
 
-    # ---- the same kernels on config 3 (27-point stencil: x gathers are local,
-    # so SpMV meets the HBM roofline there; config 2's random columns make
-    # every kernel L2-sector-bound)
-    also = {}
-    if not args.no_also and args.config != 3:
-        m3 = sp.HostCrs(3, 128, 0.0, args.seed).upload()
-        d3 = m3.describe()
-        nz3 = m3.row_stats().max_row
-        x3 = torch.from_numpy(sp.gen_vector(d3.n, args.seed + 1)).cuda()
-        y3 = torch.empty(d3.n, dtype=torch.float64, device="cuda")
-        e3 = m3.convert(sp.Format.ELL)
-        c3 = m3.convert(sp.Format.COO_ROW)
-        tab3 = {}
-        for name, h3, k3 in (("crs", m3, sp.Kernel.CRS), ("ell-inner", e3, sp.Kernel.ELL_INNER),
-                             ("coo-row", c3, sp.Kernel.COO_ROW_OUTER)):
-            for _ in range(5):
-                h3.spmv_device(k3, x3.data_ptr(), y3.data_ptr())
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            for _ in range(200):
-                h3.spmv_device(k3, x3.data_ptr(), y3.data_ptr())
-            e1.record()
-            torch.cuda.synchronize()
-            t3 = e0.elapsed_time(e1) / 200 * 1e-3
-            b3 = spmv_bytes(name, d3.n, d3.nnz, nz3)
-            tab3[name] = {"gbs": b3 / t3 / 1e9, "gflops": 2 * d3.nnz / t3 / 1e9,
-                          "us": t3 * 1e6, "frac": b3 / t3 / 1e9 / peak}
-        also["config3"] = {"n": d3.n, "nnz": d3.nnz, "formats": tab3,
-                           "ell_transform_kernel_ms":
-                               m3.transform_kernel_seconds(sp.Format.ELL, 3) * 1e3}
-        for h3 in (e3, c3, m3):
-            h3.free()
-        # config 1 (5 MB, L2-resident, launch-bound): SURVEY.md §8d asks for a
-        # CUDA graph of >= 1000 SpMVs so launch overhead does not dominate
-        try:
-            also["config1_graph"] = l2_resident_graph(sp, torch, args.seed, peak)
-        except Exception as e:  # reported, not fatal for the headline
-            also["config1_graph"] = {"error": f"{type(e).__name__}: {e}"[:200]}
-
-    # ---- CPU baseline: the reference itself on this host (bounded sample)
+    # ---- CPU baseline: the reference itself on this host (bounded sample),
+    # on the same matrix
     cpu = None
     if not args.no_cpu_baseline:
         try:
-            r = cpu_reference_run(host, n, nnz, nz)
-            r.pop("handles")
+            from oracle.oracle import Ref
+            ref = Ref()
+            rp, ci, v = host.arrays(index_base=1)
+            rh = ref.matrix(n, rp, ci, v)
+            del rp, ci, v
+            r = cpu_reference_run(ref, rh, n, nnz, nz)
+            for hh in r.pop("handles").values():
+                ref.free(hh)
             b = r["table"][r["best"]]
             cpu = {"value": b["gbs"], "unit": "GB/s", "cores": b["lanes"], "kind": "reference",
                    "sample": (f"reference measure_spmv (warm-up + median of 3) per format on the "
@@ -549,21 +597,43 @@ def impl_ours(args):
                    "cpu_model": r["cpu_model"], "nproc": r["cores"]}
         except Exception as e:  # reported, never silently replaced
             cpu = {"value": None, "unit": "GB/s", "cores": os.cpu_count(), "kind": "reference",
-                   "sample": f"unavailable: {e}"}
+                   "sample": f"unavailable: {type(e).__name__}: {e}"[:300]}
+    host.free()
+    for name, hh in handles.items():
+        if name != "crs":
+            hh.free()
 
+    # ---- the other full-size configs, measured in the same run
+    also = {}
+    if not args.no_also:
+        for cfg in (2, 3):
+            if cfg == args.config:
+                continue
+            mc = sp.HostCrs(cfg, DEFAULT_PARAM[cfg], 0.0, args.seed).upload()
+            tab, trs, hs, _, _, _ = measure_matrix(sp, torch, mc, args.seed, peak, 200, 5)
+            dc = mc.describe()
+            also[f"config{cfg}"] = {"n": dc.n, "nnz": dc.nnz, "d_mat": mc.row_stats().d_mat,
+                                    "best": best_format(tab), "formats": tab, "transforms": trs}
+            for name, hh in hs.items():
+                hh.free()
+        # config 1 (5 MB, L2-resident, launch-bound): SURVEY.md §8d asks for a
+        # CUDA graph of >= 1000 SpMVs so launch overhead does not dominate
+        try:
+            also["config1_graph"] = l2_resident_graph(sp, torch, args.seed, peak)
+        except Exception as e:  # reported, not fatal for the headline
+            also["config1_graph"] = {"error": f"{type(e).__name__}: {e}"[:200]}
+
+    traffic = ncu_traffic(args.config, best)
     line = {
         "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"baseline config {args.config} (random rows U{{8..24}}, "
-                               f"n={n})" if args.config == 2 else f"baseline config {args.config}",
-                   "n": n, "nnz": nnz, "max_row": nz, "d_mat": st.d_mat, "format": best,
-                   "gflops": 2 * nnz / t_step / 1e9,
-                   "l2": "inputs larger than L2 (no flush)"},
+        "config": workload_config(args.config, args.param, 0.0, args.seed, n, nnz, nz, st.d_mat),
+        "format": best, "gflops": 2 * nnz / t_step / 1e9,
         "roofline": {"bound": "hbm", "achieved": value, "peak": peak, "unit": "GB/s",
-                     "frac": value / peak, "traffic": ncu_traffic(args.config, best),
-                     "peak_kind": peak_kind,
-                     "kernel": best, "bytes_per_launch": bytes_step},
+                     "frac": value / peak, "traffic": traffic[0] if traffic else None,
+                     "traffic_source": traffic[1] if traffic else None,
+                     "peak_kind": peak_kind, "kernel": best, "bytes_per_launch": bytes_step},
         "roofline_gather": gather_roofline,
         "e2e": {"value": bytes_step / t_e2e / 1e9, "unit": "GB/s", "h2d_bytes_per_step": 8 * n,
                 "d2h_bytes_per_step": 8 * n, "ms_per_step": t_e2e * 1e3,
@@ -571,10 +641,9 @@ def impl_ours(args):
                        "host x/y, copies of one product overlap other products)",
                 "sync": {"value": bytes_step / t_e2e_sync / 1e9, "ms_per_step": t_e2e_sync * 1e3,
                          "api": "spmvtk_spmv (the reference's synchronous call)"}},
-        "gpu_launches": args.steps * launches_per_step,
+        "gpu_launches": gpu_launches,
         "clocks": clk.summary(),
-        "formats": table, "transforms": transforms,
-        "at": {"variant": "ell-inner", "sp": sp_, "tt": tt_, "r": r_},
+        "formats": table, "transforms": transforms, "at": at,
         "also": also,
         "cpu_baseline": cpu,
     }
@@ -588,18 +657,18 @@ def main():
     ap.add_argument("--steps", type=int, default=5000)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=DEFAULT_CONFIG)
     ap.add_argument("--param", type=int, default=None)
     ap.add_argument("--seed", type=int, default=2407)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-also", action="store_true", help="skip the config-3 side table")
+    ap.add_argument("--no-also", action="store_true", help="skip the configs 1-3 side tables")
     ap.add_argument("--force-dist", action="store_true",
                     help="use the row-block/NCCL path even on one rank (testing)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     if args.param is None:
-        args.param = {1: 256, 2: 1 << 20, 3: 128, 4: 1 << 22, 5: 1 << 21}[args.config]
+        args.param = DEFAULT_PARAM[args.config]
     if args.impl == "reference":
         return impl_reference(args)
     return impl_ours(args)

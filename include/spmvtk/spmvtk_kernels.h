@@ -223,6 +223,10 @@ int spmvtk_k_tune(const char* key, int value);
  * forwards keys it does not know here. */
 int spmvtk_k_tune_convert(const char* key, int value);
 
+/* SpMV kernel launches this process has made through the library (every
+ * SpMV entry point counts the kernels it launches): bench.py's gpu_launches. */
+unsigned long long spmvtk_k_launch_count(void);
+
 /* Forces every kernel of the library to be loaded (lazy module loading
  * would otherwise charge the first timed call). */
 int spmvtk_k_preload(void);

@@ -176,5 +176,7 @@ void preload_convert();
 void preload_util();
 void preload_inverse();
 void preload_seg();
+// Host-side count of the SpMV kernels this library launched (spmvtk_k_launch_count).
+void count_launches(int k);
 
 }  // namespace spmvtk_dev

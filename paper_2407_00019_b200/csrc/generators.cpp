@@ -322,7 +322,15 @@ HostCrs random_rows(std::int64_t n, std::uint64_t seed, std::int64_t window, Len
       val[k] = normal(r);
     }
   };
-  return build_blocked(n, seed, len_fn, fill);
+  // a row holds at most the distinct columns of its (edge-clipped) window
+  auto len_clipped = [n, window, &len_fn](Rng& r, std::int64_t i) {
+    const std::int64_t len = len_fn(r, i);
+    if (window <= 0) return std::min<std::int64_t>(len, n);
+    const std::int64_t range = std::min<std::int64_t>(n, i + window + 1) -
+                               std::max<std::int64_t>(0, i - window);
+    return std::min<std::int64_t>(len, range);
+  };
+  return build_blocked(n, seed, len_clipped, fill);
 }
 
 }  // namespace

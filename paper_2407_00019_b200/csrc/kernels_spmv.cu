@@ -612,6 +612,7 @@ void dispatch_vec(double mean, int64_t max_row, int64_t n, Rows rows, const int3
           n, rows, col, val, x, y, long_limit, long_rows);
       break;
   }
+  count_launches(1);
 }
 
 }  // namespace
@@ -628,8 +629,10 @@ int spmvtk_k_spmv_crs(int64_t n, const int32_t* irp, const int32_t* icol, const 
   if (use_long) cudaMemsetAsync(long_rows, 0, sizeof(int32_t), s);
   dispatch_vec(mean_row, max_row, n, CrsRows{irp}, icol, val, x, PlainOut{y},
                use_long ? long_limit : INT64_MAX, long_rows, s);
-  if (use_long)
+  if (use_long) {
     k_spmv_crs_long<<<kSMs * 4, 256, 0, s>>>(irp, icol, val, x, PlainOut{y}, long_rows);
+    count_launches(1);
+  }
   SPMVTK_LAUNCH_RETURN();
 }
 
@@ -679,6 +682,7 @@ int spmvtk_k_spmv_crs_push(int64_t n, const int32_t* irp, const int32_t* icol,
     lng.s.nwait = 0;
     dispatch_vec(mean_row, max_row, n, CrsRows{irp}, icol, val, x, vec, long_limit, long_rows, s);
     k_spmv_crs_long<<<kSMs * 4, 256, 0, s>>>(irp, icol, val, x, lng, long_rows);
+    count_launches(1);
   } else {
     dispatch_vec(mean_row, max_row, n, CrsRows{irp}, icol, val, x, vec, INT64_MAX, long_rows, s);
   }
@@ -712,6 +716,7 @@ int spmvtk_k_spmv_coo_row(int64_t n, int64_t nnz, const int32_t* row, const int3
   }
   const int64_t warps = (nnz + chunk - 1) / chunk;
   const int64_t blocks = (warps * 32 + 255) / 256;
+  count_launches(1);
   if (quad)
     k_spmv_coo_row4<<<static_cast<unsigned>(blocks), 256, 0, s>>>(n, nnz, chunk, row, col, val,
                                                                   x, y);
@@ -726,8 +731,10 @@ int spmvtk_k_spmv_coo_col(int64_t n, int64_t nnz, const int32_t* row, const int3
   cudaStream_t s = as_stream(stream);
   if (n <= 0) SPMVTK_LAUNCH_RETURN();
   cudaMemsetAsync(y, 0, static_cast<size_t>(n) * sizeof(double), s);
-  if (nnz > 0)
+  if (nnz > 0) {
     k_spmv_coo_col<<<grid_for((nnz + 3) / 4, 256, 8), 256, 0, s>>>(nnz, row, col, val, x, y);
+    count_launches(1);
+  }
   SPMVTK_LAUNCH_RETURN();
 }
 
@@ -742,6 +749,7 @@ int spmvtk_k_spmv_ell_cm(int64_t n, int32_t nz, int64_t ld, const double* val,
   const int64_t pairs = (n + 1) / 2;
   const unsigned blocks = static_cast<unsigned>((pairs + 255) / 256);
   k_spmv_ell_cm<4><<<blocks, 256, 0, s>>>(n, 0, nz, ld, val, col, x, PlainOut{y});
+  count_launches(1);
   SPMVTK_LAUNCH_RETURN();
 }
 
@@ -769,6 +777,7 @@ int spmvtk_k_spmv_ell_cm_split(int64_t n, int32_t nz, int64_t ld, const double* 
   dim3 grid(static_cast<unsigned>((pairs + 255) / 256), static_cast<unsigned>(splits));
   k_spmv_ell_cm_part<4><<<grid, 256, 0, s>>>(n, nz, splits, ld, val, col, x, partial);
   k_reduce_partials<<<grid_for(n, 256), 256, 0, s>>>(n, splits, partial, y);
+  count_launches(2);
   SPMVTK_LAUNCH_RETURN();
 }
 

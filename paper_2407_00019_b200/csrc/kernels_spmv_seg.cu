@@ -240,6 +240,7 @@ int launch_crs_seg(const int32_t* irp, const int32_t* icol, const double* val, c
   const unsigned blocks = static_cast<unsigned>((static_cast<int64_t>(warps) * 32 + 255) / 256);
 k_spmv_crs_seg<Out><<<blocks, 256, 0, s>>>(irp, icol, val, x, y, plan, w_base, w_end, row_lo,
                                              row_hi);
+  count_launches(1);
   SPMVTK_LAUNCH_RETURN();
 }
 

@@ -3,6 +3,8 @@
 //
 // HBM-bound integer work: grid-stride loops sized to a multiple of the 148
 // SMs, warp-shuffle reductions, one atomic per warp.
+#include <atomic>
+
 #include "common.cuh"
 #include "spmvtk/spmvtk.h"
 #include "spmvtk/spmvtk_kernels.h"
@@ -337,6 +339,7 @@ __global__ void __launch_bounds__(512) k_gather_probe(const double* __restrict__
 
 extern "C" {
 
+
 int spmvtk_k_row_stats(const int32_t* ptr, int64_t n, unsigned long long* acc,
                        void* stream) {
   cudaStream_t s = as_stream(stream);
@@ -408,6 +411,9 @@ int spmvtk_k_exclusive_scan(const int32_t* in, int32_t* out, int64_t n,
 }  // extern "C"
 
 namespace spmvtk_dev {
+std::atomic<unsigned long long> g_spmv_launches{0};
+void count_launches(int k) { g_spmv_launches.fetch_add(static_cast<unsigned long long>(k)); }
+
 void preload_util() {
   cudaFuncAttributes a;
   cudaFuncGetAttributes(&a, k_gather_probe);
@@ -421,6 +427,10 @@ void preload_util() {
   cudaFuncGetAttributes(&a, k_scan_lookback);
 }
 }  // namespace spmvtk_dev
+
+extern "C" unsigned long long spmvtk_k_launch_count(void) {
+  return spmvtk_dev::g_spmv_launches.load();
+}
 
 extern "C" {
 

@@ -30,10 +30,37 @@ def test_reference_arm_json_line():
     assert {"ell-inner@1", "coo-row@1", "crs"} <= set(line["formats"])
 
 
+def test_reference_arm_loads_only_the_reference_library():
+    """The reference arm must not map the product library (the driver voids
+    the ratio otherwise): its matrix is generated inside oracle/_ref."""
+    if not os.path.exists(os.path.join(ROOT, "oracle", "_ref", "libspmvtk_ref.so")):
+        pytest.skip("oracle/_ref not built")
+    code = ("import sys; sys.argv=['bench.py','--impl','reference','--config','2','--param',"
+            "'4096','--steps','3','--warmup','1']\n"
+            "import bench; bench.main()\n"
+            "maps=open('/proc/self/maps').read()\n"
+            "print('MAPPED', sorted({l.split()[-1] for l in maps.splitlines() "
+            "if 'spmvtk' in l}))\n")
+    out = subprocess.run([sys.executable, "-c", code], cwd=ROOT, capture_output=True, text=True,
+                         timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    mapped = [ln for ln in out.stdout.splitlines() if ln.startswith("MAPPED")][0]
+    assert "libspmvtk_ref.so" in mapped and "paper_2407_00019_b200" not in mapped, mapped
+
+
+def test_both_arms_share_the_config_dict():
+    """workload_config() is the one source of the `config` dict in both arms."""
+    sys.path.insert(0, ROOT)
+    import bench
+    a = bench.workload_config(4, 1 << 22, 0.0, 2407, 4194304, 67171957, 4096, 1.80181234)
+    b = bench.workload_config(4, 1 << 22, 0.0, 2407, 4194304, 67171957, 4096, 1.80179999)
+    assert a == b and a["workload"].startswith("BASELINE config 4")
+
+
 @pytest.mark.gpu
 def test_gpu_arm_json_line():
-    """Our arm on the GPU (config 2, few steps): every key the driver and the
-    judge read, with sane values (the driver re-runs the full default)."""
+    """Our arm on the GPU (default config 4, few steps): every key the driver
+    and the judge read, with sane values (the driver re-runs the full default)."""
     out = subprocess.run([sys.executable, "bench.py", "--steps", "30", "--warmup", "3",
                           "--no-also"], cwd=ROOT, capture_output=True, text=True, timeout=900)
     assert out.returncode == 0, out.stderr[-2000:]
@@ -44,7 +71,7 @@ def test_gpu_arm_json_line():
         assert key in line, key
     assert line["n_gpus"] == 1 and line["steps"] == 30 and line["warmup"] == 3
     assert line["value"] > 0 and line["unit"] == "GB/s" and line["higher_is_better"] is True
-    assert "workload" in line["config"]
+    assert line["config"]["workload"].startswith("BASELINE config 4")
     rf = line["roofline"]
     assert {"bound", "achieved", "peak", "unit", "frac", "traffic"} <= set(rf)
     assert 0 < rf["frac"] < 2 and abs(rf["achieved"] / rf["peak"] - rf["frac"]) < 1e-9

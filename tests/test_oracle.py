@@ -8,10 +8,12 @@
    tests/golden/make_golden.py from /root/reference compiled as-is).
 3. When oracle/_ref is present it is also checked live on fresh inputs.
 """
+import os
+
 import numpy as np
 import pytest
 
-from oracle.oracle import dense_matvec, max_rel_error, random_crs
+from oracle.oracle import REF_LIB, Ref, dense_matvec, max_rel_error, random_crs
 
 
 def test_kat_coo_row(port, kat):
@@ -199,3 +201,23 @@ def test_find_d_star_brute_force(port, ref):
             assert got == best == ref.find_d_star(recs, c)
             assert got <= prev
             prev = got
+
+
+def test_reference_arm_generator_matches_the_product_generator():
+    """bench.py --impl reference builds its matrix inside oracle/_ref (the
+    generator compiled there); it must equal the product's byte for byte."""
+    if not os.path.exists(REF_LIB):
+        pytest.skip("oracle/_ref not built")
+    from paper_2407_00019_b200 import spmvtk as sp
+    ref = Ref()
+    for cfg, param, dparam in ((1, 16, 0.0), (2, 4096, 0.0), (3, 8, 0.0), (4, 8192, 0.0),
+                               (5, 4096, 0.7)):
+        h = ref.gen_baseline(cfg, param, dparam, 11)
+        hc = sp.HostCrs(cfg, param, dparam, 11)
+        rp, ci, v = hc.arrays(1)
+        assert np.array_equal(ref.array(h, 1), rp), cfg
+        assert np.array_equal(ref.array(h, 3), ci), cfg
+        assert ref.array(h, 0).tobytes() == v.tobytes(), cfg
+        ref.free(h)
+        hc.free()
+    assert np.array_equal(ref.gen_vector(1000, 5), sp.gen_vector(1000, 5))
