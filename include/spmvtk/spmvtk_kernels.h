@@ -64,9 +64,18 @@ int spmvtk_k_crs_to_coo_row(int64_t n, int64_t nnz, const int32_t* irp,
                             int32_t* out_row, int32_t* out_col, double* out_val,
                             void* stream);
 
+/* Entries of a CRS whose column is not above the previous column of the same
+ * row (0 = columns strictly ascending in every row: no duplicate pairs). */
+int spmvtk_k_count_row_descents(const int32_t* irp, int64_t n, const int32_t* col,
+                                unsigned long long* bad, void* stream);
+
 /* CRS -> CCS Phase I (convert.cpp:24-53).  scratch: device buffer of
  * spmvtk_k_ccs_scratch_bytes(n, nnz) bytes.  Row indices come out ascending
- * inside every column, exactly as the reference's cursor scatter. */
+ * inside every column, exactly as the reference's cursor scatter.
+ * spmvtk_k_crs_to_ccs / _coo_col place each entry by its rank by row inside
+ * its column, so they need distinct (row, col) pairs;
+ * spmvtk_k_crs_to_ccs_stable / _coo_col_stable are stable partitions that
+ * keep the CRS order of every pair, duplicates included (same scratch). */
 size_t spmvtk_k_ccs_scratch_bytes(int64_t n, int64_t nnz);
 int spmvtk_k_crs_to_ccs(int64_t n, int64_t nnz, const int32_t* irp,
                         const int32_t* icol, const double* val,
@@ -76,6 +85,17 @@ int spmvtk_k_crs_to_ccs(int64_t n, int64_t nnz, const int32_t* irp,
  * :55-66) in one pass: as spmvtk_k_crs_to_ccs, and the sort that places each
  * entry also writes its column into col_idx (no separate col_ptr expansion).
  * Same scratch as spmvtk_k_crs_to_ccs. */
+/* 1 when the "ccs_stable" tuning knob routes every conversion to the stable
+ * pipeline (testing). */
+int spmvtk_k_ccs_force_stable(void);
+int spmvtk_k_crs_to_ccs_stable(int64_t n, int64_t nnz, const int32_t* irp,
+                               const int32_t* icol, const double* val, int32_t* col_ptr,
+                               int32_t* row_idx, double* out_val, void* scratch,
+                               void* stream);
+int spmvtk_k_crs_to_coo_col_stable(int64_t n, int64_t nnz, const int32_t* irp,
+                                   const int32_t* icol, const double* val,
+                                   int32_t* col_ptr, int32_t* row_idx, int32_t* col_idx,
+                                   double* out_val, void* scratch, void* stream);
 int spmvtk_k_crs_to_coo_col(int64_t n, int64_t nnz, const int32_t* irp,
                             const int32_t* icol, const double* val,
                             int32_t* col_ptr, int32_t* row_idx, int32_t* col_idx,

@@ -176,6 +176,22 @@ void preload_convert();
 void preload_util();
 void preload_inverse();
 void preload_seg();
+// CRS->CCS: the bucketed rank-by-row pipeline (kernels_convert.cu) for
+// duplicate-free matrices, the stable partition (kernels_ccs.cu) otherwise;
+// g_ccs_force_stable routes every conversion to the stable one (testing)
+extern int g_ccs_force_stable;
+void preload_ccs();
+}  // namespace spmvtk_dev
+extern "C" {
+size_t legacy_ccs_scratch_bytes(int64_t n, int64_t nnz);
+int legacy_crs_to_ccs(int64_t n, int64_t nnz, const int32_t* irp, const int32_t* icol,
+                      const double* val, int32_t* col_ptr, int32_t* row_idx, double* out_val,
+                      void* scratch, void* stream);
+int legacy_crs_to_coo_col(int64_t n, int64_t nnz, const int32_t* irp, const int32_t* icol,
+                          const double* val, int32_t* col_ptr, int32_t* row_idx,
+                          int32_t* col_idx, double* out_val, void* scratch, void* stream);
+}
+namespace spmvtk_dev {
 // Host-side count of the SpMV kernels this library launched (spmvtk_k_launch_count).
 void count_launches(int k);
 

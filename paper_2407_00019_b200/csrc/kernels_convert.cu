@@ -1051,6 +1051,10 @@ int spmvtk_k_tune_convert(const char* key, int value) {
     g_stage_threads = value == 512 ? 512 : 1024;
     return 0;
   }
+  if (key && std::string(key) == "ccs_stable") {  // force the stable pipeline (testing)
+    spmvtk_dev::g_ccs_force_stable = value;
+    return 0;
+  }
   if (key && std::string(key) == "ccs_coarse") {
     g_ccs_coarse = value;
     return 0;
@@ -1058,7 +1062,7 @@ int spmvtk_k_tune_convert(const char* key, int value) {
   return static_cast<int>(cudaErrorInvalidValue);
 }
 
-size_t spmvtk_k_ccs_scratch_bytes(int64_t n, int64_t nnz) {
+size_t legacy_ccs_scratch_bytes(int64_t n, int64_t nnz) {
   const BucketPlan bp = bucket_plan(n, nnz);
   const size_t t = static_cast<size_t>(bp.nb) * kSlices + 1;
   const size_t tc = static_cast<size_t>(bp.nc) * kSlices + 1;
@@ -1190,16 +1194,16 @@ int crs_to_ccs_impl(int64_t n, int64_t nnz, const int32_t* irp, const int32_t* i
 }
 }  // namespace
 
-int spmvtk_k_crs_to_ccs(int64_t n, int64_t nnz, const int32_t* irp, const int32_t* icol,
-                        const double* val, int32_t* col_ptr, int32_t* row_idx,
-                        double* out_val, void* scratch, void* stream) {
+int legacy_crs_to_ccs(int64_t n, int64_t nnz, const int32_t* irp, const int32_t* icol,
+                      const double* val, int32_t* col_ptr, int32_t* row_idx,
+                      double* out_val, void* scratch, void* stream) {
   return crs_to_ccs_impl(n, nnz, irp, icol, val, col_ptr, row_idx, out_val, nullptr, scratch,
                          stream);
 }
 
-int spmvtk_k_crs_to_coo_col(int64_t n, int64_t nnz, const int32_t* irp, const int32_t* icol,
-                            const double* val, int32_t* col_ptr, int32_t* row_idx,
-                            int32_t* col_idx, double* out_val, void* scratch, void* stream) {
+int legacy_crs_to_coo_col(int64_t n, int64_t nnz, const int32_t* irp, const int32_t* icol,
+                          const double* val, int32_t* col_ptr, int32_t* row_idx,
+                          int32_t* col_idx, double* out_val, void* scratch, void* stream) {
   return crs_to_ccs_impl(n, nnz, irp, icol, val, col_ptr, row_idx, out_val, col_idx, scratch,
                          stream);
 }

@@ -839,6 +839,7 @@ int spmvtk_k_preload(void) {
   spmvtk_dev::preload_util();
   spmvtk_dev::preload_inverse();
   spmvtk_dev::preload_seg();
+  spmvtk_dev::preload_ccs();
   cudaFuncAttributes a;
   cudaFuncGetAttributes(&a, k_spmv_crs_long<PlainOut>);
   cudaFuncGetAttributes(&a, k_spmv_crs_long<PushOut>);

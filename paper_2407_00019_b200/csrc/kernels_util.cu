@@ -158,6 +158,33 @@ __global__ void k_descents(const int32_t* __restrict__ key, int64_t len,
   if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(bad, cnt);
 }
 
+// entries whose column is not above the previous one IN THE SAME ROW (0 =
+// columns strictly ascending in every row, so no duplicate (row, col) pair):
+// a warp per 32-row group walks the group's entries 32 at a time; the row
+// starts among them come from the group's row ends (one per lane) as a
+// 32-bit mask
+__global__ void k_row_descents(const int32_t* __restrict__ irp, int64_t n,
+                               const int32_t* __restrict__ col, unsigned long long* bad) {
+  unsigned long long cnt = 0;
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t r0 = ((static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * 32;
+       r0 < n; r0 += warps * 32) {
+    const int64_t r1 = r0 + 32 < n ? r0 + 32 : n;
+    const int32_t a = __ldg(irp + r0), b = __ldg(irp + r1);
+    const int32_t end = r0 + lane < r1 ? __ldg(irp + r0 + lane + 1) : INT_MAX;
+    for (int32_t p0 = a; p0 < b; p0 += 32) {
+      const unsigned bit = (end >= p0 && end < p0 + 32) ? 1u << (end - p0) : 0u;
+      const unsigned starts = __reduce_or_sync(kFull, bit);
+      const int32_t p = p0 + lane;
+      if (p > a && p < b && !((starts >> lane) & 1u) && __ldg(col + p) <= __ldg(col + p - 1))
+        ++cnt;
+    }
+  }
+  cnt = warp_sum(cnt);
+  if (lane == 0 && cnt) atomicAdd(bad, cnt);
+}
+
 // ---- exclusive scan (tiles of 4096) -----------------------------------------
 constexpr int kScanThreads = 256;
 constexpr int kScanItems = 16;
@@ -384,6 +411,14 @@ int spmvtk_k_count_descents(const int32_t* key, int64_t len,
   cudaStream_t s = as_stream(stream);
   cudaMemsetAsync(bad, 0, sizeof(unsigned long long), s);
   if (len > 1) k_descents<<<grid_for(len, 256), 256, 0, s>>>(key, len, bad);
+  SPMVTK_LAUNCH_RETURN();
+}
+
+int spmvtk_k_count_row_descents(const int32_t* irp, int64_t n, const int32_t* col,
+                                unsigned long long* bad, void* stream) {
+  cudaStream_t s = as_stream(stream);
+  cudaMemsetAsync(bad, 0, sizeof(unsigned long long), s);
+  if (n > 0) k_row_descents<<<grid_for((n + 31) / 32 * 32, 256, 16), 256, 0, s>>>(irp, n, col, bad);
   SPMVTK_LAUNCH_RETURN();
 }
 

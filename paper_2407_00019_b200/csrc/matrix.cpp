@@ -170,6 +170,45 @@ void spmv_crs_rows(const Matrix& m, const double* x, double* y, std::int64_t r0,
 }
 }  // namespace
 
+bool pairs_ascending(const Matrix& m) {
+  std::lock_guard<std::mutex> lk(m.mu);
+  if (!m.pairs_ascending) {
+    const DevArray<std::int32_t>& idx = m.format == SPMVTK_FORMAT_CCS ? m.row : m.col;
+    DevArray<unsigned long long> bad(1, "ordering check");
+    rt::check_launch(spmvtk_k_count_row_descents(m.ptr.get(), m.n, idx.get(), bad.get(), s()),
+                     "ordering check");
+    unsigned long long h = 0;
+    rt::copy_to_host(&h, bad.get(), sizeof(h));
+    m.pairs_ascending = h == 0;
+  }
+  return *m.pairs_ascending;
+}
+
+namespace {
+// CRS (or CCS read as the CRS of the transpose) -> CCS / COO-col: the
+// rank-by-row pipeline when every segment's indices ascend strictly (no
+// duplicate pairs), else the stable partition that keeps duplicates in CRS
+// order (convert.cpp:43-51 semantics either way).
+void launch_ccs(const Matrix& a, const std::int32_t* seg_idx, std::int32_t* col_ptr,
+                std::int32_t* row_out, std::int32_t* col_out, double* val_out, void* scratch,
+                cudaStream_t st) {
+  const bool stable = spmvtk_k_ccs_force_stable() || !pairs_ascending(a);
+  const std::int64_t n = a.n, nnz = a.nnz;
+  int rc;
+  if (col_out)
+    rc = stable ? spmvtk_k_crs_to_coo_col_stable(n, nnz, a.ptr.get(), seg_idx, a.val.get(),
+                                                 col_ptr, row_out, col_out, val_out, scratch, st)
+                : spmvtk_k_crs_to_coo_col(n, nnz, a.ptr.get(), seg_idx, a.val.get(), col_ptr,
+                                          row_out, col_out, val_out, scratch, st);
+  else
+    rc = stable ? spmvtk_k_crs_to_ccs_stable(n, nnz, a.ptr.get(), seg_idx, a.val.get(), col_ptr,
+                                             row_out, val_out, scratch, st)
+                : spmvtk_k_crs_to_ccs(n, nnz, a.ptr.get(), seg_idx, a.val.get(), col_ptr,
+                                      row_out, val_out, scratch, st);
+  rt::check_launch(rc, col_out ? "CRS->COO-col" : "CRS->CCS");
+}
+}  // namespace
+
 Matrix* crs_from_arrays(std::int64_t n, std::int64_t nnz, const void* row_ptr,
                         const void* col_idx, const double* values, int index_width,
                         int index_base, bool on_device) {
@@ -218,6 +257,7 @@ Matrix* crs_block_from_arrays(std::int64_t n, std::int64_t ncols, std::int64_t r
   m->moments = mo;
   if (nnz && count_bad_indices(m->col.get(), nnz, ncols))
     throw Error(ErrorCode::Validation, "column index out of range");
+  pairs_ascending(*m);  // ordering of every row, cached (a CCS precondition)
   return m.release();
 }
 
@@ -361,15 +401,11 @@ Matrix* convert(const Matrix& a, spmvtk_format to, std::uint64_t max_bytes) {
         // Phase II folded into Phase I: the sort writes each entry's column
         m->ordering = 1;
         m->col.reset(nnz, "COO col_idx");
-        rt::check_launch(spmvtk_k_crs_to_coo_col(n, nnz, a.ptr.get(), a.col.get(), a.val.get(),
-                                                 colptr.get(), m->row.get(), m->col.get(),
-                                                 m->val.get(), scratch.get(), st),
-                         "CRS->COO-col");
+        launch_ccs(a, a.col.get(), colptr.get(), m->row.get(), m->col.get(), m->val.get(),
+                   scratch.get(), st);
       } else {
-        rt::check_launch(spmvtk_k_crs_to_ccs(n, nnz, a.ptr.get(), a.col.get(), a.val.get(),
-                                             colptr.get(), m->row.get(), m->val.get(),
-                                             scratch.get(), st),
-                         "CRS->CCS");
+        launch_ccs(a, a.col.get(), colptr.get(), m->row.get(), nullptr, m->val.get(),
+                   scratch.get(), st);
         m->ptr = std::move(colptr);
       }
       return m.release();
@@ -442,10 +478,8 @@ Matrix* to_crs(const Matrix& a) {
     case SPMVTK_FORMAT_CCS:
       // the CCS of A is the CRS of A^T: transposing it back yields the CRS of
       // A with rows visited in order, i.e. columns ascending in every row
-      rt::check_launch(spmvtk_k_crs_to_ccs(n, nnz, a.ptr.get(), a.row.get(), a.val.get(),
-                                           m->ptr.get(), m->col.get(), m->val.get(),
-                                           scratch.get(), st),
-                       "CCS->CRS");
+      launch_ccs(a, a.row.get(), m->ptr.get(), m->col.get(), nullptr, m->val.get(),
+                 scratch.get(), st);
       check_dup = false;
       break;
     case SPMVTK_FORMAT_COO_ROW:
@@ -507,17 +541,9 @@ double transform_kernel_seconds(const Matrix& a, spmvtk_format to, int repeats) 
         break;
       case SPMVTK_FORMAT_CCS:
       case SPMVTK_FORMAT_COO_COL:
-        if (to == SPMVTK_FORMAT_COO_COL)
-          rt::check_launch(spmvtk_k_crs_to_coo_col(n, nnz, a.ptr.get(), a.col.get(),
-                                                   a.val.get(), colptr.get(), out->row.get(),
-                                                   out->col.get(), out->val.get(), scratch.get(),
-                                                   st),
-                           "CRS->COO-col");
-        else
-          rt::check_launch(spmvtk_k_crs_to_ccs(n, nnz, a.ptr.get(), a.col.get(), a.val.get(),
-                                               colptr.get(), out->row.get(), out->val.get(),
-                                               scratch.get(), st),
-                           "CRS->CCS");
+        launch_ccs(a, a.col.get(), colptr.get(), out->row.get(),
+                   to == SPMVTK_FORMAT_COO_COL ? out->col.get() : nullptr, out->val.get(),
+                   scratch.get(), st);
         break;
       case SPMVTK_FORMAT_ELL:
         rt::check_launch(spmvtk_k_row_stats(a.ptr.get(), n, acc.get(), st), "row stats");

@@ -42,6 +42,9 @@ struct spmvtk_matrix {
   mutable spmvtk::rt::DevArray<std::int32_t> seg_plan;
   mutable std::vector<std::int32_t> seg_plan_host;
   mutable std::int32_t seg_plan_chunk = 0;
+  // CRS / CCS: columns (rows) strictly ascending inside every row (column),
+  // hence no duplicate pairs -- the fast CCS pipeline's precondition
+  mutable std::optional<bool> pairs_ascending;
 
   std::uint64_t device_bytes() const {
     return val.bytes() + ptr.bytes() + row.bytes() + col.bytes() + count.bytes();
@@ -54,6 +57,9 @@ using Matrix = spmvtk_matrix;
 
 // Exact row moments of a CRS handle (cached after the first GPU reduction).
 rt::Moments crs_moments(const Matrix& m);
+// Whether the pointer-structured handle (CRS; CCS = CRS of the transpose)
+// has strictly ascending indices inside every segment (cached).
+bool pairs_ascending(const Matrix& m);
 // The segmented-SpMV plan of a CRS handle (cached; nwarps + 1 entries).
 const std::vector<std::int32_t>& crs_seg_plan(const Matrix& m, const std::int32_t** dev);
 

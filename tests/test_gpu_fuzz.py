@@ -113,3 +113,64 @@ def test_fuzz_path(gpu, port, kind, n):
         back.free()
     for h in (ccs, coo, cooc, ell, ellr, m):
         h.free()
+
+
+STABLE_CASES = [("random", 33), ("random", 257), ("banded", 70000), ("powerlaw", 70000),
+                ("dense_col", 20000), ("dense_row", 3000), ("empty", 32), ("diag", 1)]
+
+
+@pytest.mark.parametrize("kind,n", STABLE_CASES)
+def test_stable_ccs_pipeline(gpu, port, kind, n):
+    """The stable partition pipeline (kernels_ccs.cu), forced for matrices the
+    rank-by-row pipeline would take, is bit-exact against the port too."""
+    sp = gpu
+    lib = sp.load_library()
+    rng = np.random.default_rng(zlib.crc32(f"stable:{kind}:{n}".encode()))
+    rows = _case(kind, n, rng)
+    rp, ci, v = _rows_to_crs(n, rows, rng, shuffle=kind == "random")
+    m = sp.Matrix.from_crs(n, rp, ci, v, index_base=1)
+    assert lib.spmvtk_k_tune(b"ccs_stable", 1) == 0
+    try:
+        cp, ri, cv = port.crs_to_ccs(n, rp, ci, v)
+        ccs = m.convert(sp.Format.CCS)
+        np.testing.assert_array_equal(ccs.array(sp.Array.POINTER, 8, 1), cp)
+        np.testing.assert_array_equal(ccs.array(sp.Array.ROW_IDX, 8, 1), ri)
+        assert ccs.array(sp.Array.VALUES).tobytes() == cv.tobytes()
+        cr, cc, cvv = port.crs_to_coo_col(n, rp, ci, v)
+        cooc = m.convert(sp.Format.COO_COL)
+        np.testing.assert_array_equal(cooc.array(sp.Array.ROW_IDX, 8, 1), cr)
+        np.testing.assert_array_equal(cooc.array(sp.Array.COL_IDX, 8, 1), cc)
+        assert cooc.array(sp.Array.VALUES).tobytes() == cvv.tobytes()
+        for h in (ccs, cooc):
+            h.free()
+    finally:
+        lib.spmvtk_k_tune(b"ccs_stable", 0)
+        m.free()
+
+
+@pytest.mark.parametrize("n,dups", [(50, 40), (3000, 2500), (70000, 50000)])
+def test_ccs_with_duplicate_pairs(gpu, port, n, dups):
+    """A CRS holding duplicate (row, col) pairs (allowed by crs_to_ccs,
+    convert.cpp:24-53): the conversion keeps every copy in CRS order, exactly
+    as the reference's cursor scatter -- routed to the stable pipeline by the
+    handle's ordering check."""
+    sp = gpu
+    rng = np.random.default_rng(n)
+    rows = [np.sort(rng.choice(n, size=int(rng.integers(0, 6)), replace=False)) for _ in range(n)]
+    for i in rng.choice(n, size=dups):  # repeat one of the row's columns
+        if rows[i].size:
+            rows[i] = np.sort(np.append(rows[i], rows[i][rng.integers(0, rows[i].size)]))
+    rp, ci, v = _rows_to_crs(n, rows, rng, shuffle=False)
+    m = sp.Matrix.from_crs(n, rp, ci, v, index_base=1)
+    cp, ri, cv = port.crs_to_ccs(n, rp, ci, v)
+    ccs = m.convert(sp.Format.CCS)
+    np.testing.assert_array_equal(ccs.array(sp.Array.POINTER, 8, 1), cp)
+    np.testing.assert_array_equal(ccs.array(sp.Array.ROW_IDX, 8, 1), ri)
+    assert ccs.array(sp.Array.VALUES).tobytes() == cv.tobytes()
+    cr, cc, cvv = port.crs_to_coo_col(n, rp, ci, v)
+    cooc = m.convert(sp.Format.COO_COL)
+    np.testing.assert_array_equal(cooc.array(sp.Array.ROW_IDX, 8, 1), cr)
+    np.testing.assert_array_equal(cooc.array(sp.Array.COL_IDX, 8, 1), cc)
+    assert cooc.array(sp.Array.VALUES).tobytes() == cvv.tobytes()
+    for h in (ccs, cooc, m):
+        h.free()
