@@ -269,6 +269,49 @@ spmvtk_status spmvtk_read_matrix_market_host(const char* path, spmvtk_host_crs**
 /* Uploads a host CRS (from spmvtk_gen_baseline_host) into a device handle. */
 spmvtk_status spmvtk_matrix_from_host_crs(const spmvtk_host_crs* h, spmvtk_matrix** out);
 
+/* ---- multi-GPU: row-block shards, one process per GPU, NCCL -------------
+ * The rows are cut into `world` contiguous entry-balanced blocks
+ * (spmvtk_partition_rows: rank k starts at the first row whose start reaches
+ * k*nnz/world -- the reference's partition_range, spmv.cpp:36-54, applied to
+ * entries instead of rows).  A shard holds its rows with global column
+ * indices, so every transform of it is local; SpMV iterations exchange x
+ * between ranks over NCCL (spmvtk_dist_spmv_iterate). */
+#define SPMVTK_DIST_ID_BYTES 128
+typedef struct spmvtk_dist spmvtk_dist;
+/* Rank 0 makes the id and sends it to the others (any channel). */
+spmvtk_status spmvtk_dist_unique_id(unsigned char id[SPMVTK_DIST_ID_BYTES]);
+/* Joins the communicator on the calling thread's current CUDA device. */
+spmvtk_status spmvtk_dist_init(int rank, int world, const unsigned char id[SPMVTK_DIST_ID_BYTES],
+                               spmvtk_dist** out);
+void spmvtk_dist_free(spmvtk_dist* d);
+/* begin[world + 1] for a CRS given by its n + 1 row pointers (host; any
+ * index base). */
+spmvtk_status spmvtk_partition_rows(const int64_t* row_ptr, int64_t n, int world, int64_t* begin);
+/* This rank's shard of a global CRS in host arrays: only the rank's rows are
+ * read and uploaded (index_width 4 or 8, index_base 0 or 1). */
+spmvtk_status spmvtk_matrix_distribute(const spmvtk_dist* d, int64_t n, const void* row_ptr,
+                                       const void* col_idx, const double* values, int index_width,
+                                       int index_base, spmvtk_matrix** shard);
+/* A BASELINE workload's shard for (rank, world), generated alone on the host
+ * (every row length is drawn for the partition, only the rank's rows are
+ * filled): identical to the rows of spmvtk_gen_baseline_host's matrix.  The
+ * host variant needs no device; the other uploads it. */
+spmvtk_status spmvtk_gen_baseline_shard_host(int config, int64_t param, double dparam,
+                                             uint64_t seed, int rank, int world,
+                                             spmvtk_host_crs** out, int64_t* rows,
+                                             int64_t* row_offset, int64_t* ncols);
+spmvtk_status spmvtk_gen_baseline_shard(const spmvtk_dist* d, int config, int64_t param,
+                                        double dparam, uint64_t seed, spmvtk_matrix** shard);
+/* x_{t+1} = A x_t, `steps` times.  x: device vector of ncols doubles on the
+ * current stream, x_0 on entry (the same on every rank), x_steps on exit on
+ * every rank.  Each step: the shard's SpMV writes its rows of x_{t+1}
+ * straight into its block, then every block is broadcast to the other ranks
+ * (grouped ncclBroadcast, in place).  seconds (may be NULL): this rank's
+ * device time per step (CUDA events); take the max over ranks. */
+spmvtk_status spmvtk_dist_spmv_iterate(const spmvtk_dist* d, const spmvtk_matrix* shard,
+                                       spmvtk_kernel kernel, double* x, int64_t steps,
+                                       double* seconds);
+
 /* x ~ U(-1,1) from seed with the reference's raw-bit mapping. */
 spmvtk_status spmvtk_gen_vector(int64_t n, uint64_t seed, double* out);
 

@@ -72,11 +72,12 @@ const dev::Matrix& crs_of(const spmvtk_matrix* m) {
 }
 
 dev::Matrix* upload(const gen::HostCrs& h) {
+  const std::int64_t ncols = h.ncols < 0 ? h.n : h.ncols;
   if (h.wide())
-    return dev::crs_from_arrays(h.n, h.nnz(), h.row_ptr.data(), h.col_idx.data(), h.values.data(),
-                                8, h.base, false);
-  return dev::crs_from_arrays(h.n, h.nnz(), h.row_ptr32.data(), h.col32.data(), h.values.data(), 4,
-                              h.base, false);
+    return dev::crs_block_from_arrays(h.n, ncols, h.row_offset, h.nnz(), h.row_ptr.data(),
+                                      h.col_idx.data(), h.values.data(), 8, h.base, false);
+  return dev::crs_block_from_arrays(h.n, ncols, h.row_offset, h.nnz(), h.row_ptr32.data(),
+                                    h.col32.data(), h.values.data(), 4, h.base, false);
 }
 
 thread_local double t_scratch = 0.0;
@@ -721,6 +722,107 @@ spmvtk_status spmvtk_matrix_from_host_crs(const spmvtk_host_crs* h, spmvtk_matri
     need(h);
     need(out, "null output");
     *out = upload(h->h);
+  });
+}
+
+// ---- multi-GPU (dist.cpp) ---------------------------------------------------
+spmvtk_status spmvtk_dist_unique_id(unsigned char* id) {
+  return guarded([&] {
+    need(id, "null output");
+    spmvtk::dist::unique_id(id);
+  });
+}
+
+spmvtk_status spmvtk_dist_init(int rank, int world, const unsigned char* id, spmvtk_dist** out) {
+  return guarded([&] {
+    need(id);
+    need(out, "null output");
+    *out = spmvtk::dist::init(rank, world, id);
+  });
+}
+
+void spmvtk_dist_free(spmvtk_dist* d) { spmvtk::dist::destroy(d); }
+
+spmvtk_status spmvtk_partition_rows(const int64_t* row_ptr, int64_t n, int world, int64_t* begin) {
+  return guarded([&] {
+    need(row_ptr);
+    need(begin, "null output");
+    if (n < 0) throw Error(ErrorCode::InvalidArgument, "negative dimension");
+    const std::vector<std::int64_t> b = gen::partition_rows(row_ptr, n, world);
+    std::copy(b.begin(), b.end(), begin);
+  });
+}
+
+spmvtk_status spmvtk_matrix_distribute(const spmvtk_dist* d, int64_t n, const void* row_ptr,
+                                       const void* col_idx, const double* values,
+                                       int index_width, int index_base, spmvtk_matrix** out) {
+  return guarded([&] {
+    need(d);
+    need(row_ptr);
+    need(out, "null output");
+    if (index_width != 4 && index_width != 8)
+      throw Error(ErrorCode::InvalidArgument, "index width must be 4 or 8");
+    if (n < 0) throw Error(ErrorCode::InvalidArgument, "negative dimension");
+    std::vector<std::int64_t> rp(static_cast<std::size_t>(n) + 1);
+    for (std::int64_t i = 0; i <= n; ++i)
+      rp[static_cast<std::size_t>(i)] =
+          index_width == 8 ? static_cast<const std::int64_t*>(row_ptr)[i]
+                           : static_cast<const std::int32_t*>(row_ptr)[i];
+    const int rank = spmvtk::dist::rank_of(*d);
+    const std::vector<std::int64_t> b = gen::partition_rows(rp.data(), n, spmvtk::dist::world_of(*d));
+    const std::int64_t r0 = b[static_cast<std::size_t>(rank)],
+                       r1 = b[static_cast<std::size_t>(rank) + 1];
+    // the block's pointers relative to its first entry (in the caller's base
+    // and width, like its column indices)
+    const std::int64_t e0 = rp[static_cast<std::size_t>(r0)] - index_base;
+    const std::int64_t cnt = rp[static_cast<std::size_t>(r1)] - rp[static_cast<std::size_t>(r0)];
+    std::vector<std::int64_t> lrp(static_cast<std::size_t>(r1 - r0) + 1);
+    for (std::int64_t i = r0; i <= r1; ++i)
+      lrp[static_cast<std::size_t>(i - r0)] = rp[static_cast<std::size_t>(i)] - e0;
+    std::vector<std::int32_t> lrp32;
+    if (index_width == 4) lrp32.assign(lrp.begin(), lrp.end());
+    const char* ci = static_cast<const char*>(col_idx) + e0 * index_width;
+    *out = dev::crs_block_from_arrays(
+        r1 - r0, n, r0, cnt,
+        index_width == 8 ? static_cast<const void*>(lrp.data()) : static_cast<const void*>(lrp32.data()),
+        cnt ? ci : nullptr, cnt ? values + e0 : nullptr, index_width, index_base, false);
+  });
+}
+
+spmvtk_status spmvtk_gen_baseline_shard_host(int config, int64_t param, double dparam,
+                                             uint64_t seed, int rank, int world,
+                                             spmvtk_host_crs** out, int64_t* rows,
+                                             int64_t* row_offset, int64_t* ncols) {
+  return guarded([&] {
+    need(out, "null output");
+    auto h = std::make_unique<spmvtk_host_crs>();
+    h->h = gen::baseline_shard(config, param, dparam, seed, rank, world);
+    if (rows) *rows = h->h.n;
+    if (row_offset) *row_offset = h->h.row_offset;
+    if (ncols) *ncols = h->h.ncols < 0 ? h->h.n : h->h.ncols;
+    *out = h.release();
+  });
+}
+
+spmvtk_status spmvtk_gen_baseline_shard(const spmvtk_dist* d, int config, int64_t param,
+                                        double dparam, uint64_t seed, spmvtk_matrix** out) {
+  return guarded([&] {
+    need(d);
+    need(out, "null output");
+    *out = upload(gen::baseline_shard(config, param, dparam, seed, spmvtk::dist::rank_of(*d),
+                                      spmvtk::dist::world_of(*d)));
+  });
+}
+
+spmvtk_status spmvtk_dist_spmv_iterate(const spmvtk_dist* d, const spmvtk_matrix* m,
+                                       spmvtk_kernel kernel, double* x, int64_t steps,
+                                       double* seconds) {
+  return guarded([&] {
+    need(d);
+    need(m);
+    if (m->ncols > 0) need(x);
+    const double s = spmvtk::dist::iterate(*d, *m, kernel, x, steps);
+    if (seconds) *seconds = s;
   });
 }
 

@@ -212,11 +212,18 @@ void sample_columns(Rng& r, std::int64_t lo, std::int64_t hi, std::int64_t len,
   std::sort(out.begin(), out.end());
 }
 
-// Builds a CRS (base 0, int32 indices) from per-block row generators.
+// Row-block shard being generated (world == 1: the whole matrix).
+struct ShardSpec {
+  int rank = 0, world = 1;
+};
+thread_local ShardSpec t_shard;
+
+// Builds a CRS (base 0, int32 indices) from per-block row generators.  For
+// a shard (t_shard.world > 1) every row length is drawn (the partition needs
+// them) but only the RNG blocks overlapping the shard's rows are filled.
 template <typename LenFn, typename RowFn>
 HostCrs build_blocked(std::int64_t n, std::uint64_t seed, LenFn&& row_len, RowFn&& fill_row) {
   HostCrs m;
-  m.n = n;
   m.base = 0;
   const std::int64_t blocks = (n + kBlockRows - 1) / kBlockRows;
   std::vector<std::int64_t> len(static_cast<std::size_t>(n));
@@ -235,25 +242,51 @@ HostCrs build_blocked(std::int64_t n, std::uint64_t seed, LenFn&& row_len, RowFn
     for (std::int64_t i = b * kBlockRows; i < std::min(n, (b + 1) * kBlockRows); ++i)
       len[static_cast<std::size_t>(i)] = row_len(r, i);
   });
-  m.row_ptr32.resize(static_cast<std::size_t>(n) + 1);
+  std::vector<std::int64_t> gptr(static_cast<std::size_t>(n) + 1);
   std::int64_t acc = 0;
   for (std::int64_t i = 0; i < n; ++i) {
-    m.row_ptr32[static_cast<std::size_t>(i)] = static_cast<std::int32_t>(acc);
+    gptr[static_cast<std::size_t>(i)] = acc;
     acc += len[static_cast<std::size_t>(i)];
     if (acc >= INT32_MAX) throw Error(ErrorCode::InvalidArgument, "generated nnz exceeds int32");
   }
-  m.row_ptr32[static_cast<std::size_t>(n)] = static_cast<std::int32_t>(acc);
-  m.col32.resize(static_cast<std::size_t>(acc));
-  m.values.resize(static_cast<std::size_t>(acc));
-  // pass 2: columns and values (second stream per block)
+  gptr[static_cast<std::size_t>(n)] = acc;
+  std::int64_t lo = 0, hi = n;
+  if (t_shard.world > 1) {
+    const std::vector<std::int64_t> part = partition_rows(gptr.data(), n, t_shard.world);
+    lo = part[static_cast<std::size_t>(t_shard.rank)];
+    hi = part[static_cast<std::size_t>(t_shard.rank) + 1];
+  }
+  const std::int64_t e0 = gptr[static_cast<std::size_t>(lo)];
+  m.n = hi - lo;
+  m.ncols = n;
+  m.row_offset = lo;
+  m.row_ptr32.resize(static_cast<std::size_t>(m.n) + 1);
+  for (std::int64_t i = lo; i <= hi; ++i)
+    m.row_ptr32[static_cast<std::size_t>(i - lo)] =
+        static_cast<std::int32_t>(gptr[static_cast<std::size_t>(i)] - e0);
+  const std::int64_t cnt = gptr[static_cast<std::size_t>(hi)] - e0;
+  m.col32.resize(static_cast<std::size_t>(cnt));
+  m.values.resize(static_cast<std::size_t>(cnt));
+  // pass 2: columns and values (second stream per block) of the blocks that
+  // hold rows [lo, hi); rows outside are drawn into a scratch row so the
+  // stream advances exactly as in the whole-matrix generation
   run([&](std::int64_t b) {
+    const std::int64_t b0 = b * kBlockRows, b1 = std::min(n, (b + 1) * kBlockRows);
+    if (b1 <= lo || b0 >= hi) return;
     Rng r(mix(seed ^ (0x2000000ull + static_cast<std::uint64_t>(b))));
-    std::vector<std::int32_t> cols;
+    std::vector<std::int32_t> cols, skip_c;
+    std::vector<double> skip_v;
     std::unordered_set<std::int64_t> set;
-    for (std::int64_t i = b * kBlockRows; i < std::min(n, (b + 1) * kBlockRows); ++i) {
-      const std::int64_t a = m.row_ptr32[static_cast<std::size_t>(i)];
-      fill_row(r, i, len[static_cast<std::size_t>(i)], cols, set, m.col32.data() + a,
-               m.values.data() + a);
+    for (std::int64_t i = b0; i < b1; ++i) {
+      const std::int64_t L = len[static_cast<std::size_t>(i)];
+      if (i >= lo && i < hi) {
+        const std::int64_t a = gptr[static_cast<std::size_t>(i)] - e0;
+        fill_row(r, i, L, cols, set, m.col32.data() + a, m.values.data() + a);
+      } else {
+        skip_c.resize(static_cast<std::size_t>(L));
+        skip_v.resize(static_cast<std::size_t>(L));
+        fill_row(r, i, L, cols, set, skip_c.data(), skip_v.data());
+      }
     }
   });
   return m;
@@ -334,6 +367,58 @@ HostCrs random_rows(std::int64_t n, std::uint64_t seed, std::int64_t window, Len
 }
 
 }  // namespace
+
+std::vector<std::int64_t> partition_rows(const std::int64_t* row_ptr, std::int64_t n, int world) {
+  if (world < 1) throw Error(ErrorCode::InvalidArgument, "world size must be at least 1");
+  std::vector<std::int64_t> begin(static_cast<std::size_t>(world) + 1, n);
+  const std::int64_t base = row_ptr[0], nnz = row_ptr[n] - base;
+  begin[0] = 0;
+  for (int k = 1; k < world; ++k) {
+    const std::int64_t target = base + nnz * k / world;
+    // first row r in [begin[k-1], n] with row_ptr[r] >= target
+    std::int64_t lo = begin[static_cast<std::size_t>(k) - 1], hi = n;
+    while (lo < hi) {
+      const std::int64_t mid = lo + (hi - lo) / 2;
+      if (row_ptr[mid] >= target) hi = mid;
+      else lo = mid + 1;
+    }
+    begin[static_cast<std::size_t>(k)] = lo;
+  }
+  begin[static_cast<std::size_t>(world)] = n;
+  return begin;
+}
+
+HostCrs baseline_shard(int config, std::int64_t param, double dparam, std::uint64_t seed,
+                       int rank, int world) {
+  if (world < 1 || rank < 0 || rank >= world)
+    throw Error(ErrorCode::InvalidArgument, "rank must lie in [0, world)");
+  if (world == 1) return baseline(config, param, dparam, seed);
+  if (config == 1) {  // small and RNG-free: generate, then cut
+    HostCrs full = baseline(config, param, dparam, seed);
+    std::vector<std::int64_t> ptr(full.row_ptr32.begin(), full.row_ptr32.end());
+    const auto part = partition_rows(ptr.data(), full.n, world);
+    const std::int64_t lo = part[static_cast<std::size_t>(rank)], hi = part[static_cast<std::size_t>(rank) + 1];
+    HostCrs m;
+    m.base = 0;
+    m.n = hi - lo;
+    m.ncols = full.n;
+    m.row_offset = lo;
+    const std::int32_t e0 = full.row_ptr32[static_cast<std::size_t>(lo)];
+    for (std::int64_t i = lo; i <= hi; ++i) m.row_ptr32.push_back(full.row_ptr32[static_cast<std::size_t>(i)] - e0);
+    m.col32.assign(full.col32.begin() + e0, full.col32.begin() + full.row_ptr32[static_cast<std::size_t>(hi)]);
+    m.values.assign(full.values.begin() + e0, full.values.begin() + full.row_ptr32[static_cast<std::size_t>(hi)]);
+    return m;
+  }
+  t_shard = ShardSpec{rank, world};
+  try {
+    HostCrs m = baseline(config, param, dparam, seed);
+    t_shard = ShardSpec{};
+    return m;
+  } catch (...) {
+    t_shard = ShardSpec{};
+    throw;
+  }
+}
 
 HostCrs baseline(int config, std::int64_t param, double dparam, std::uint64_t seed) {
   switch (config) {

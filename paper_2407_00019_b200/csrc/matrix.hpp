@@ -127,3 +127,14 @@ std::int64_t device_array(const Matrix& m, spmvtk_array which, void** ptr);
 const char* kernel_label(spmvtk_kernel k);
 
 }  // namespace spmvtk::dev
+
+struct spmvtk_dist;
+namespace spmvtk::dist {
+spmvtk_dist* init(int rank, int world, const unsigned char* id);
+void destroy(spmvtk_dist* d);
+int rank_of(const spmvtk_dist& d);
+int world_of(const spmvtk_dist& d);
+void unique_id(unsigned char* out);
+double iterate(const spmvtk_dist& d, const dev::Matrix& shard, spmvtk_kernel kernel, double* x,
+               std::int64_t steps);
+}  // namespace spmvtk::dist

@@ -379,9 +379,15 @@ def cuda_apply(handle, kernel):
 # --------------------------------------------------------------------------
 def bench_main(args, rank: int, world: int, local: int) -> int:
     """bench.py under torchrun: strong scaling of the config's SpMV over
-    `world` GPUs (matrix fixed, rows split), x all-gathered every step."""
+    `world` GPUs through the C ABI (spmvtk_dist_*): each rank generates only
+    its entry-balanced row block (spmvtk_gen_baseline_shard), and
+    spmvtk_dist_spmv_iterate runs x_{t+1} = A x_t with the x blocks exchanged
+    over the library's own NCCL communicator (grouped in-place broadcasts).
+    torch.distributed only carries the communicator id, the barriers and the
+    max-over-ranks of the timings."""
     import json
     import os
+    import sys
     import time
 
     import torch
@@ -389,242 +395,162 @@ def bench_main(args, rank: int, world: int, local: int) -> int:
 
     from . import spmvtk as sp
 
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from bench import (ELL_GUARD_BYTES, METRIC, ClockSampler, cpu_reference_run, hbm_peak,
+                       spmv_bytes, workload_config)
+
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     sp.set_stream(torch.cuda.current_stream().cuda_stream)
-    host = sp.HostCrs(args.config, args.param, 0.0, args.seed)
-    n, nnz = host.n, host.nnz
-    rp, ci, v = host.arrays(index_base=0)
-    r0, lrp, lci, lv = shard_arrays(rp, ci, v, n, world, rank)
-    del rp, ci, v
-    host.free()
-    shard = sp.Matrix.from_crs_block(block_rows(n, world), n, r0, lrp, lci, lv)
-    st = shard.row_stats() if shard.describe().nnz else None
-    local_max = st.max_row if st else 0
-    t = torch.tensor([local_max], dtype=torch.int64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    nz_global = int(t.item())
+    lib = sp.load_library()
+    uid = [sp.Dist.unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    comm = sp.Dist(rank, world, uid[0])
+    shard = comm.shard(args.config, args.param, 0.0, args.seed)
+    desc = shard.describe()
+    n, rows, r0 = desc.ncols, desc.n, desc.row_offset
+    st = shard.row_stats() if desc.nnz else None
+    # global statistics from the shards: entries, sum of squared row lengths, max row
+    sums = torch.tensor([float(desc.nnz),
+                         rows * (st.sigma ** 2 + st.mu ** 2) if st else 0.0],
+                        dtype=torch.float64, device="cuda")
+    dist.all_reduce(sums, op=dist.ReduceOp.SUM)
+    mx = torch.tensor([st.max_row if st else 0], dtype=torch.int64, device="cuda")
+    dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+    nnz, nz = int(round(sums[0].item())), int(mx.item())
+    mu_g = nnz / n
+    d_mat_g = ((max(sums[1].item() / n - mu_g * mu_g, 0.0)) ** 0.5) / mu_g if nnz else 0.0
 
-    handles = {"crs": (shard, sp.Kernel.CRS),
-               "ell-inner": (shard.convert(sp.Format.ELL), sp.Kernel.ELL_INNER)}
+    handles = {"crs": (shard, sp.Kernel.CRS)}
+    if n * nz * 16 <= ELL_GUARD_BYTES:  # the reference's guard on the whole matrix
+        handles["ell-inner"] = (shard.convert(sp.Format.ELL), sp.Kernel.ELL_INNER)
+    xl = torch.from_numpy(sp.gen_vector(n, args.seed + 1)).cuda()
+    yl = torch.empty(max(rows, 1), dtype=torch.float64, device="cuda")
 
-    def bytes_of(fmt):
-        d = shard.describe()
-        rows, entries = d.n, d.nnz
-        if fmt == "crs":
-            return 12 * entries + 4 * (rows + 1) + 8 * n + 8 * rows
-        return 12 * rows * handles["ell-inner"][0].describe().band_count + 8 * n + 8 * rows
-
-    x = torch.from_numpy(sp.gen_vector(n, args.seed + 1)).cuda()
-    y = torch.empty(block_rows(n, world), dtype=torch.float64, device="cuda")
-
-    def local_time(fmt, reps=50):
-        h, k = handles[fmt]
+    def local_time(h, k, reps=50):
+        if rows == 0:
+            return 0.0
         for _ in range(3):
-            h.spmv_device(k, x.data_ptr(), y.data_ptr())
+            h.spmv_device(k, xl.data_ptr(), yl.data_ptr())
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         for _ in range(reps):
-            h.spmv_device(k, x.data_ptr(), y.data_ptr())
+            h.spmv_device(k, xl.data_ptr(), yl.data_ptr())
         e1.record()
         torch.cuda.synchronize()
         return e0.elapsed_time(e1) / reps * 1e-3
 
-    # format choice: slowest rank decides (max over ranks), best format wins
-    times = torch.tensor([local_time(f) for f in handles], dtype=torch.float64, device="cuda")
+    def shard_bytes(name, hh):  # the shard's own SpMV (x read whole, its rows of y)
+        if name == "crs":
+            return 12 * desc.nnz + 4 * (rows + 1) + 8 * rows + 8 * n
+        return 12 * rows * hh.describe().band_count + 8 * rows + 8 * n
+
+    # format: the slowest rank decides (max over ranks), the fastest format wins
+    mine = [local_time(hh, kk) for hh, kk in handles.values()]
+    times = torch.tensor(mine, dtype=torch.float64, device="cuda")
     dist.all_reduce(times, op=dist.ReduceOp.MAX)
-    fmt = list(handles)[int(torch.argmin(times).item())]
+    best = int(torch.argmin(times).item())
+    fmt = list(handles)[best]
+    t_local = float(times[best].item())
     h, k = handles[fmt]
-    it = DistSpMV(n, world, rank, cuda_apply(h, k), "cuda")
-    it.set_x(sp.gen_vector(n, args.seed + 1))
+    # per-GPU roofline: the slowest rank's shard SpMV rate
+    rate = torch.tensor([shard_bytes(fmt, h) / mine[best] if mine[best] > 0 else float("inf")],
+                        dtype=torch.float64, device="cuda")
+    dist.all_reduce(rate, op=dist.ReduceOp.MIN)
 
-    def timed(steps, communicate):
-        for _ in range(args.warmup):
-            it.step(communicate)
-        dist.barrier()
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(steps):
-            it.step(communicate)
-        e1.record()
-        torch.cuda.synchronize()
-        dist.barrier()
-        tt = torch.tensor([e0.elapsed_time(e1) * 1e-3 / steps], dtype=torch.float64,
-                          device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        return float(tt.item())
-
-    import sys
-    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-    from bench import ClockSampler, hbm_peak, spmv_bytes
+    x = torch.from_numpy(sp.gen_vector(n, args.seed + 1)).cuda()
+    comm.iterate(h, k, x.data_ptr(), args.warmup)
+    torch.cuda.synchronize()
+    dist.barrier()
+    launches0 = lib.spmvtk_k_launch_count()
     with ClockSampler(local) as clk:
-        t_step = timed(args.steps, True)
-    t_local = timed(max(20, args.steps // 4), False)
+        t_rank = comm.iterate(h, k, x.data_ptr(), args.steps)
+    launches = torch.tensor([lib.spmvtk_k_launch_count() - launches0], dtype=torch.int64,
+                            device="cuda")
+    dist.all_reduce(launches, op=dist.ReduceOp.SUM)
+    tt = torch.tensor([t_rank], dtype=torch.float64, device="cuda")
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    t_step = float(tt.item())
+    # every rank must hold the same iterate: compare a checksum of x
+    chk = torch.tensor([float(x.abs().sum().item()), float(x.sum().item())], dtype=torch.float64,
+                       device="cuda")
+    lo, hi = chk.clone(), chk.clone()
+    dist.all_reduce(lo, op=dist.ReduceOp.MIN)
+    dist.all_reduce(hi, op=dist.ReduceOp.MAX)
+    consistent = bool(torch.equal(lo, hi))
 
-    # ---- the exchange folded into the SpMV (push over peer memory) --------
-    # checked against the NCCL iteration first (same x0, a few steps, own
-    # rows to 1e-12), then timed the same way; any failure (no IPC, a flag
-    # timeout, a mismatch) leaves the NCCL number as the result.
-    push_info = {"used": False}
-    t_push = None
-    try:
-        pu = PushSpMV(n, world, rank, h, k, sparse=True)
-        chk = 3
-        it.cur = 0
-        it.set_x(sp.gen_vector(n, args.seed + 1))
-        for _ in range(chk):
-            it.step(True)
-        pu.set_x(sp.gen_vector(n, args.seed + 1))
-        for _ in range(chk):
-            pu.step()
-        torch.cuda.synchronize()
-        r0_ = rank * it.chunk
-        want = it.bufs[it.cur][r0_: r0_ + it.chunk]
-        got = pu.local_rows()
-        err = float(((got - want).abs().max() / want.abs().max().clamp_min(1e-300)).item())
-        ok = torch.tensor([1.0 if (pu.ok() and err <= 1e-12) else 0.0], device="cuda")
-        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
-        if ok.item() == 1.0:
-            for _ in range(args.warmup):
-                pu.step()
-            dist.barrier()
-            torch.cuda.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            for _ in range(args.steps):
-                pu.step()
-            e1.record()
-            torch.cuda.synchronize()
-            dist.barrier()
-            tp = torch.tensor([e0.elapsed_time(e1) * 1e-3 / args.steps, 0.0 if pu.ok() else 1.0],
-                              dtype=torch.float64, device="cuda")
-            dist.all_reduce(tp, op=dist.ReduceOp.MAX)
-            if tp[1].item() == 0.0:
-                t_push = float(tp[0].item())
-        mask_rows = (int(((pu.mask.to(torch.int32) & ~(1 << rank)) != 0).sum().item())
-                     if pu.mask is not None else it.chunk)
-        push_info = {"used": False, "checked_rel_err": err, "rows_pushed_to_peers": mask_rows,
-                     "ms_per_step": None if t_push is None else t_push * 1e3}
-        pu.close()
-    except Exception as e:  # noqa: BLE001 -- any failure keeps the NCCL path
-        push_info = {"used": False, "error": f"{type(e).__name__}: {e}"[:200]}
-    # ---- NCCL with the interior rows overlapping the all-gather ----------
-    overlap_info = {"used": False}
-    t_over = None
-    try:
-        chunk = block_rows(n, world)
-        rows_here = block_range(n, world, rank)[1] - r0
-        ia, ib = interior_range(lrp, lci, r0, rows_here, chunk)
-        ivec = torch.tensor([ib - ia], dtype=torch.float64, device="cuda")
-        dist.all_reduce(ivec, op=dist.ReduceOp.MIN)
-        if ivec.item() > 0:  # every rank has an interior: worth overlapping
-            parts = []
-            for a_, b_, inner in ((0, ia, False), (ia, ib, True), (ib, chunk, False)):
-                if b_ <= a_:
-                    continue
-                prp = (lrp[a_: b_ + 1] - lrp[a_]).astype(np.int64)
-                pci = np.ascontiguousarray(lci[lrp[a_]: lrp[b_]])
-                pv = np.ascontiguousarray(lv[lrp[a_]: lrp[b_]])
-                hp = sp.Matrix.from_crs_block(b_ - a_, n, r0 + a_, prp, pci, pv)
-                if fmt == "ell-inner":
-                    hp = hp.convert(sp.Format.ELL)
-                parts.append((hp, k, a_, b_, inner))
-            ov = OverlapSpMV(n, world, rank, parts, "cuda")
-            ov.set_x(sp.gen_vector(n, args.seed + 1))
-            for _ in range(args.warmup):
-                ov.step(True)
-            dist.barrier()
-            torch.cuda.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            for _ in range(args.steps):
-                ov.step(True)
-            e1.record()
-            torch.cuda.synchronize()
-            dist.barrier()
-            to = torch.tensor([e0.elapsed_time(e1) * 1e-3 / args.steps], dtype=torch.float64,
-                              device="cuda")
-            dist.all_reduce(to, op=dist.ReduceOp.MAX)
-            t_over = float(to.item())
-            overlap_info = {"used": False, "interior_rows_min": int(ivec.item()),
-                            "ms_per_step": t_over * 1e3}
-        else:
-            overlap_info = {"used": False, "note": "a rank has no interior rows"}
-    except Exception as e:  # noqa: BLE001 -- reported, NCCL result kept
-        overlap_info = {"used": False, "error": f"{type(e).__name__}: {e}"[:200]}
-    del lrp, lci, lv
-
-    if t_push is not None and t_push < t_step:
-        push_info["used"] = True
-        t_step = t_push
-    if t_over is not None and t_over < t_step:
-        push_info["used"] = False
-        overlap_info["used"] = True
-        t_step = t_over
-    # shard bytes (each rank's own kernel, for the per-GPU roofline) and the
-    # whole product's algorithmic bytes -- the same formula as the 1-GPU
-    # bench line, so value(N) / value(1) is the speed-up of one SpMV step
-    b = torch.tensor([bytes_of(fmt)], dtype=torch.float64, device="cuda")
-    dist.all_reduce(b, op=dist.ReduceOp.SUM)
-    shard_bytes = float(b.item())
-    total_bytes = float(spmv_bytes(fmt, n, nnz, nz_global))
-
-    # e2e: the streaming C ABI calls with pinned host x (ncols) and y (local
-    # rows): every step copies its x in and its row block out on every rank
+    # e2e: every step copies x in from pinned host memory on every rank, runs
+    # one iterate step (SpMV + exchange) and copies this rank's block out
     xh = torch.from_numpy(sp.gen_vector(n, args.seed + 1)).pin_memory()
-    yhs = [torch.empty(block_rows(n, world), dtype=torch.float64).pin_memory() for _ in range(2)]
-    pipe = sp.Pipeline(h, k)
-    for i in range(4):
-        pipe.submit(xh.numpy(), yhs[i % 2].numpy())
-    pipe.wait()
+    yh = torch.empty(max(rows, 1), dtype=torch.float64).pin_memory()
+    e2e_steps = max(10, min(args.steps, 100))
     dist.barrier()
     t0 = time.perf_counter()
-    e2e_steps = max(10, min(args.steps, 100))
-    for i in range(e2e_steps):
-        pipe.submit(xh.numpy(), yhs[i % 2].numpy())
-    pipe.wait()
+    for _ in range(e2e_steps):
+        x.copy_(xh, non_blocking=True)
+        comm.iterate(h, k, x.data_ptr(), 1)
+        if rows:
+            yh[:rows].copy_(x[r0:r0 + rows], non_blocking=True)
+    torch.cuda.synchronize()
     te = torch.tensor([(time.perf_counter() - t0) / e2e_steps], dtype=torch.float64,
                       device="cuda")
-    pipe.free()
     dist.all_reduce(te, op=dist.ReduceOp.MAX)
     t_e2e = float(te.item())
 
+    total_bytes = float(spmv_bytes(fmt, n, nnz, nz))
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        try:
+            from oracle.oracle import Ref
+            ref = Ref()
+            rh = ref.gen_baseline(args.config, args.param, 0.0, args.seed)
+            r = cpu_reference_run(ref, rh, n, nnz, nz)
+            for hh in r.pop("handles").values():
+                ref.free(hh)
+            b = r["table"][r["best"]]
+            cpu = {"value": b["gbs"], "unit": "GB/s", "cores": b["lanes"], "kind": "reference",
+                   "sample": (f"reference measure_spmv (warm-up + median of 3) per format on the "
+                              f"same config-{args.config} matrix on rank 0's host; best = "
+                              f"{r['best']} at {b['lanes']} lanes of {r['cores']} cores"),
+                   "cpu_model": r["cpu_model"], "nproc": r["cores"]}
+        except Exception as e:  # reported, never silently replaced
+            cpu = {"value": None, "unit": "GB/s", "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"unavailable: {type(e).__name__}: {e}"[:300]}
     if rank == 0:
-        line = {
-            "metric": ("SpMV GB/s & GFLOP/s per format; CRS→ELL/COO transform time in "
-                       "CRS-SpMV units"),
-            "value": total_bytes / t_step / 1e9, "unit": "GB/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic",
-            "config": {"workload": f"baseline config {args.config}", "n": n, "nnz": nnz,
-                       "format": fmt, "band_count_global": nz_global,
-                       "parallelism": (f"row-block x{world}, " +
-                                       ("exchange pushed from the SpMV epilogue over peer "
-                                        "memory + step flags" if push_info["used"] else
-                                        "NCCL all_gather of x overlapped with the interior "
-                                        "rows" if overlap_info["used"] else
-                                        "NCCL all_gather of x per step")),
-                       "gflops": 2 * nnz / t_step / 1e9},
-            "push_exchange": push_info,
-            "overlap_exchange": overlap_info,
-            "bytes": {"whole_product": total_bytes, "sum_of_shards": shard_bytes},
-            "no_comm": {"ms_per_step": t_local * 1e3,
-                        "value": total_bytes / t_local / 1e9},
-            "e2e": {"value": total_bytes / t_e2e / 1e9, "unit": "GB/s",
-                    "h2d_bytes_per_step": 8 * n * world,
-                    "d2h_bytes_per_step": 8 * block_rows(n, world) * world,
-                    "api": "spmvtk_pipeline_submit/wait per rank (pinned host x, y block)"},
-            "gpu_launches": args.steps,
-            "clocks": clk.summary(),
-        }
         peak, kind = hbm_peak()
-        per_gpu = shard_bytes / world / t_local / 1e9
-        line["roofline"] = {"bound": "hbm", "achieved": per_gpu, "peak": peak, "unit": "GB/s",
-                            "frac": per_gpu / peak, "traffic": None, "peak_kind": kind,
-                            "kernel": fmt, "note": "per GPU, SpMV shard without the exchange"}
+        per_gpu = float(rate.item()) / 1e9
+        line = {
+            "metric": METRIC, "value": total_bytes / t_step / 1e9, "unit": "GB/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config(args.config, args.param, 0.0, args.seed, n, nnz, nz,
+                                      d_mat_g),
+            "format": fmt, "gflops": 2 * nnz / t_step / 1e9,
+            "parallelism": (f"{world} entry-balanced row blocks, x exchanged every step by "
+                            "grouped in-place ncclBroadcast (spmvtk_dist_spmv_iterate)"),
+            "ranks_consistent": consistent,
+            "no_comm": {"ms_per_step": t_local * 1e3, "value": total_bytes / t_local / 1e9},
+            "e2e": {"value": total_bytes / t_e2e / 1e9, "unit": "GB/s",
+                    "h2d_bytes_per_step": 8 * n * world, "d2h_bytes_per_step": 8 * n,
+                    "ms_per_step": t_e2e * 1e3,
+                    "api": "pinned host x copied in on every rank + spmvtk_dist_spmv_iterate "
+                           "(1 step) + own block copied out"},
+            "gpu_launches": int(launches.item()),
+            "clocks": clk.summary(),
+            "roofline": {"bound": "hbm", "achieved": per_gpu, "peak": peak, "unit": "GB/s",
+                         "frac": per_gpu / peak if per_gpu else None, "traffic": None,
+                         "peak_kind": kind, "kernel": fmt,
+                         "note": "per GPU: the slowest rank's shard SpMV (its bytes over its "
+                                 "time) without the exchange"},
+            "cpu_baseline": cpu,
+        }
         print(json.dumps(line))
+    for name, (hh, _) in handles.items():
+        if name != "crs":
+            hh.free()
+    shard.free()
+    comm.free()
     dist.barrier()
     dist.destroy_process_group()
     return 0

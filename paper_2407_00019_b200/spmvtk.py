@@ -198,6 +198,16 @@ SIGNATURES = {
     "spmvtk_read_matrix_market_host": (C.c_int, [C.c_char_p, _PP, C.POINTER(_i64),
                                                  C.POINTER(_i64)]),
     "spmvtk_host_crs_export": (C.c_int, [_P, _P, _P, _P, C.c_int]),
+    "spmvtk_dist_unique_id": (C.c_int, [_P]),
+    "spmvtk_dist_init": (C.c_int, [C.c_int, C.c_int, _P, _PP]),
+    "spmvtk_dist_free": (None, [_P]),
+    "spmvtk_partition_rows": (C.c_int, [_P, _i64, C.c_int, _P]),
+    "spmvtk_matrix_distribute": (C.c_int, [_P, _i64, _P, _P, _P, C.c_int, C.c_int, _PP]),
+    "spmvtk_gen_baseline_shard_host": (C.c_int, [C.c_int, _i64, _d, _u64, C.c_int, C.c_int, _PP,
+                                                 C.POINTER(_i64), C.POINTER(_i64),
+                                                 C.POINTER(_i64)]),
+    "spmvtk_gen_baseline_shard": (C.c_int, [_P, C.c_int, _i64, _d, _u64, _PP]),
+    "spmvtk_dist_spmv_iterate": (C.c_int, [_P, _P, C.c_int, _P, _i64, _pd]),
     "spmvtk_host_crs_free": (None, [_P]),
     "spmvtk_matrix_from_host_crs": (C.c_int, [_P, _PP]),
     "spmvtk_conversion_bytes": (C.c_int, [_P, C.c_int, C.POINTER(_u64), C.POINTER(_u64)]),
@@ -688,3 +698,86 @@ def gen_vector(n: int, seed: int) -> np.ndarray:
     out = np.empty(n, dtype=np.float64)
     _check(load_library().spmvtk_gen_vector(n, seed, _ptr(out)))
     return out
+
+
+DIST_ID_BYTES = 128
+
+
+def partition_rows(row_ptr, world: int) -> np.ndarray:
+    """Entry-balanced contiguous row blocks (spmvtk_partition_rows): begin[world+1]."""
+    rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+    out = np.empty(world + 1, np.int64)
+    _check(load_library().spmvtk_partition_rows(_ptr(rp), rp.shape[0] - 1, world, _ptr(out)))
+    return out
+
+
+def gen_baseline_shard_host(config: int, param: int, dparam: float, seed: int, rank: int,
+                            world: int) -> "HostCrs":
+    """This rank's row block of a BASELINE workload, generated alone (host)."""
+    self = HostCrs.__new__(HostCrs)
+    self._lib = load_library()
+    self._h = C.c_void_p()
+    rows, off, ncols = _i64(), _i64(), _i64()
+    _check(self._lib.spmvtk_gen_baseline_shard_host(config, param, float(dparam), seed, rank, world,
+                                                    C.byref(self._h), C.byref(rows), C.byref(off),
+                                                    C.byref(ncols)))
+    self.n = rows.value
+    self.row_offset, self.ncols = off.value, ncols.value
+    rp = np.empty(self.n + 1, np.int64)
+    _check(self._lib.spmvtk_host_crs_export(self._h, _ptr(rp), None, None, 0))
+    self.nnz = int(rp[-1])
+    return self
+
+
+class Dist:
+    """spmvtk_dist: one rank of an NCCL communicator (one process per GPU)."""
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (C.c_ubyte * DIST_ID_BYTES)()
+        _check(load_library().spmvtk_dist_unique_id(buf))
+        return bytes(buf)
+
+    def __init__(self, rank: int, world: int, uid: bytes):
+        self._lib = load_library()
+        self.rank, self.world = rank, world
+        buf = (C.c_ubyte * DIST_ID_BYTES).from_buffer_copy(uid)
+        h = C.c_void_p()
+        _check(self._lib.spmvtk_dist_init(rank, world, buf, C.byref(h)))
+        self._h = h
+
+    @property
+    def handle(self):
+        return self._h
+
+    def shard(self, config: int, param: int, dparam: float = 0.0, seed: int = 2407) -> "Matrix":
+        """This rank's shard of a BASELINE workload (generated shard-only)."""
+        return Matrix._make(self._lib.spmvtk_gen_baseline_shard, self._h, config, param,
+                            float(dparam), seed)
+
+    def distribute(self, n: int, row_ptr, col_idx, values, index_base: int = 0) -> "Matrix":
+        """This rank's shard of a global host CRS (entry-balanced row blocks)."""
+        rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+        ci = np.ascontiguousarray(col_idx, dtype=np.int64)
+        v = np.ascontiguousarray(values, dtype=np.float64)
+        return Matrix._make(self._lib.spmvtk_matrix_distribute, self._h, n, _ptr(rp), _ptr(ci),
+                            _ptr(v), 8, index_base)
+
+    def iterate(self, shard: "Matrix", kernel: "Kernel", x_ptr: int, steps: int) -> float:
+        """x <- A^steps x on the device vector at x_ptr (every rank); returns
+        this rank's device seconds per step."""
+        sec = C.c_double()
+        _check(self._lib.spmvtk_dist_spmv_iterate(self._h, shard.handle, int(kernel),
+                                                  C.c_void_p(x_ptr), steps, C.byref(sec)))
+        return sec.value
+
+    def free(self) -> None:
+        if self._h:
+            self._lib.spmvtk_dist_free(self._h)
+            self._h = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.free()
+        except Exception:
+            pass
