@@ -269,6 +269,12 @@ spmvtk_status spmvtk_read_matrix_market_host(const char* path, spmvtk_host_crs**
 /* Uploads a host CRS (from spmvtk_gen_baseline_host) into a device handle. */
 spmvtk_status spmvtk_matrix_from_host_crs(const spmvtk_host_crs* h, spmvtk_matrix** out);
 
+/* Bands [k0, k1) (0-based) of a band-major ELL handle, in the reference
+ * layout: (k1-k0)*n values and int64 column indices in index_base (either
+ * output may be NULL) -- to stream an ELL too large for one host copy. */
+spmvtk_status spmvtk_matrix_copy_ell_bands(const spmvtk_matrix* m, int64_t k0, int64_t k1,
+                                           double* values, int64_t* col_idx, int index_base);
+
 /* ---- multi-GPU: row-block shards, one process per GPU, NCCL -------------
  * The rows are cut into `world` contiguous entry-balanced blocks
  * (spmvtk_partition_rows: rank k starts at the first row whose start reaches

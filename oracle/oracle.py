@@ -69,6 +69,7 @@ class Port:
             getattr(L, f).argtypes = [_i64, _P, _P, _P, _P, _P, _P]
         L.or_crs_to_ell.argtypes = [_i64, _P, _P, _P, C.c_uint64, _i64, _P, _P, _P]
         L.or_ell_to_rowmajor.argtypes = [_i64, _i64, _P, _P, _P, _P]
+        L.or_crs_to_ell_bands.argtypes = [_i64, _P, _P, _P, _i64, _i64, _P, _P]
         L.or_partition_range.argtypes = [_i64, C.c_int, _P, _P]
         L.or_reduce_partials.argtypes = [_i64, C.c_int, _P, _P]
         L.or_spmv_crs.argtypes = [_i64, _P, _P, _P, _P, _P]
@@ -135,6 +136,14 @@ class Port:
             est = self.estimate_ell_bytes(n, rp)
             raise MemoryError(f"ELL footprint estimate {est} bytes exceeds limit {max_bytes}")
         return bc, vv, cc, cnt
+
+    def crs_to_ell_bands(self, n, row_ptr, col_idx, values, k0, k1):
+        """Bands [k0, k1) (1-based) of crs_to_ell: ((k1-k0)*n values, columns)."""
+        rp, ci, v = _i(row_ptr), _i(col_idx), _f(values)
+        vv = np.empty((k1 - k0) * n)
+        cc = np.empty((k1 - k0) * n, np.int64)
+        self.lib.or_crs_to_ell_bands(n, _p(rp), _p(ci), _p(v), k0, k1, _p(vv), _p(cc))
+        return vv, cc
 
     def ell_to_rowmajor(self, n, bc, values, col_idx):
         v, c = _f(values), _i(col_idx)

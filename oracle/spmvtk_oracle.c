@@ -133,6 +133,29 @@ int or_crs_to_ell(idx_t n, const idx_t* row_ptr, const idx_t* col_idx,
   return 0;
 }
 
+/* Bands [k0, k1) (1-based k) of crs_to_ell's band-major arrays, the same
+ * fill as convert.cpp:101-113 restricted to those bands: out has
+ * (k1 - k0) * n slots, band k at offset (k - k0) * n.  Lets a test compare
+ * an ELL too large for host memory band by band. */
+void or_crs_to_ell_bands(idx_t n, const idx_t* row_ptr, const idx_t* col_idx,
+                         const double* val, idx_t k0, idx_t k1, double* out_val,
+                         idx_t* out_col) {
+  for (idx_t i = 1; i <= n; ++i) {
+    idx_t r = row_ptr[i] - row_ptr[i - 1];
+    for (idx_t k = k0; k < k1; ++k) {
+      size_t s = (size_t)(n * (k - k0) + (i - 1));
+      if (k <= r) {
+        size_t p = (size_t)(row_ptr[i - 1] - 1 + k - 1);
+        out_val[s] = val[p];
+        out_col[s] = col_idx[p];
+      } else {
+        out_val[s] = 0.0;
+        out_col[s] = i;
+      }
+    }
+  }
+}
+
 /* Row-major ELL has no reference counterpart: its oracle is
  * the transpose of the band-major arrays, same padding rules. */
 void or_ell_to_rowmajor(idx_t n, idx_t band_count, const double* bm_val,

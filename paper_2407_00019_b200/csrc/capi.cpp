@@ -725,6 +725,16 @@ spmvtk_status spmvtk_matrix_from_host_crs(const spmvtk_host_crs* h, spmvtk_matri
   });
 }
 
+spmvtk_status spmvtk_matrix_copy_ell_bands(const spmvtk_matrix* m, int64_t k0, int64_t k1,
+                                           double* values, int64_t* col_idx, int index_base) {
+  return guarded([&] {
+    need(m);
+    if (index_base != 0 && index_base != 1)
+      throw Error(ErrorCode::InvalidArgument, "index_base must be 0 or 1");
+    dev::copy_ell_bands(*m, k0, k1, values, col_idx, index_base);
+  });
+}
+
 // ---- multi-GPU (dist.cpp) ---------------------------------------------------
 spmvtk_status spmvtk_dist_unique_id(unsigned char* id) {
   return guarded([&] {

@@ -809,4 +809,30 @@ std::int64_t copy_array(const Matrix& m, spmvtk_array which, void* dst, std::int
   return len;
 }
 
+void copy_ell_bands(const Matrix& m, std::int64_t k0, std::int64_t k1, double* values,
+                    std::int64_t* col_idx, int index_base) {
+  if (m.format != SPMVTK_FORMAT_ELL)
+    throw Error(ErrorCode::InvalidArgument, "kernel requires an ELL handle");
+  if (k0 < 0 || k1 > m.band_count || k0 > k1)
+    throw Error(ErrorCode::InvalidArgument, "band range out of bounds");
+  const std::int64_t bands = k1 - k0, len = bands * m.n;
+  if (len == 0) return;
+  cudaStream_t st = rt::stream();
+  if (values)
+    rt::check(cudaMemcpy2DAsync(values, m.n * 8, m.val.get() + k0 * m.ld, m.ld * 8, m.n * 8, bands,
+                                cudaMemcpyDeviceToHost, st),
+              "ELL band export");
+  if (col_idx) {
+    DevArray<std::int32_t> compact(static_cast<std::size_t>(len), "ELL band export");
+    rt::check(cudaMemcpy2DAsync(compact.get(), m.n * 4, m.col.get() + k0 * m.ld, m.ld * 4, m.n * 4,
+                                bands, cudaMemcpyDeviceToDevice, st),
+              "ELL band export");
+    DevArray<std::int64_t> wide(static_cast<std::size_t>(len), "ELL band export");
+    rt::check_launch(spmvtk_k_widen_index(compact.get(), wide.get(), len, index_base, st),
+                     "ELL band export");
+    rt::copy_to_host(col_idx, wide.get(), static_cast<std::size_t>(len) * 8);
+  }
+  rt::sync();
+}
+
 }  // namespace spmvtk::dev

@@ -123,6 +123,10 @@ void spmv_device_rows(const Matrix& m, spmvtk_kernel kernel, const double* x, do
 std::int64_t copy_array(const Matrix& m, spmvtk_array which, void* dst, std::int64_t capacity,
                         int index_width, int index_base);
 std::int64_t device_array(const Matrix& m, spmvtk_array which, void** ptr);
+// Bands [k0, k1) of a band-major ELL handle in the reference layout
+// ((k1-k0) * n slots; columns widened to int64 in index_base).
+void copy_ell_bands(const Matrix& m, std::int64_t k0, std::int64_t k1, double* values,
+                    std::int64_t* col_idx, int index_base);
 
 const char* kernel_label(spmvtk_kernel k);
 

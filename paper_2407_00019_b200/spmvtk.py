@@ -198,6 +198,7 @@ SIGNATURES = {
     "spmvtk_read_matrix_market_host": (C.c_int, [C.c_char_p, _PP, C.POINTER(_i64),
                                                  C.POINTER(_i64)]),
     "spmvtk_host_crs_export": (C.c_int, [_P, _P, _P, _P, C.c_int]),
+    "spmvtk_matrix_copy_ell_bands": (C.c_int, [_P, _i64, _i64, _P, _P, C.c_int]),
     "spmvtk_dist_unique_id": (C.c_int, [_P]),
     "spmvtk_dist_init": (C.c_int, [C.c_int, C.c_int, _P, _PP]),
     "spmvtk_dist_free": (None, [_P]),
@@ -443,6 +444,15 @@ class Matrix:
         _check(self._lib.spmvtk_spmv(self._h, int(kernel), _ptr(xs), xs.shape[0], lanes,
                                      _ptr(y), C.byref(el)))
         return y, el.value
+
+    def ell_bands(self, k0: int, k1: int, index_base: int = 1):
+        """Bands [k0, k1) (0-based) of a band-major ELL: (values, columns)."""
+        n = self.describe().n
+        v = np.empty((k1 - k0) * n)
+        c = np.empty((k1 - k0) * n, np.int64)
+        _check(self._lib.spmvtk_matrix_copy_ell_bands(self._h, k0, k1, _ptr(v), _ptr(c),
+                                                      index_base))
+        return v, c
 
     def spmv_device(self, kernel: Kernel, x_ptr: int, y_ptr: int) -> None:
         _check(self._lib.spmvtk_spmv_device(self._h, int(kernel), C.c_void_p(x_ptr),

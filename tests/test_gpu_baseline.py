@@ -5,10 +5,14 @@
   1e-12 max-norm relative, D_mat as measured in SURVEY.md §0.15;
 * config 4 (power-law, n = 2^22): statistics, the ELL memory guard refusal
   (≈160 GB in GPU layout), CRS/COO parity, the CCS bit-exact at full size;
-* config 5 (D_mat sweep) at reduced n for oracle parity, and at full size
-  for D in {0, 1, 2}: size-independent properties (ELL and COO SpMV equal
-  CRS SpMV to 1e-12, band count = max row length, exported row counts = row
-  lengths, D_mat close to the target).
+* config 4 also: COO-row and COO-col arrays bit-exact at full size;
+* configs 1-3: row-major ELL arrays bit-exact (the transpose of the port's);
+* config 5 (D_mat sweep) at reduced n for oracle parity, and at FULL size
+  for D in {0, 0.5, 1, 2}: CCS, COO-col and COO-row arrays bit-exact against
+  the port, and the ELL (up to ~35 GB) compared band by band against the
+  port's band-range ELL, streamed so neither side is materialised whole;
+  plus size-independent properties (ELL and COO SpMV equal CRS SpMV to
+  1e-12, band count = max row length, D_mat close to the target).
 """
 import numpy as np
 import pytest
@@ -74,6 +78,14 @@ def check_all(sp, port, h, n, rp, ci, v, x, ell=True):
         del ev, ec
         er = m.convert(sp.Format.ELL_ROWMAJOR)
         assert max_rel_error(er.spmv(x, sp.Kernel.ELL_ROWMAJOR)[0], want) <= TOL
+        # row-major arrays = the transpose of the port's band-major ones
+        bc, ev, ec, _ = port.crs_to_ell(n, rp, ci, v)
+        rv, rc = port.ell_to_rowmajor(n, bc, ev, ec)
+        del ev, ec
+        assert er.describe().band_count == bc
+        assert er.array(sp.Array.VALUES).tobytes() == rv.tobytes()
+        assert np.array_equal(er.array(sp.Array.COL_IDX), rc)
+        del rv, rc
         er.free()
     return m
 
@@ -128,7 +140,73 @@ def test_config_4_power_law(gpu, port):
     del cp, ri, cv
     cc = m.convert(sp.Format.COO_COL)
     assert max_rel_error(cc.spmv(x, sp.Kernel.COO_COL_OUTER)[0], want) <= TOL
+    # COO-col arrays at full size
+    kr, kc, kv = port.crs_to_coo_col(n, rp, ci, v)
+    assert np.array_equal(cc.array(sp.Array.ROW_IDX), kr)
+    assert np.array_equal(cc.array(sp.Array.COL_IDX), kc)
+    assert cc.array(sp.Array.VALUES).tobytes() == kv.tobytes()
+    del kr, kc, kv
     cc.free()
+    # COO-row arrays at full size
+    r, c, vv = port.crs_to_coo_row(n, rp, ci, v)
+    coo = m.convert(sp.Format.COO_ROW)
+    assert np.array_equal(coo.array(sp.Array.ROW_IDX), r)
+    assert np.array_equal(coo.array(sp.Array.COL_IDX), c)
+    assert coo.array(sp.Array.VALUES).tobytes() == vv.tobytes()
+    coo.free()
+
+
+def check_ell_bands(sp, port, m, n, rp, ci, v, chunk=16):
+    """The band-major ELL compared band by band with the port's band-range
+    ELL (or_crs_to_ell_bands): an ELL of tens of GB is never whole on the
+    host."""
+    e = m.convert(sp.Format.ELL)
+    bc = e.describe().band_count
+    assert bc == port.max_row(n, rp)
+    for k0 in range(0, bc, chunk):
+        k1 = min(bc, k0 + chunk)
+        gv, gc = e.ell_bands(k0, k1, index_base=1)
+        wv, wc = port.crs_to_ell_bands(n, rp, ci, v, k0 + 1, k1 + 1)
+        assert gv.tobytes() == wv.tobytes(), (k0, k1)
+        assert np.array_equal(gc, wc), (k0, k1)
+    cnt = e.array(sp.Array.ROW_ENTRY_COUNT)
+    assert np.array_equal(cnt, np.diff(rp))
+    e.free()
+    return bc
+
+
+@pytest.mark.parametrize("d", [0.0, 0.5, 1.0, 2.0])
+def test_config_5_full_size_parity(gpu, port, d):
+    """Config 5 at full size (n = 2^21, ~67M entries): every transform array
+    against the port -- CCS, COO-col, COO-row in full, ELL band by band."""
+    sp = gpu
+    h, rp, ci, v = host_arrays(sp, 5, 1 << 21, d)
+    n = h.n
+    m = h.upload()
+    cp, ri, cv = port.crs_to_ccs(n, rp, ci, v)
+    ccs = m.convert(sp.Format.CCS)
+    assert np.array_equal(ccs.array(sp.Array.POINTER), cp)
+    assert np.array_equal(ccs.array(sp.Array.ROW_IDX), ri)
+    assert ccs.array(sp.Array.VALUES).tobytes() == cv.tobytes()
+    ccs.free()
+    del cp, ri, cv
+    kr, kc, kv = port.crs_to_coo_col(n, rp, ci, v)
+    cc = m.convert(sp.Format.COO_COL)
+    assert np.array_equal(cc.array(sp.Array.ROW_IDX), kr)
+    assert np.array_equal(cc.array(sp.Array.COL_IDX), kc)
+    assert cc.array(sp.Array.VALUES).tobytes() == kv.tobytes()
+    cc.free()
+    del kr, kc, kv
+    r, c, vv = port.crs_to_coo_row(n, rp, ci, v)
+    coo = m.convert(sp.Format.COO_ROW)
+    assert np.array_equal(coo.array(sp.Array.ROW_IDX), r)
+    assert np.array_equal(coo.array(sp.Array.COL_IDX), c)
+    assert coo.array(sp.Array.VALUES).tobytes() == vv.tobytes()
+    coo.free()
+    del r, c, vv
+    check_ell_bands(sp, port, m, n, rp, ci, v)
+    m.free()
+    h.free()
 
 
 @pytest.mark.parametrize("d", [0.0, 0.3, 1.0, 2.0])

@@ -221,3 +221,19 @@ def test_reference_arm_generator_matches_the_product_generator():
         ref.free(h)
         hc.free()
     assert np.array_equal(ref.gen_vector(1000, 5), sp.gen_vector(1000, 5))
+
+
+def test_ell_bands_are_slices_of_crs_to_ell(port, golden):
+    """or_crs_to_ell_bands (band-range ELL for arrays too large to hold at
+    once) equals the band slices of the pinned crs_to_ell."""
+    for name in sorted(k for k in golden.files if k.endswith("_row_ptr"))[:8]:
+        pre = name[: -len("_row_ptr")]
+        rp, ci, v = golden[pre + "_row_ptr"], golden[pre + "_col_idx"], golden[pre + "_values"]
+        n = rp.shape[0] - 1
+        bc, ev, ec, _ = port.crs_to_ell(n, rp, ci, v)
+        for k0, k1 in ((1, bc + 1), (1, 2), (max(1, bc // 2), bc + 1)):
+            if k1 <= k0:
+                continue
+            vv, cc = port.crs_to_ell_bands(n, rp, ci, v, k0, k1)
+            assert vv.tobytes() == ev[(k0 - 1) * n:(k1 - 1) * n].tobytes()
+            np.testing.assert_array_equal(cc, ec[(k0 - 1) * n:(k1 - 1) * n])
