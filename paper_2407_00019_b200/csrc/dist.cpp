@@ -9,11 +9,14 @@
 // GPU with no communication); the only exchange is the iterate's x: after
 // each SpMV every rank's block of x_{t+1} is broadcast to the others
 // (grouped ncclBroadcast, in place: an all-gather with per-rank counts).
-#include <nccl.h>
+#include <dlfcn.h>
+#include <nccl.h>  // types only: the library is loaded at run time (below)
 
 #include <cstring>
+#include <mutex>
 #include <memory>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "generators.hpp"
@@ -25,17 +28,60 @@
 struct spmvtk_dist {
   ncclComm_t comm = nullptr;
   int rank = 0, world = 1, device = 0;
-  ~spmvtk_dist() {
-    if (comm) ncclCommDestroy(comm);
-  }
+  ~spmvtk_dist();
 };
 
 namespace spmvtk::dist {
 
 namespace {
+// NCCL is resolved at run time, not linked: a process that already holds an
+// NCCL (PyTorch's, loaded first) must keep using that one -- two copies under
+// one soname break whichever loads second -- and the library must load in
+// processes that never touch multi-GPU.  Order: the NCCL already in the
+// process, else libnccl.so.2 from the loader path.
+struct Nccl {
+  decltype(&::ncclGetUniqueId) getUniqueId = nullptr;
+  decltype(&::ncclCommInitRank) commInitRank = nullptr;
+  decltype(&::ncclCommDestroy) commDestroy = nullptr;
+  decltype(&::ncclAllGather) allGather = nullptr;
+  decltype(&::ncclBroadcast) broadcast = nullptr;
+  decltype(&::ncclGroupStart) groupStart = nullptr;
+  decltype(&::ncclGroupEnd) groupEnd = nullptr;
+  decltype(&::ncclGetErrorString) getErrorString = nullptr;
+};
+
+const Nccl& nccl() {
+  static Nccl lib;
+  static std::once_flag once;
+  static std::string error;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+    if (!h) {
+      error = std::string("NCCL not found: ") + dlerror();
+      return;
+    }
+    auto sym = [&](auto& fn, const char* name) {
+      fn = reinterpret_cast<std::remove_reference_t<decltype(fn)>>(dlsym(h, name));
+      if (!fn && error.empty()) error = std::string("NCCL symbol missing: ") + name;
+    };
+    sym(lib.getUniqueId, "ncclGetUniqueId");
+    sym(lib.commInitRank, "ncclCommInitRank");
+    sym(lib.commDestroy, "ncclCommDestroy");
+    sym(lib.allGather, "ncclAllGather");
+    sym(lib.broadcast, "ncclBroadcast");
+    sym(lib.groupStart, "ncclGroupStart");
+    sym(lib.groupEnd, "ncclGroupEnd");
+    sym(lib.getErrorString, "ncclGetErrorString");
+  });
+  if (!error.empty()) throw Error(ErrorCode::Validation, error);
+  return lib;
+}
+
 void nccl_check(ncclResult_t r, const char* what) {
   if (r == ncclSuccess) return;
-  throw Error(ErrorCode::Validation, std::string(what) + ": NCCL error " + ncclGetErrorString(r));
+  throw Error(ErrorCode::Validation,
+              std::string(what) + ": NCCL error " + nccl().getErrorString(r));
 }
 }  // namespace
 
@@ -50,17 +96,20 @@ spmvtk_dist* init(int rank, int world, const unsigned char* id) {
   d->rank = rank;
   d->world = world;
   rt::check(cudaGetDevice(&d->device), "cudaGetDevice");
-  nccl_check(ncclCommInitRank(&d->comm, world, uid, rank), "ncclCommInitRank");
+  nccl_check(nccl().commInitRank(&d->comm, world, uid, rank), "ncclCommInitRank");
   return d.release();
 }
 
 void destroy(spmvtk_dist* d) { delete d; }
+void release(ncclComm_t c) {
+  if (c) nccl().commDestroy(c);
+}
 int rank_of(const spmvtk_dist& d) { return d.rank; }
 int world_of(const spmvtk_dist& d) { return d.world; }
 
 void unique_id(unsigned char* out) {
   ncclUniqueId uid;
-  nccl_check(ncclGetUniqueId(&uid), "ncclGetUniqueId");
+  nccl_check(nccl().getUniqueId(&uid), "ncclGetUniqueId");
   std::memcpy(out, &uid, sizeof(uid));
 }
 
@@ -70,7 +119,7 @@ std::vector<std::int64_t> row_blocks(const spmvtk_dist& d, const dev::Matrix& sh
                                                          "row blocks");
   const std::int64_t h[2] = {shard.row_offset, shard.n};
   rt::copy_to_device(mine.get(), h, sizeof(h));
-  nccl_check(ncclAllGather(mine.get(), all.get(), 2, ncclInt64, d.comm, rt::stream()),
+  nccl_check(nccl().allGather(mine.get(), all.get(), 2, ncclInt64, d.comm, rt::stream()),
              "row-block exchange");
   std::vector<std::int64_t> ha(2 * static_cast<std::size_t>(d.world));
   rt::copy_to_host(ha.data(), all.get(), ha.size() * sizeof(std::int64_t));
@@ -101,16 +150,16 @@ double iterate(const spmvtk_dist& d, const dev::Matrix& shard, spmvtk_kernel ker
   double* cur = x;
   double* nxt = other.get();
   auto exchange = [&](double* buf) {
-    nccl_check(ncclGroupStart(), "ncclGroupStart");
+    nccl_check(nccl().groupStart(), "ncclGroupStart");
     for (int r = 0; r < d.world; ++r) {
       const std::int64_t b0 = begin[static_cast<std::size_t>(r)],
                          cnt = begin[static_cast<std::size_t>(r) + 1] - b0;
       if (cnt > 0)
-        nccl_check(ncclBroadcast(buf + b0, buf + b0, static_cast<std::size_t>(cnt), ncclDouble, r,
+        nccl_check(nccl().broadcast(buf + b0, buf + b0, static_cast<std::size_t>(cnt), ncclDouble, r,
                                  d.comm, st),
                    "x exchange");
     }
-    nccl_check(ncclGroupEnd(), "ncclGroupEnd");
+    nccl_check(nccl().groupEnd(), "ncclGroupEnd");
   };
   rt::EventTimer timer;
   timer.start();
@@ -130,3 +179,5 @@ double iterate(const spmvtk_dist& d, const dev::Matrix& shard, spmvtk_kernel ker
 }
 
 }  // namespace spmvtk::dist
+
+spmvtk_dist::~spmvtk_dist() { spmvtk::dist::release(comm); }
