@@ -2,6 +2,9 @@
 #include "matrix.hpp"
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <climits>
 #include <cstring>
 #include <memory>
@@ -415,7 +418,10 @@ Matrix* convert(const Matrix& a, spmvtk_format to, std::uint64_t max_bytes) {
       // convert.cpp:81-115: guard, band_count = max row, padded scatter.
       // The max row comes from a fresh GPU reduction (as the reference
       // recomputes it), never from a cache.
-      rt::Moments mo = rt::row_moments(a.ptr.get(), n);
+      // band_count = the max row, from the handle's exact row moments
+      // (reduced on the GPU when the handle was built; the handle is
+      // immutable, so no reduction or host round trip on this path)
+      rt::Moments mo = crs_moments(a);
       if (max_bytes != 0) {
         std::uint64_t est = static_cast<std::uint64_t>(n) * mo.max * 16ull;
         if (est > max_bytes)
@@ -432,9 +438,15 @@ Matrix* convert(const Matrix& a, spmvtk_format to, std::uint64_t max_bytes) {
       m->ld = cm ? round_up(n, 32) : n;
       const std::size_t slots =
           static_cast<std::size_t>(cm ? m->ld : n) * static_cast<std::size_t>(nz);
-      m->val.reset(slots, "ELL values");
-      m->col.reset(slots, "ELL col_idx");
-      m->count.reset(n, "ELL row_entry_count");
+      // values | col_idx | row_entry_count in one allocation
+      const std::size_t vbytes = (slots * 8 + 255) & ~std::size_t(255);
+      const std::size_t cbytes = (slots * 4 + 255) & ~std::size_t(255);
+      m->block.reset(vbytes + cbytes + static_cast<std::size_t>(n) * 4, "ELL arrays");
+      unsigned char* base = m->block.get();
+      m->val.view(reinterpret_cast<double*>(base), slots);
+      m->col.view(reinterpret_cast<std::int32_t*>(base + vbytes), slots);
+      m->count.view(reinterpret_cast<std::int32_t*>(base + vbytes + cbytes),
+                    static_cast<std::size_t>(n));
       cudaStream_t st = rt::stream();
       if (cm)
         rt::check_launch(spmvtk_k_crs_to_ell_cm(n, nz, m->ld, a.ptr.get(), a.col.get(),
@@ -525,7 +537,6 @@ double transform_kernel_seconds(const Matrix& a, spmvtk_format to, int repeats) 
     colptr.reset(n + 1, "CCS col_ptr");
     scratch.reset(spmvtk_k_ccs_scratch_bytes(n, nnz), "CCS scratch");
   }
-  DevArray<unsigned long long> acc(3, "row statistics");
   auto once = [&] {
     switch (to) {
       case SPMVTK_FORMAT_CRS:
@@ -546,7 +557,6 @@ double transform_kernel_seconds(const Matrix& a, spmvtk_format to, int repeats) 
                    scratch.get(), st);
         break;
       case SPMVTK_FORMAT_ELL:
-        rt::check_launch(spmvtk_k_row_stats(a.ptr.get(), n, acc.get(), st), "row stats");
         rt::check_launch(spmvtk_k_crs_to_ell_cm(n, out->band_count, out->ld, a.ptr.get(),
                                                 a.col.get(), a.val.get(), out->val.get(),
                                                 out->col.get(), out->count.get(), a.row_offset,
@@ -554,7 +564,6 @@ double transform_kernel_seconds(const Matrix& a, spmvtk_format to, int repeats) 
                          "CRS->ELL");
         break;
       case SPMVTK_FORMAT_ELL_ROWMAJOR:
-        rt::check_launch(spmvtk_k_row_stats(a.ptr.get(), n, acc.get(), st), "row stats");
         rt::check_launch(spmvtk_k_crs_to_ell_rm(n, out->band_count, a.ptr.get(), a.col.get(),
                                                 a.val.get(), out->val.get(), out->col.get(),
                                                 out->count.get(), a.row_offset, st),

@@ -32,6 +32,9 @@ struct spmvtk_matrix {
   spmvtk::rt::DevArray<std::int32_t> row;    // COO / CCS row indices
   spmvtk::rt::DevArray<std::int32_t> col;    // CRS / COO / ELL column indices
   spmvtk::rt::DevArray<std::int32_t> count;  // ELL row_entry_count
+  // one allocation holding several of the arrays above (they are views into
+  // it); declared after them so it is released last
+  spmvtk::rt::DevArray<unsigned char> block;
   std::int32_t band_count = 0;               // ELL
   std::int64_t ld = 0;                       // ELL band-major leading dim
 

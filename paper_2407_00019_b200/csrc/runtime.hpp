@@ -45,12 +45,14 @@ class DevArray {
   explicit DevArray(std::size_t count, const char* what = "device buffer") { reset(count, what); }
   DevArray(const DevArray&) = delete;
   DevArray& operator=(const DevArray&) = delete;
-  DevArray(DevArray&& o) noexcept : p_(std::exchange(o.p_, nullptr)), n_(std::exchange(o.n_, 0)) {}
+  DevArray(DevArray&& o) noexcept
+      : p_(std::exchange(o.p_, nullptr)), n_(std::exchange(o.n_, 0)), own_(o.own_) {}
   DevArray& operator=(DevArray&& o) noexcept {
     if (this != &o) {
       release();
       p_ = std::exchange(o.p_, nullptr);
       n_ = std::exchange(o.n_, 0);
+      own_ = o.own_;
     }
     return *this;
   }
@@ -62,9 +64,18 @@ class DevArray {
     n_ = count;
   }
   void release() {
-    if (p_) free_bytes(p_);
+    if (p_ && own_) free_bytes(p_);
     p_ = nullptr;
     n_ = 0;
+    own_ = true;
+  }
+  // A non-owning view into another buffer (e.g. a slice of one allocation
+  // that holds several arrays of a handle); the owner must outlive it.
+  void view(T* p, std::size_t count) {
+    release();
+    p_ = p;
+    n_ = count;
+    own_ = false;
   }
   T* get() const { return p_; }
   std::size_t size() const { return n_; }
@@ -73,6 +84,7 @@ class DevArray {
  private:
   T* p_ = nullptr;
   std::size_t n_ = 0;
+  bool own_ = true;
 };
 
 // Exact integer moments of the row lengths, from the GPU reduction.

@@ -1,8 +1,12 @@
-"""Breaks down t_trans of CRS->ELL (config 2): wall clock of the public
-convert call vs the row-statistics round trip alone vs the kernels alone."""
+"""Breaks down t_trans of CRS->ELL: the library's own measure_transformation
+timing (spmvtk_matrix_convert_timed: device synchronised, wall clock around
+the conversion) against the kernels alone, per config.
+
+    SPMVTK_TRACE_ELL=1 python tools/ttrans_probe.py --configs 1,2
+"""
+import argparse
 import os
 import sys
-import time
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
@@ -10,30 +14,25 @@ import torch  # noqa: E402
 
 from paper_2407_00019_b200 import spmvtk as sp  # noqa: E402
 
+ap = argparse.ArgumentParser()
+ap.add_argument("--configs", default="1,2")
+ap.add_argument("--reps", type=int, default=15)
+a = ap.parse_args()
+PARAM = {1: 256, 2: 1 << 20, 3: 128, 4: 1 << 22, 5: 1 << 21}
 sp.set_stream(torch.cuda.current_stream().cuda_stream)
 sp.reserve_device_memory(8 << 30)
-m = sp.HostCrs(2, 1 << 20).upload()
-for _ in range(3):
-    m.convert(sp.Format.ELL).free()
-
-
-def wall(fn, reps=20):
-    ts = []
-    for _ in range(reps):
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        r = fn()
-        torch.cuda.synchronize()
-        ts.append(time.perf_counter() - t0)
-        if r is not None and hasattr(r, "free"):
-            r.free()
-    ts.sort()
-    return ts[len(ts) // 2] * 1e6
-
-
-print(f"convert(ELL) wall      {wall(lambda: m.convert(sp.Format.ELL)):8.1f} us")
-print(f"row_stats() wall       {wall(lambda: m.row_stats()):8.1f} us")
-print(f"empty sync wall        {wall(lambda: None):8.1f} us")
-print(f"ELL kernels (events)   {m.transform_kernel_seconds(sp.Format.ELL, 15) * 1e6:8.1f} us")
-print(f"convert(COO_ROW) wall  {wall(lambda: m.convert(sp.Format.COO_ROW)):8.1f} us")
-print(f"COO_ROW kernel         {m.transform_kernel_seconds(sp.Format.COO_ROW, 15) * 1e6:8.1f} us")
+for cfg in [int(c) for c in a.configs.split(",")]:
+    m = sp.HostCrs(cfg, PARAM[cfg]).upload()
+    for fmt in (sp.Format.ELL, sp.Format.ELL_ROWMAJOR, sp.Format.COO_ROW):
+        for _ in range(3):
+            m.convert(fmt).free()
+        ts = []
+        for _ in range(a.reps):
+            h, t = m.convert_timed(fmt)
+            ts.append(t)
+            h.free()
+        ts.sort()
+        k = m.transform_kernel_seconds(fmt, a.reps)
+        print(f"config {cfg} {fmt.name:13s}: t_trans median {ts[len(ts) // 2] * 1e6:7.1f} us "
+              f"(min {ts[0] * 1e6:7.1f})  kernels {k * 1e6:7.1f} us", flush=True)
+    m.free()
