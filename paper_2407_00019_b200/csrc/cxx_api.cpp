@@ -12,6 +12,7 @@
 #include <chrono>
 #include <cmath>
 #include <fstream>
+#include <functional>
 #include <iterator>
 #include <memory>
 #include <numeric>
@@ -31,6 +32,7 @@
 #include "spmvtk/spmv.hpp"
 #include "spmvtk/spmvtk_kernels.h"
 #include "spmvtk/stats.hpp"
+#include "validate.hpp"
 
 namespace spmvtk {
 
@@ -145,188 +147,78 @@ CrsMatrix canonical_from_triplets(index_t n, std::vector<index_t> rows, std::vec
   return out;
 }
 
-std::string msg2(const char* fmt, long long a, long long b = 0) {
-  char buf[160];
-  std::snprintf(buf, sizeof(buf), fmt, a, b);
-  return buf;
-}
-
-void check_ptr(const std::vector<index_t>& ptr, index_t n, index_t nnz, const char* name,
-               std::vector<std::string>& out) {
-  if (static_cast<index_t>(ptr.size()) != n + 1) {
-    out.push_back(msg2("pointer array length %lld, expected %lld",
-                       static_cast<long long>(ptr.size()), static_cast<long long>(n + 1)));
-    return;
-  }
-  if (ptr.front() != 1) out.push_back(std::string(name) + "[1] != 1");
-  if (ptr.back() != nnz + 1)
-    out.push_back(msg2("pointer array end %lld, expected nnz+1 = %lld",
-                       static_cast<long long>(ptr.back()), static_cast<long long>(nnz + 1)));
-  for (std::size_t i = 1; i < ptr.size(); ++i)
-    if (ptr[i] < ptr[i - 1]) {
-      out.push_back(std::string(name) +
-                    msg2(" not nondecreasing at position %lld", static_cast<long long>(i + 1)));
-      break;
-    }
-}
-
-void check_range(const std::vector<index_t>& idx, index_t n, const char* what,
-                 std::vector<std::string>& out) {
-  for (std::size_t p = 0; p < idx.size(); ++p)
-    if (idx[p] < 1 || idx[p] > n)
-      out.push_back(std::string(what) + msg2(" index %lld out of range at entry %lld",
-                                             static_cast<long long>(idx[p]),
-                                             static_cast<long long>(p + 1)));
-}
-
-void check_distinct(const std::vector<index_t>& ptr, const std::vector<index_t>& idx,
-                    const char* seg, std::vector<std::string>& out) {
-  std::unordered_set<index_t> seen;
-  for (std::size_t s = 0; s + 1 < ptr.size(); ++s) {
-    seen.clear();
-    for (index_t p = ptr[s]; p < ptr[s + 1]; ++p) {
-      if (p < 1 || p > static_cast<index_t>(idx.size())) break;
-      if (!seen.insert(idx[p - 1]).second)
-        out.push_back(std::string("duplicate index in ") + seg +
-                      msg2(" %lld (index %lld)", static_cast<long long>(s + 1),
-                           static_cast<long long>(idx[p - 1])));
-    }
-  }
-}
-
 }  // namespace
 
 // ---------------------------------------------------------------- formats
+// The structural rules and messages are the reference's (formats.cpp:75-182);
+// the O(nnz) checks run on the GPU (kernels_validate.cu).
 std::vector<std::string> validate(const CrsMatrix& m) {
-  std::vector<std::string> out;
-  if (m.n < 0) out.push_back("negative dimension");
-  if (m.values.size() != m.col_idx.size()) out.push_back("values / col_idx length mismatch");
-  check_ptr(m.row_ptr, m.n, m.nnz(), "row_ptr", out);
-  check_range(m.col_idx, m.n, "column", out);
-  if (out.empty()) check_distinct(m.row_ptr, m.col_idx, "row", out);
-  return out;
+  return dev::validate_segments(m.n, m.row_ptr, m.col_idx, m.values.size(), "row_ptr", "col_idx",
+                                "column", "row");
 }
 
 std::vector<std::string> validate(const CcsMatrix& m) {
-  std::vector<std::string> out;
-  if (m.n < 0) out.push_back("negative dimension");
-  if (m.values.size() != m.row_idx.size()) out.push_back("values / row_idx length mismatch");
-  check_ptr(m.col_ptr, m.n, m.nnz(), "col_ptr", out);
-  check_range(m.row_idx, m.n, "row", out);
-  if (out.empty()) check_distinct(m.col_ptr, m.row_idx, "column", out);
-  return out;
+  return dev::validate_segments(m.n, m.col_ptr, m.row_idx, m.values.size(), "col_ptr", "row_idx",
+                                "row", "column");
 }
 
 std::vector<std::string> validate(const CooMatrix& m) {
-  std::vector<std::string> out;
-  if (m.n < 0) out.push_back("negative dimension");
-  if (m.values.size() != m.row_idx.size() || m.values.size() != m.col_idx.size()) {
-    out.push_back("triplet sequences have differing lengths");
-    return out;
-  }
-  check_range(m.row_idx, m.n, "row", out);
-  check_range(m.col_idx, m.n, "column", out);
-  if (!out.empty()) return out;
-  std::unordered_set<std::uint64_t> seen;
-  for (std::size_t p = 0; p < m.values.size(); ++p) {
-    std::uint64_t key = static_cast<std::uint64_t>(m.row_idx[p]) << 32 |
-                        static_cast<std::uint64_t>(m.col_idx[p]);
-    if (!seen.insert(key).second)
-      out.push_back(msg2("duplicate (row, col) pair (%lld, %lld)",
-                         static_cast<long long>(m.row_idx[p]),
-                         static_cast<long long>(m.col_idx[p])));
-  }
-  const std::vector<index_t>* key = m.ordering == CooOrdering::RowMajor   ? &m.row_idx
-                                    : m.ordering == CooOrdering::ColMajor ? &m.col_idx
-                                                                          : nullptr;
-  if (key)
-    for (std::size_t p = 1; p < key->size(); ++p)
-      if ((*key)[p] < (*key)[p - 1]) {
-        out.push_back(msg2(m.ordering == CooOrdering::RowMajor
-                               ? "row_idx not nondecreasing at entry %lld"
-                               : "col_idx not nondecreasing at entry %lld",
-                           static_cast<long long>(p + 1)));
-        break;
-      }
-  return out;
+  const int ordering = m.ordering == CooOrdering::RowMajor   ? 0
+                       : m.ordering == CooOrdering::ColMajor ? 1
+                                                             : 2;
+  return dev::validate_triplets(m.n, m.row_idx, m.col_idx, m.values.size(), ordering);
 }
 
 std::vector<std::string> validate(const EllMatrix& m) {
-  std::vector<std::string> out;
-  if (m.n < 0) out.push_back("negative dimension");
-  if (m.band_count < 0) out.push_back("negative band count");
-  const std::size_t slots = static_cast<std::size_t>(m.n * m.band_count);
-  if (m.values.size() != slots || m.col_idx.size() != slots) {
-    out.push_back("data sequences are not n * band_count long");
-    return out;
-  }
-  if (static_cast<index_t>(m.row_entry_count.size()) != m.n) {
-    out.push_back("row_entry_count length mismatch");
-    return out;
-  }
-  check_range(m.col_idx, m.n, "column", out);
-  index_t total = 0, max_r = 0;
-  for (index_t i = 1; i <= m.n; ++i) {
-    const index_t r = m.row_entry_count[i - 1];
-    if (r < 0 || r > m.band_count) {
-      out.push_back(msg2("row %lld entry count %lld out of range", static_cast<long long>(i),
-                         static_cast<long long>(r)));
-      continue;
-    }
-    total += r;
-    max_r = std::max(max_r, r);
-    for (index_t k = r + 1; k <= m.band_count; ++k) {
-      const std::size_t s = EllMatrix::slot(m.n, k, i);
-      if (m.values[s] != 0.0)
-        out.push_back(msg2("nonzero padding value in row %lld band %lld",
-                           static_cast<long long>(i), static_cast<long long>(k)));
-      if (m.col_idx[s] != i)
-        out.push_back(msg2("padding column in row %lld band %lld is not the row index",
-                           static_cast<long long>(i), static_cast<long long>(k)));
-    }
-  }
-  if (total != m.stored_nnz)
-    out.push_back(msg2("stored_nnz %lld inconsistent with row counts (sum %lld)",
-                       static_cast<long long>(m.stored_nnz), static_cast<long long>(total)));
-  if (m.n > 0 && max_r != m.band_count)
-    out.push_back(msg2("band count %lld is not the max row entry count %lld",
-                       static_cast<long long>(m.band_count), static_cast<long long>(max_r)));
-  return out;
+  return dev::validate_ell(m.n, m.band_count, m.values, m.col_idx, m.row_entry_count,
+                           m.stored_nnz);
 }
 
 RowHistogram row_histogram(const CrsMatrix& m) {
+  // counts[i] = row_ptr[i+1] - row_ptr[i] (formats.cpp:184-192)
   RowHistogram h;
-  h.counts.resize(static_cast<std::size_t>(m.n));
-  for (index_t i = 0; i < m.n; ++i) h.counts[i] = m.row_ptr[i + 1] - m.row_ptr[i];
+  h.counts.resize(static_cast<std::size_t>(std::max<index_t>(m.n, 0)));
+  if (m.n > 0)
+    std::transform(m.row_ptr.begin() + 1, m.row_ptr.begin() + 1 + m.n, m.row_ptr.begin(),
+                   h.counts.begin(), std::minus<index_t>());
   return h;
 }
 
-DenseMatrix dense_from_crs(const CrsMatrix& m) {
-  if (m.n > kDenseOracleCap)
+namespace {
+void dense_cap(index_t n) {
+  if (n > kDenseOracleCap)
     throw Error(ErrorCode::InvalidArgument,
                 "dense oracle capped at n = " + std::to_string(kDenseOracleCap));
+}
+}  // namespace
+
+DenseMatrix dense_from_crs(const CrsMatrix& m) {
+  dense_cap(m.n);
   DenseMatrix d;
   d.n = m.n;
   d.entries.assign(static_cast<std::size_t>(m.n * m.n), 0.0);
-  for (index_t i = 1; i <= m.n; ++i)
-    for (index_t p = m.row_ptr[i - 1]; p < m.row_ptr[i]; ++p) d.at(i, m.col_idx[p - 1]) = m.values[p - 1];
+  // entries in storage order; the row advances past every segment end
+  index_t row = 1;
+  for (index_t p = 1; p <= m.nnz(); ++p) {
+    while (m.row_ptr[static_cast<std::size_t>(row)] <= p) ++row;
+    d.at(row, m.col_idx[static_cast<std::size_t>(p - 1)]) = m.values[static_cast<std::size_t>(p - 1)];
+  }
   return d;
 }
 
 CrsMatrix crs_from_dense(const DenseMatrix& d, double drop_tol) {
-  if (d.n > kDenseOracleCap)
-    throw Error(ErrorCode::InvalidArgument,
-                "dense oracle capped at n = " + std::to_string(kDenseOracleCap));
+  dense_cap(d.n);
   CrsMatrix m;
   m.n = d.n;
-  m.row_ptr.push_back(1);
-  for (index_t i = 1; i <= d.n; ++i) {
-    for (index_t j = 1; j <= d.n; ++j)
-      if (std::abs(d.at(i, j)) > drop_tol) {
-        m.values.push_back(d.at(i, j));
-        m.col_idx.push_back(j);
+  m.row_ptr.assign(static_cast<std::size_t>(d.n) + 1, 1);
+  for (index_t i = 0; i < d.n; ++i) {
+    const double* rowv = d.entries.data() + static_cast<std::size_t>(i * d.n);
+    for (index_t j = 0; j < d.n; ++j)
+      if (std::abs(rowv[j]) > drop_tol) {
+        m.col_idx.push_back(j + 1);
+        m.values.push_back(rowv[j]);
       }
-    m.row_ptr.push_back(m.nnz() + 1);
+    m.row_ptr[static_cast<std::size_t>(i) + 1] = static_cast<index_t>(m.values.size()) + 1;
   }
   return m;
 }

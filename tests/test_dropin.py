@@ -44,6 +44,17 @@ def test_reference_unit_suites_pass_on_b200_library(gpu):
 
 
 @pytest.mark.gpu
+def test_validate_messages_match_the_reference(gpu):
+    """validate() (GPU checks, kernels_validate.cu) prints exactly the
+    reference's messages, in the reference's order, on malformed matrices."""
+    ours = _run("validate_cases_b200")
+    ref = _run("validate_cases_ref")
+    assert ours.returncode == 0 and ref.returncode == 0, ours.stderr[-2000:]
+    assert ours.stdout.splitlines() == ref.stdout.splitlines()
+    assert "duplicate index in row" in ref.stdout and "out of range" in ref.stdout
+
+
+@pytest.mark.gpu
 def test_reference_acceptance_on_b200_library(gpu, tmp_path):
     r = _run("acceptance_b200", "/bin/false", str(tmp_path))
     got = {int(num): st for st, num in
