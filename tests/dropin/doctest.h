@@ -214,6 +214,14 @@ inline int run_all() {
                               __LINE__);                                                   \
   } while (0)
 
+namespace doctest {
+// doctest::Context for programs with their own main (DOCTEST_CONFIG_IMPLEMENT):
+// run() runs every registered test case and returns the failure status
+struct Context {
+  int run() { return ::doctest::detail::run_all(); }
+};
+}  // namespace doctest
+
 #ifdef DOCTEST_CONFIG_IMPLEMENT_WITH_MAIN
 int main() { return ::doctest::detail::run_all(); }
 #endif

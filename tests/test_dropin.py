@@ -54,13 +54,41 @@ def test_validate_messages_match_the_reference(gpu):
     assert "duplicate index in row" in ref.stdout and "out of range" in ref.stdout
 
 
+CLI = os.path.join(os.path.dirname(HERE), "paper_2407_00019_b200", "spmvtk")
+
+
 @pytest.mark.gpu
 def test_reference_acceptance_on_b200_library(gpu, tmp_path):
-    r = _run("acceptance_b200", "/bin/false", str(tmp_path))
+    """acceptance.cpp with OUR CLI: criteria 1-7 and 9 (8 needs SuiteSparse
+    fixtures that are not available)."""
+    r = _run("acceptance_b200", CLI, str(tmp_path))
     got = {int(num): st for st, num in
            re.findall(r"\[(PASS|FAIL|SKIP)\] criterion (\d+)", r.stdout)}
-    for c in (1, 2, 3, 4, 5, 9):
+    for c in (1, 2, 3, 4, 5, 6, 7, 9):
         assert got.get(c) == "PASS", (c, r.stdout[-3000:])
+
+
+@pytest.mark.gpu
+def test_reference_cli_tests_on_our_cli(gpu):
+    """The reference's own CLI test program (cli_tests.cpp: gen, info,
+    convert round trips, spmv --check on every kernel, bench CSV rows and
+    excluded records, profile + select, exit statuses) driving our CLI."""
+    r = _run("cli_tests_b200", CLI)
+    tail = r.stdout[-4000:] + r.stderr[-2000:]
+    assert r.returncode == 0, tail
+    assert re.search(r"test cases: *(\d+) \| *\1 passed \| 0 failed", r.stdout), tail
+
+
+def test_cli_usage_errors_exit_1():
+    """No device needed: argument errors are caught before any library call."""
+    if not os.path.exists(CLI):
+        pytest.skip("CLI not built")
+    for args in ([], ["info"], ["no-such-command"], ["convert", "a.mtx"],
+                 ["spmv", "a.mtx", "--bogus"], ["gen", "banded", "10"]):
+        r = subprocess.run([CLI, *args], capture_output=True, text=True, timeout=60)
+        assert r.returncode == 1, (args, r.stderr)
+    r = subprocess.run([CLI, "--help"], capture_output=True, text=True, timeout=60)
+    assert r.returncode == 0 and "profile" in r.stdout
 
 
 @pytest.mark.gpu
