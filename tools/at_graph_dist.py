@@ -1,6 +1,7 @@
 """Off-line AT phase on k GPUs (torchrun, one rank per GPU): every matrix of
 BASELINE config 5's D_mat sweep (plus configs 1-3 with --extra) is cut into
-row-block shards (dist.shard_arrays, as the multi-GPU SpMV runs it); each
+the entry-balanced row blocks the multi-GPU SpMV uses, each rank generating
+only its own block (spmvtk_gen_baseline_shard_host); each
 rank times its shard with spmvtk_bench (t_crs, t_ell, t_trans -- the
 reference's protocol), the job's time is the max over ranks, and
 R = SP / TT and D* follow from those (autotune.cpp:36-44, :130-158).  D_mat
@@ -20,7 +21,6 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
 
-from paper_2407_00019_b200 import dist as D  # noqa: E402
 from paper_2407_00019_b200 import spmvtk as sp  # noqa: E402
 
 ap = argparse.ArgumentParser()
@@ -29,7 +29,7 @@ ap.add_argument("--repeats", type=int, default=9)
 ap.add_argument("--max-bytes", type=int, default=48 << 30)
 ap.add_argument("--extra", action="store_true", help="add configs 1-3")
 ap.add_argument("--reserve", type=int, default=64, help="GiB of pool grown up front")
-ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01_at_graph_dist"))
+ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r02_at_graph_dist"))
 a = ap.parse_args()
 rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
 local = int(os.environ.get("LOCAL_RANK", 0))
@@ -47,27 +47,40 @@ if a.extra:
     work += [(f"cfg{c}", c, p, 0.0, 2407) for c, p in ((1, 256), (2, 1 << 20), (3, 128))]
 records = []
 for mid, cfg, param, dp, seed in work:
-    host = sp.HostCrs(cfg, param, dp, seed)
-    n = host.n
-    rp, ci, v = host.arrays(index_base=0)
-    host.free()
-    lens = np.diff(rp).astype(np.float64)
-    d_mat = float(lens.std() / lens.mean())
-    r0, lrp, lci, lv = D.shard_arrays(rp, ci, v, n, world, rank)
-    del rp, ci, v
-    shard = sp.Matrix.from_crs_block(D.block_rows(n, world), n, r0, lrp, lci, lv)
-    del lrp, lci, lv
-    t = torch.zeros(4, dtype=torch.float64, device="cuda")
+    # t = [t_crs, t_ell, t_trans, excluded, failed, rows, entries, sum of squared lengths]
+    t = torch.zeros(8, dtype=torch.float64, device="cuda")
+    err = ""
     try:
-        b = sp.bench(shard, sp.Kernel.ELL_INNER, 1, a.repeats, a.max_bytes)
-        t[:3] = torch.tensor([b["t_crs"], b["t_ell"], b["t_trans"]], dtype=torch.float64)
-    except sp.SpmvtkError as e:  # the memory guard: excluded on every rank
-        if e.status != sp.Status.ERR_MEMORY_LIMIT:
-            raise
-        t[3] = 1.0
-    shard.free()
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    t_crs, t_ell, t_trans, excl = (float(u) for u in t.tolist())
+        host = sp.gen_baseline_shard_host(cfg, param, dp, seed, rank, world)
+        lrp, _, _ = host.arrays(index_base=0)
+        lens = np.diff(lrp).astype(np.float64)
+        t[5:8] = torch.tensor([host.n, lens.sum(), (lens * lens).sum()], dtype=torch.float64)
+        n = host.ncols
+        shard = host.upload()
+        host.free()
+        try:
+            b = sp.bench(shard, sp.Kernel.ELL_INNER, 1, a.repeats, a.max_bytes)
+            t[:3] = torch.tensor([b["t_crs"], b["t_ell"], b["t_trans"]], dtype=torch.float64)
+        except sp.SpmvtkError as e:  # the memory guard: excluded on every rank
+            if e.status != sp.Status.ERR_MEMORY_LIMIT:
+                raise
+            t[3] = 1.0
+        finally:
+            shard.free()
+    except Exception as e:  # noqa: BLE001 -- agreed below, never a lone raise
+        t[4] = 1.0
+        err = f"{type(e).__name__}: {e}"
+    mx = t[:5].clone()
+    dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+    sums = t[5:].clone()
+    dist.all_reduce(sums, op=dist.ReduceOp.SUM)
+    if mx[4].item():  # some rank failed: every rank stops here together
+        raise SystemExit(f"rank {rank}: {mid} failed on a rank ({err or 'another rank'})")
+    t = torch.cat([mx[:4], sums])
+    rows_g, ent_g, sq_g = (float(u) for u in sums.tolist())
+    mu = ent_g / rows_g
+    d_mat = (max(sq_g / rows_g - mu * mu, 0.0) ** 0.5) / mu
+    t_crs, t_ell, t_trans, excl = (float(u) for u in t[:4].tolist())
     rec = {"matrix_id": mid, "d_mat": d_mat, "excluded": bool(excl)}
     if not excl:
         spd, tt, r = sp.compute_metrics(t_crs, t_ell, t_trans)
