@@ -169,7 +169,7 @@ int spmvtk_k_seg_plan(int64_t n, int64_t nnz, const int32_t* irp, int32_t chunk,
 int spmvtk_k_spmv_crs_seg(const int32_t* irp, const int32_t* icol, const double* val,
                           const double* x, double* y, const int32_t* plan,
                           int32_t w_base, int32_t w_end, int64_t row_lo, int64_t row_hi,
-                          void* stream);
+                          int64_t nnz, void* stream);
 /* The CRS kernel choice: 1 = segmented (plan needed), 0 = sub-warp per row. */
 int spmvtk_k_crs_use_seg(double mean_row, int64_t max_row);
 /* Row length above which spmvtk_k_spmv_crs hands a row to the block-per-row
@@ -217,7 +217,7 @@ int spmvtk_k_spmv_crs_push(int64_t n, const int32_t* irp, const int32_t* icol,
 int spmvtk_k_spmv_crs_seg_push(const int32_t* irp, const int32_t* icol, const double* val,
                                const double* x, const struct spmvtk_push* push,
                                const struct spmvtk_push_sync* sync, const int32_t* plan,
-                               int32_t nwarps, int64_t n, void* stream);
+                               int32_t nwarps, int64_t n, int64_t nnz, void* stream);
 int spmvtk_k_spmv_ell_cm_push(int64_t n, int32_t nz, int64_t ld, const double* val,
                               const int32_t* col, const double* x,
                               const struct spmvtk_push* push,

@@ -20,6 +20,7 @@
 #include <algorithm>
 #include <climits>
 #include <cstdint>
+#include <string>
 
 #include "common.cuh"
 #include "spmv_out.cuh"
@@ -231,15 +232,17 @@ __global__ void k_seg_plan(const int32_t* __restrict__ irp, int32_t n, int32_t c
 }
 
 
+
 template <typename Out>
 int launch_crs_seg(const int32_t* irp, const int32_t* icol, const double* val, const double* x,
                    Out y, const int32_t* plan, int32_t w_base, int32_t w_end, int32_t row_lo,
-                   int32_t row_hi, cudaStream_t s) {
+                   int32_t row_hi, int32_t nnz, cudaStream_t s) {
   const int32_t warps = w_end - w_base;
   if (warps <= 0) SPMVTK_LAUNCH_RETURN();
   const unsigned blocks = static_cast<unsigned>((static_cast<int64_t>(warps) * 32 + 255) / 256);
-k_spmv_crs_seg<Out><<<blocks, 256, 0, s>>>(irp, icol, val, x, y, plan, w_base, w_end, row_lo,
-                                             row_hi);
+(void)nnz;  // (the array length: bounds of stream prefetchers; unused here)
+  k_spmv_crs_seg<Out><<<blocks, 256, 0, s>>>(irp, icol, val, x, y, plan, w_base, w_end, row_lo,
+                                               row_hi);
   count_launches(1);
   SPMVTK_LAUNCH_RETURN();
 }
@@ -273,22 +276,23 @@ int spmvtk_k_seg_plan(int64_t n, int64_t nnz, const int32_t* irp, int32_t chunk,
 
 int spmvtk_k_spmv_crs_seg(const int32_t* irp, const int32_t* icol, const double* val,
                           const double* x, double* y, const int32_t* plan, int32_t w_base,
-                          int32_t w_end, int64_t row_lo, int64_t row_hi, void* stream) {
+                          int32_t w_end, int64_t row_lo, int64_t row_hi, int64_t nnz,
+                          void* stream) {
   return launch_crs_seg(irp, icol, val, x, PlainOut{y}, plan, w_base, w_end,
                         static_cast<int32_t>(row_lo), static_cast<int32_t>(row_hi),
-                        as_stream(stream));
+                        static_cast<int32_t>(nnz), as_stream(stream));
 }
 
 int spmvtk_k_spmv_crs_seg_push(const int32_t* irp, const int32_t* icol, const double* val,
                                const double* x, const struct spmvtk_push* push,
                                const struct spmvtk_push_sync* sync, const int32_t* plan,
-                               int32_t nwarps, int64_t n, void* stream) {
+                               int32_t nwarps, int64_t n, int64_t nnz, void* stream) {
   if (push == nullptr || push->ndst < 1 || push->ndst > SPMVTK_MAX_PEERS)
     return static_cast<int>(cudaErrorInvalidValue);
   spmvtk_push_sync none{};
   PushOut out{*push, sync ? *sync : none};
   return launch_crs_seg(irp, icol, val, x, out, plan, 0, nwarps, 0, static_cast<int32_t>(n),
-                        as_stream(stream));
+                        static_cast<int32_t>(nnz), as_stream(stream));
 }
 
 }  // extern "C"

@@ -156,7 +156,7 @@ void spmv_crs_rows(const Matrix& m, const double* x, double* y, std::int64_t r0,
     const auto& hp = crs_seg_plan(m, &plan);
     auto [w0, w1] = plan_warps_for(hp, r0, r1);
     rt::check_launch(spmvtk_k_spmv_crs_seg(m.ptr.get(), m.col.get(), m.val.get(), x, y, plan, w0,
-                                           w1, r0, r1, st),
+                                           w1, r0, r1, m.nnz, st),
                      "spmv crs");
     return;
   }
@@ -699,7 +699,8 @@ void spmv_device_push(const Matrix& m, spmvtk_kernel kernel, const double* x,
       const auto& hp = crs_seg_plan(m, &plan);
       rt::check_launch(spmvtk_k_spmv_crs_seg_push(m.ptr.get(), m.col.get(), m.val.get(), x, &push,
                                                   sync, plan,
-                                                  static_cast<std::int32_t>(hp.size()) - 1, m.n, st),
+                                                  static_cast<std::int32_t>(hp.size()) - 1, m.n,
+                                                  m.nnz, st),
                        "spmv crs (push)");
       return;
     }

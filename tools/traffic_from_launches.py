@@ -20,7 +20,7 @@ for r in rows[hi + 1:]:
     v *= {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(r[ix["Metric Unit"]], 1)
     per[r[ix["ID"]]][r[ix["Metric Name"]]] = v
     names[r[ix["ID"]]] = r[ix["Kernel Name"]]
-pats = [("CrsRows", "crs"), ("k_spmv_coo_row", "coo-row"), ("k_spmv_coo_col", "coo-col"),
+pats = [("CrsRows", "crs"), ("k_spmv_crs_seg", "crs"), ("k_spmv_coo_row", "coo-row"), ("k_spmv_coo_col", "coo-col"),
         ("k_spmv_ell_cm<", "ell-inner"), ("EllRowMajorRows", "ell-row")]
 out = defaultdict(list)
 for i, k in names.items():
