@@ -318,6 +318,22 @@ spmvtk_status spmvtk_dist_spmv_iterate(const spmvtk_dist* d, const spmvtk_matrix
                                        spmvtk_kernel kernel, double* x, int64_t steps,
                                        double* seconds);
 
+/* The same iteration with the exchange folded into the SpMV: every rank's
+ * x buffers and step flags are shared through CUDA IPC (handles exchanged
+ * over the communicator), and each step is ONE kernel launch that waits for
+ * the step's flags, computes the shard's rows and stores each of them
+ * straight into the next-x buffer of every rank that reads it (sparse != 0:
+ * only the ranks whose shard references the row; else all), then raises the
+ * next flag on every rank.  CRS or band-major ELL_INNER shards, up to 8
+ * ranks.  iterate: x as for spmvtk_dist_spmv_iterate; a flag wait that times
+ * out returns SPMVTK_ERR_DATA. */
+typedef struct spmvtk_dist_push spmvtk_dist_push;
+spmvtk_status spmvtk_dist_push_create(const spmvtk_dist* d, const spmvtk_matrix* shard,
+                                      spmvtk_kernel kernel, int sparse, spmvtk_dist_push** out);
+spmvtk_status spmvtk_dist_push_iterate(spmvtk_dist_push* p, double* x, int64_t steps,
+                                       double* seconds);
+void spmvtk_dist_push_free(spmvtk_dist_push* p);
+
 /* x ~ U(-1,1) from seed with the reference's raw-bit mapping. */
 spmvtk_status spmvtk_gen_vector(int64_t n, uint64_t seed, double* out);
 
@@ -381,13 +397,17 @@ void spmvtk_pipeline_free(spmvtk_pipeline* p);
  * Buffers live in cudaMalloc'ed memory shared through CUDA IPC handles.
  * dst[w] must point at THIS shard's first row inside rank w's buffer (so
  * row r of the shard lands at dst[w][r]); mask (device, one byte per local
- * row, may be NULL = all ranks) selects the ranks that read row r (bit w). */
+ * row, may be NULL = all ranks) selects the ranks that read row r (bit w).
+ * dst[local] is in this GPU's own memory: kernels that stage (the
+ * entry-balanced CRS SpMV) write every row there first and copy each
+ * finished tile of rows to the other destinations with coalesced stores. */
 #define SPMVTK_MAX_PEERS 8
 #define SPMVTK_IPC_HANDLE_BYTES 64
 typedef struct spmvtk_push {
   double* dst[SPMVTK_MAX_PEERS];
   const uint8_t* mask;
   int32_t ndst;
+  int32_t local; /* 0 <= local < ndst */
 } spmvtk_push;
 /* flag targets: ptr[w] = address of this rank's flag slot inside rank w's
  * flag array (system-scope release stores). */

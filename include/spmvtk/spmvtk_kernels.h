@@ -230,6 +230,13 @@ int spmvtk_k_flags_signal(const struct spmvtk_flag_targets* targets, uint64_t va
 int spmvtk_k_flags_wait(const uint64_t* flags, int32_t n, uint64_t value,
                         uint64_t timeout_ns, uint32_t* status, void* stream);
 
+/* Push-exchange setup: need[c] = 1 for every column in col[0..len); the
+ * per-row reader mask from every rank's need array (need_all: world * n
+ * bytes): bit w of mask[r] = rank w reads global row row_offset + r. */
+int spmvtk_k_mark_columns(const int32_t* col, int64_t len, uint8_t* need, void* stream);
+int spmvtk_k_push_mask(const uint8_t* need_all, int32_t world, int64_t n, int64_t row_offset,
+                       int64_t rows, int32_t rank, uint8_t* mask, void* stream);
+
 /* Random 8-byte gathers from x[0..n_pow2) (L2-resident), 2 CTAs x 512
  * threads per SM, `iters` per thread: the gather-rate roofline of the SpMV
  * kernels (gathers = 1024 * SMs * iters). */

@@ -836,6 +836,35 @@ spmvtk_status spmvtk_dist_spmv_iterate(const spmvtk_dist* d, const spmvtk_matrix
   });
 }
 
+struct spmvtk_dist_push {
+  spmvtk::dist::Push* p = nullptr;
+  ~spmvtk_dist_push() { spmvtk::dist::push_free(p); }
+};
+
+spmvtk_status spmvtk_dist_push_create(const spmvtk_dist* d, const spmvtk_matrix* shard,
+                                      spmvtk_kernel kernel, int sparse, spmvtk_dist_push** out) {
+  return guarded([&] {
+    need(d);
+    need(shard);
+    need(out, "null output");
+    auto h = std::make_unique<spmvtk_dist_push>();
+    h->p = spmvtk::dist::push_create(*d, *shard, kernel, sparse != 0);
+    *out = h.release();
+  });
+}
+
+spmvtk_status spmvtk_dist_push_iterate(spmvtk_dist_push* p, double* x, int64_t steps,
+                                       double* seconds) {
+  return guarded([&] {
+    need(p);
+    need(x);
+    const double s = spmvtk::dist::push_iterate(*p->p, x, steps);
+    if (seconds) *seconds = s;
+  });
+}
+
+void spmvtk_dist_push_free(spmvtk_dist_push* p) { delete p; }
+
 spmvtk_status spmvtk_gen_vector(int64_t n, uint64_t seed, double* out) {
   return guarded([&] {
     need(out, "null output");

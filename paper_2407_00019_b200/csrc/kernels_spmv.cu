@@ -653,7 +653,9 @@ int sync_only(const spmvtk_push_sync* sync, void* stream) {
   SPMVTK_LAUNCH_RETURN();
 }
 bool bad_push(const spmvtk_push* push, const spmvtk_push_sync* sync) {
-  if (push == nullptr || push->ndst < 1 || push->ndst > SPMVTK_MAX_PEERS) return true;
+  if (push == nullptr || push->ndst < 1 || push->ndst > SPMVTK_MAX_PEERS || push->local < 0 ||
+      push->local >= push->ndst)
+    return true;
   if (sync && (sync->nwait < 0 || sync->nwait > SPMVTK_MAX_PEERS ||
                (sync->nwait > 0 && (sync->wait_flags == nullptr || sync->status == nullptr)) ||
                sync->signal.n < 0 || sync->signal.n > SPMVTK_MAX_PEERS))

@@ -30,6 +30,7 @@
 using namespace spmvtk_dev;
 
 namespace {
+constexpr int kSegWarps = 8;  // warps per CTA
 
 __device__ __forceinline__ bool real_row(int32_t r) { return r >= 0 && r != INT_MAX; }
 
@@ -80,7 +81,7 @@ __device__ __forceinline__ void seg_reduce(const int32_t (&r)[K], const double (
 #pragma unroll
   for (int k = 1; k < K; ++k) {
     if (r[k] != r[k - 1]) {
-      if (!in_first && real_row(r[k - 1])) y.put(r[k - 1], run);
+      if (!in_first && real_row(r[k - 1])) y.put_local(r[k - 1], run);
       in_first = false;
       run = p[k];
     } else {
@@ -106,15 +107,15 @@ __device__ __forceinline__ void seg_reduce(const int32_t (&r)[K], const double (
     double tot = first_sum;
     if (lane > 0 && head == prev_tail) tot += s_prev;
     if (lane == 0 && head == carry_row) tot += carry_val;
-    y.put(head, tot);
+    y.put_local(head, tot);
   }
   const int32_t head0 = __shfl_sync(kFull, head, 0);
   if (lane == 0 && carry_row >= 0 && head0 != carry_row) {  // carried row ended at the edge
-    y.put(carry_row, carry_val);
+    y.put_local(carry_row, carry_val);
   }
   const int32_t next_head = __shfl_down_sync(kFull, head, 1);
   if (lane < 31 && next_head != tail) {  // tail run completes at the lane boundary
-    if (real_row(tail)) y.put(tail, s);
+    if (real_row(tail)) y.put_local(tail, s);
   }
   carry_row = __shfl_sync(kFull, tail, 31);
   carry_val = __shfl_sync(kFull, s, 31);
@@ -133,7 +134,7 @@ __device__ __forceinline__ void load_window(const int32_t* __restrict__ irp, int
   E = lane < nrw ? __ldg(irp + t + lane + 1) : INT_MAX;
   const int32_t up = __shfl_up_sync(kFull, E, 1);
   const int32_t start = lane == 0 ? __ldg(irp + t) : up;
-  if (lane < nrw && E == start) y.put(int64_t(t) + lane, 0.0);
+  if (lane < nrw && E == start) y.put_local(int64_t(t) + lane, 0.0);
   Elast = __shfl_sync(kFull, E, 31);
 }
 
@@ -151,7 +152,7 @@ __device__ __forceinline__ int window_rank(int32_t E, int32_t Elast, int32_t e) 
 // CRS.  plan[w] = first row whose start >= w*C (plan[nwarps] = n); warp
 // w_base + w owns rows [plan[w], plan[w+1]) clipped to [row_lo, row_hi).
 template <typename Out>
-__global__ void __launch_bounds__(256, 4) k_spmv_crs_seg(const int32_t* __restrict__ irp,
+__global__ void __launch_bounds__(kSegWarps * 32, 4) k_spmv_crs_seg(const int32_t* __restrict__ irp,
                                                          const int32_t* __restrict__ col,
                                                          const double* __restrict__ val,
                                                          const double* __restrict__ x, Out y,
@@ -160,8 +161,14 @@ __global__ void __launch_bounds__(256, 4) k_spmv_crs_seg(const int32_t* __restri
                                                          int32_t row_lo, int32_t row_hi) {
   y.begin();
   const int lane = threadIdx.x & 31;
-  const int32_t w = w_base + static_cast<int32_t>((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
-  if (w < w_end) {
+  // one pass for a full grid; a capped grid (the pushed SpMV: one flag wait
+  // and one counter arrival per resident CTA) strides over the tiles of
+  // kSegWarps consecutive warps, whose rows are one contiguous range
+  const int32_t tiles = (w_end - w_base + kSegWarps - 1) / kSegWarps;
+  for (int32_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    const int32_t t0 = w_base + tile * kSegWarps;
+    const int32_t w = t0 + static_cast<int32_t>(threadIdx.x >> 5);
+    if (w < w_end) {
     const int32_t R0 = max(__ldg(plan + w), row_lo), R1 = min(__ldg(plan + w + 1), row_hi);
     if (R0 < R1) {
       const int32_t a = __ldg(irp + R0), b = __ldg(irp + R1);
@@ -202,13 +209,15 @@ __global__ void __launch_bounds__(256, 4) k_spmv_crs_seg(const int32_t* __restri
         seg_reduce<4>(r, p, lane, carry_row, carry_val, y);
         cur = nxt;
       }
-      if (lane == 0 && carry_row >= 0) y.put(carry_row, carry_val);
+      if (lane == 0 && carry_row >= 0) y.put_local(carry_row, carry_val);
       // trailing rows of the range (empty) still pass through a window
       while (t + 32 < R1) {
         t += 32;
         load_window(irp, t, R1, lane, E, nrw, Elast, y);
       }
     }
+    }
+    y.tile(max(__ldg(plan + t0), row_lo), min(__ldg(plan + min(t0 + kSegWarps, w_end)), row_hi));
   }
   y.done();
 }
@@ -239,9 +248,10 @@ int launch_crs_seg(const int32_t* irp, const int32_t* icol, const double* val, c
                    int32_t row_hi, int32_t nnz, cudaStream_t s) {
   const int32_t warps = w_end - w_base;
   if (warps <= 0) SPMVTK_LAUNCH_RETURN();
-  const unsigned blocks = static_cast<unsigned>((static_cast<int64_t>(warps) * 32 + 255) / 256);
-(void)nnz;  // (the array length: bounds of stream prefetchers; unused here)
-  k_spmv_crs_seg<Out><<<blocks, 256, 0, s>>>(irp, icol, val, x, y, plan, w_base, w_end, row_lo,
+  unsigned blocks = static_cast<unsigned>((warps + kSegWarps - 1) / kSegWarps);
+  (void)nnz;  // (the array length: bounds of stream prefetchers; unused here)
+  if (y.synced()) blocks = std::min<unsigned>(blocks, kSMs * 4);
+  k_spmv_crs_seg<Out><<<blocks, kSegWarps * 32, 0, s>>>(irp, icol, val, x, y, plan, w_base, w_end, row_lo,
                                                row_hi);
   count_launches(1);
   SPMVTK_LAUNCH_RETURN();
@@ -287,7 +297,8 @@ int spmvtk_k_spmv_crs_seg_push(const int32_t* irp, const int32_t* icol, const do
                                const double* x, const struct spmvtk_push* push,
                                const struct spmvtk_push_sync* sync, const int32_t* plan,
                                int32_t nwarps, int64_t n, int64_t nnz, void* stream) {
-  if (push == nullptr || push->ndst < 1 || push->ndst > SPMVTK_MAX_PEERS)
+  if (push == nullptr || push->ndst < 1 || push->ndst > SPMVTK_MAX_PEERS || push->local < 0 ||
+      push->local >= push->ndst)
     return static_cast<int>(cudaErrorInvalidValue);
   spmvtk_push_sync none{};
   PushOut out{*push, sync ? *sync : none};

@@ -414,6 +414,40 @@ int spmvtk_k_count_descents(const int32_t* key, int64_t len,
   SPMVTK_LAUNCH_RETURN();
 }
 
+// push exchange setup: need[c] = 1 for every column a shard references
+__global__ void k_mark_columns(const int32_t* __restrict__ col, int64_t len, uint8_t* need) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; p < len;
+       p += stride)
+    need[__ldg(col + p)] = 1;
+}
+
+// mask[r] bit w = rank w references global row row_offset + r (own bit set)
+__global__ void k_push_mask(const uint8_t* __restrict__ need_all, int32_t world, int64_t n,
+                            int64_t row_offset, int64_t rows, int32_t rank, uint8_t* mask) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < rows;
+       r += stride) {
+    unsigned m = 1u << rank;
+    for (int32_t w = 0; w < world; ++w)
+      if (need_all[static_cast<int64_t>(w) * n + row_offset + r]) m |= 1u << w;
+    mask[r] = static_cast<uint8_t>(m);
+  }
+}
+
+int spmvtk_k_mark_columns(const int32_t* col, int64_t len, uint8_t* need, void* stream) {
+  if (len > 0) k_mark_columns<<<grid_for(len, 256), 256, 0, as_stream(stream)>>>(col, len, need);
+  SPMVTK_LAUNCH_RETURN();
+}
+
+int spmvtk_k_push_mask(const uint8_t* need_all, int32_t world, int64_t n, int64_t row_offset,
+                       int64_t rows, int32_t rank, uint8_t* mask, void* stream) {
+  if (rows > 0)
+    k_push_mask<<<grid_for(rows, 256), 256, 0, as_stream(stream)>>>(need_all, world, n, row_offset,
+                                                                   rows, rank, mask);
+  SPMVTK_LAUNCH_RETURN();
+}
+
 int spmvtk_k_count_row_descents(const int32_t* irp, int64_t n, const int32_t* col,
                                 unsigned long long* bad, void* stream) {
   cudaStream_t s = as_stream(stream);

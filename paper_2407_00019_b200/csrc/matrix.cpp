@@ -685,6 +685,8 @@ void spmv_device_push(const Matrix& m, spmvtk_kernel kernel, const double* x,
                       const spmvtk_push& push, const spmvtk_push_sync* sync) {
   if (push.ndst < 1 || push.ndst > SPMVTK_MAX_PEERS)
     throw Error(ErrorCode::InvalidArgument, "push needs 1..8 destinations");
+  if (push.local < 0 || push.local >= push.ndst)
+    throw Error(ErrorCode::InvalidArgument, "push.local must index a destination");
   for (int w = 0; w < push.ndst; ++w)
     if (push.dst[w] == nullptr && m.n > 0)
       throw Error(ErrorCode::InvalidArgument, "null push destination");

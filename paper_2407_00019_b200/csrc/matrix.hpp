@@ -144,4 +144,9 @@ int world_of(const spmvtk_dist& d);
 void unique_id(unsigned char* out);
 double iterate(const spmvtk_dist& d, const dev::Matrix& shard, spmvtk_kernel kernel, double* x,
                std::int64_t steps);
+struct Push;
+Push* push_create(const spmvtk_dist& d, const dev::Matrix& shard, spmvtk_kernel kernel,
+                  bool sparse);
+void push_free(Push* p);
+double push_iterate(Push& p, double* x, std::int64_t steps);
 }  // namespace spmvtk::dist

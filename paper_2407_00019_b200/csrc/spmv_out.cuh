@@ -18,6 +18,9 @@ struct PlainOut {
   double* __restrict__ y;
   __device__ __forceinline__ void begin() const {}
   __device__ __forceinline__ void put(int64_t r, double v) const { y[r] = v; }
+  __device__ __forceinline__ void put_local(int64_t r, double v) const { y[r] = v; }
+  __device__ __forceinline__ void tile(int64_t, int64_t) const {}
+  bool synced() const { return false; }
   __device__ __forceinline__ void done() const {}
 };
 
@@ -35,6 +38,8 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
 struct PushOut {
   spmvtk_push p;
   spmvtk_push_sync s;  // nwait = 0 / counter = NULL switch the pieces off
+  // a flag wait or a counter arrival per CTA: launch one resident wave
+  bool synced() const { return s.nwait > 0 || s.counter != nullptr; }
   // every thread of every CTA, before x is read: the step's flag wait
   __device__ __forceinline__ void begin() const {
     if (s.nwait <= 0) return;
@@ -51,11 +56,39 @@ struct PushOut {
     }
     __syncthreads();
   }
+  // every destination whose mask bit is set (kernels with one put per
+  // thread per row: ELL, the vector CRS kernels)
   __device__ __forceinline__ void put(int64_t r, double v) const {
-    const unsigned m = p.mask ? __ldg(p.mask + r) : 0xffu;
-#pragma unroll
-    for (int w = 0; w < SPMVTK_MAX_PEERS; ++w)
-      if (w < p.ndst && ((m >> w) & 1u)) p.dst[w][r] = v;
+    unsigned m = (p.mask ? __ldg(p.mask + r) : 0xffu) & ((1u << p.ndst) - 1u);
+#pragma unroll 1
+    while (m) {
+      const int w = __ffs(m) - 1;
+      m &= m - 1;
+      p.dst[w][r] = v;
+    }
+  }
+  // staged form, for kernels whose put sites are many and divergent (the
+  // entry-balanced CRS SpMV, where a put to every destination at each site
+  // cost ~15% at one rank): rows go to dst[local] only, then tile() copies
+  // a finished contiguous range of rows to the other destinations with
+  // coalesced loads and stores
+  __device__ __forceinline__ void put_local(int64_t r, double v) const { p.dst[p.local][r] = v; }
+  // every thread of the CTA, once the CTA's rows [r0, r1) are all put
+  __device__ __forceinline__ void tile(int64_t r0, int64_t r1) const {
+    if (p.ndst <= 1) return;
+    __syncthreads();
+    const double* src = p.dst[p.local];
+    const unsigned others = ((1u << p.ndst) - 1u) & ~(1u << p.local);
+    for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
+      const double v = __ldcg(src + r);
+      unsigned m = p.mask ? (__ldg(p.mask + r) & others) : others;
+#pragma unroll 1
+      while (m) {
+        const int w = __ffs(m) - 1;
+        m &= m - 1;
+        p.dst[w][r] = v;
+      }
+    }
   }
   // every thread of every CTA, at the end: fence the pushes at system scope;
   // the last CTA to arrive stores the step flag to every rank

@@ -122,7 +122,8 @@ IPC_HANDLE_BYTES = 64
 
 class Push(C.Structure):
     """spmvtk_push: destinations of pushed result rows (spmvtk.h)."""
-    _fields_ = [("dst", C.c_void_p * MAX_PEERS), ("mask", C.c_void_p), ("ndst", C.c_int32)]
+    _fields_ = [("dst", C.c_void_p * MAX_PEERS), ("mask", C.c_void_p), ("ndst", C.c_int32),
+                ("local", C.c_int32)]
 
 
 class FlagTargets(C.Structure):
@@ -209,6 +210,9 @@ SIGNATURES = {
                                                  C.POINTER(_i64)]),
     "spmvtk_gen_baseline_shard": (C.c_int, [_P, C.c_int, _i64, _d, _u64, _PP]),
     "spmvtk_dist_spmv_iterate": (C.c_int, [_P, _P, C.c_int, _P, _i64, _pd]),
+    "spmvtk_dist_push_create": (C.c_int, [_P, _P, C.c_int, C.c_int, _PP]),
+    "spmvtk_dist_push_iterate": (C.c_int, [_P, _P, _i64, _pd]),
+    "spmvtk_dist_push_free": (None, [_P]),
     "spmvtk_host_crs_free": (None, [_P]),
     "spmvtk_matrix_from_host_crs": (C.c_int, [_P, _PP]),
     "spmvtk_conversion_bytes": (C.c_int, [_P, C.c_int, C.POINTER(_u64), C.POINTER(_u64)]),
@@ -781,6 +785,13 @@ class Dist:
                                                   C.c_void_p(x_ptr), steps, C.byref(sec)))
         return sec.value
 
+    def push(self, shard: "Matrix", kernel: "Kernel", sparse: bool = True) -> "DistPush":
+        """The exchange folded into the SpMV (spmvtk_dist_push_*)."""
+        h = C.c_void_p()
+        _check(self._lib.spmvtk_dist_push_create(self._h, shard.handle, int(kernel),
+                                                 1 if sparse else 0, C.byref(h)))
+        return DistPush(self._lib, h, shard)
+
     def free(self) -> None:
         if self._h:
             self._lib.spmvtk_dist_free(self._h)
@@ -791,3 +802,21 @@ class Dist:
             self.free()
         except Exception:
             pass
+
+
+class DistPush:
+    """spmvtk_dist_push: x <- A^steps x with every step one pushed-SpMV launch."""
+
+    def __init__(self, lib, h, shard):
+        self._lib, self._h, self._shard = lib, h, shard
+
+    def iterate(self, x_ptr: int, steps: int) -> float:
+        sec = C.c_double()
+        _check(self._lib.spmvtk_dist_push_iterate(self._h, C.c_void_p(x_ptr), steps,
+                                                  C.byref(sec)))
+        return sec.value
+
+    def free(self) -> None:
+        if self._h:
+            self._lib.spmvtk_dist_push_free(self._h)
+            self._h = None

@@ -161,6 +161,21 @@ def test_dist_capi_single_rank_nccl(gpu, port):
                 assert err <= 1e-12 and sec > 0, (config, k, err)
                 if h is not shard:
                     h.free()
+            # the exchange folded into the SpMV: same iterate (CRS and ELL)
+            for h, k in ((shard, sp.Kernel.CRS), (shard.convert(sp.Format.ELL), sp.Kernel.ELL_INNER)):
+                for sparse in (True, False):
+                    pu = d.push(h, k, sparse=sparse)
+                    x = torch.from_numpy(x0).cuda()
+                    sec = pu.iterate(x.data_ptr(), 3)
+                    got = x.cpu().numpy()
+                    err = np.max(np.abs(got - want)) / np.max(np.abs(want))
+                    assert err <= 1e-12 and sec > 0, (config, k, sparse, err)
+                    x = torch.from_numpy(x0).cuda()  # a second run on the same buffers
+                    pu.iterate(x.data_ptr(), 3)
+                    assert np.max(np.abs(x.cpu().numpy() - want)) / np.max(np.abs(want)) <= 1e-12
+                    pu.free()
+                if h is not shard:
+                    h.free()
             shard.free()
             full.free()
     finally:

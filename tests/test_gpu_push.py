@@ -89,6 +89,7 @@ def test_push_iteration_emulated(gpu, port, world, kind, fmt, sparse, fused):
                 pu.dst[w] = X[w][b].data_ptr() + r * chunk * 8
             pu.mask = masks[r].data_ptr() if masks[r] is not None else None
             pu.ndst = world
+            pu.local = r
             per_buf.append(pu)
         pushes.append(per_buf)
         tg = sp.FlagTargets()
@@ -169,6 +170,12 @@ def test_ipc_buffers_roundtrip(gpu):
     bad = sp.Push()
     bad.ndst = 0
     x = torch.zeros(100, dtype=torch.float64, device="cuda")
+    with pytest.raises(sp.SpmvtkError):
+        m.spmv_device_push(sp.Kernel.CRS, x.data_ptr(), bad)
+    bad = sp.Push()
+    bad.dst[0] = x.data_ptr()
+    bad.ndst = 1
+    bad.local = 1  # must index a destination
     with pytest.raises(sp.SpmvtkError):
         m.spmv_device_push(sp.Kernel.CRS, x.data_ptr(), bad)
     ok = sp.Push()
