@@ -847,9 +847,11 @@ __global__ void __launch_bounds__(256) k_crs_to_ell_cm(int64_t n, int32_t nz, in
 // contiguous CRS range of at most ROWS*32 entries, copied to shared memory
 // with fully coalesced loads (all of a thread's loads in flight before any
 // shared store), then written band by band (ROWS consecutive rows per band).
-int g_ell_flat_rows = 64;  // tuning: 64 or 128 rows per CTA (64 measured faster)
+// rows per CTA of the flat band-major conversion: 0 = auto (256 rows for
+// nz <= 8, else 64, measured faster than 128); 64 / 128 force one
+int g_ell_flat_rows = 0;
 
-template <int ROWS, int THREADS>
+template <int ROWS, int THREADS, int MAXNZ = 32>
 __global__ void __launch_bounds__(THREADS) k_crs_to_ell_cm_flat(int64_t n, int32_t nz, int64_t ld,
                                                                 const int32_t* __restrict__ irp,
                                                                 const int32_t* __restrict__ icol,
@@ -858,7 +860,7 @@ __global__ void __launch_bounds__(THREADS) k_crs_to_ell_cm_flat(int64_t n, int32
                                                                 int32_t* __restrict__ out_col,
                                                                 int32_t* __restrict__ out_count,
                                                                 int64_t pad_base) {
-  constexpr int kCap = ROWS * 32;
+  constexpr int kCap = ROWS * MAXNZ;  // rows hold at most MAXNZ >= nz entries
   // staged entry f lives at f + f/32: rows of exactly 16 or 32 entries read
   // in the write phase (one row per lane) would otherwise all hit one bank
   extern __shared__ unsigned char s_raw[];
@@ -1044,7 +1046,7 @@ int spmvtk_k_tune_convert(const char* key, int value) {
     return 0;
   }
   if (key && std::string(key) == "ell_flat_rows") {
-    g_ell_flat_rows = value == 64 ? 64 : 128;
+    g_ell_flat_rows = value == 64 ? 64 : value == 128 ? 128 : 0;
     return 0;
   }
   if (key && std::string(key) == "ccs_stage_threads") {
@@ -1229,7 +1231,13 @@ int spmvtk_k_crs_to_ell_cm(int64_t n, int32_t nz, int64_t ld, const int32_t* irp
       return true;
     }();
     (void)attrs;
-    if (g_ell_flat_rows == 64) {
+    if (nz <= 8 && g_ell_flat_rows == 0) {
+      // short rows: 256 rows per block (the 32-entry layout would give each
+      // block a few hundred entries and the grid many small waves)
+      unsigned blocks = static_cast<unsigned>((ld + 255) / 256);
+      k_crs_to_ell_cm_flat<256, 256, 8><<<blocks, 256, (2048 + 64) * 12, s>>>(
+          n, nz, ld, irp, icol, val, out_val, out_col, out_count, pad_base);
+    } else if (g_ell_flat_rows != 128) {
       unsigned blocks = static_cast<unsigned>((ld + 63) / 64);
       k_crs_to_ell_cm_flat<64, 256><<<blocks, 256, (2048 + 64) * 12, s>>>(
           n, nz, ld, irp, icol, val, out_val, out_col, out_count, pad_base);
@@ -1250,10 +1258,11 @@ int spmvtk_k_crs_to_ell_rm(int64_t n, int32_t nz, const int32_t* irp, const int3
                            int32_t* out_count, int64_t pad_base, void* stream) {
   cudaStream_t s = as_stream(stream);
   if (n <= 0) SPMVTK_LAUNCH_RETURN();
-  // ~4096 slots per block, at least one row
+  // ~4096 slots per block, at least one row, and at least two blocks per SM
   int rows = nz > 0 ? static_cast<int>(4096 / nz) : 4096;
-  if (rows < 1) rows = 1;
   if (rows > 4096) rows = 4096;
+  rows = static_cast<int>(std::min<int64_t>(rows, (n + 2 * kSMs - 1) / (2 * kSMs)));
+  if (rows < 1) rows = 1;
   unsigned blocks = static_cast<unsigned>((n + rows - 1) / rows);
   size_t smem = static_cast<size_t>(rows + 1) * sizeof(int32_t);
   k_crs_to_ell_rm<<<blocks, 256, smem, s>>>(n, nz, FastDiv(static_cast<uint32_t>(nz > 0 ? nz : 1)),
@@ -1281,6 +1290,7 @@ void preload_convert() {
   cudaFuncGetAttributes(&a, k_bkt_sort_big);
   cudaFuncGetAttributes(&a, k_crs_to_ell_cm<32>);
   cudaFuncGetAttributes(&a, k_crs_to_ell_cm_flat<64, 256>);
+  cudaFuncGetAttributes(&a, k_crs_to_ell_cm_flat<256, 256, 8>);
   cudaFuncGetAttributes(&a, k_crs_to_ell_cm_flat<128, 512>);
   cudaFuncGetAttributes(&a, k_crs_to_ell_rm);
 }

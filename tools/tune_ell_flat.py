@@ -1,4 +1,4 @@
-"""Times CRS->ELL (band-major, nz <= 32) with 64- and 128-row CTAs."""
+"""Times CRS->ELL (band-major, nz <= 32): auto (256-row CTAs for nz <= 8), 64- and 128-row CTAs."""
 import os
 import sys
 
@@ -12,10 +12,10 @@ lib = sp.load_library()
 sp.set_stream(torch.cuda.current_stream().cuda_stream)
 for cfg, param in ((1, 256), (2, 1 << 20), (3, 128), (5, 1 << 21)):
     m = sp.HostCrs(cfg, param).upload()
-    for rows in (64, 128):
+    for rows in (0, 64, 128):
         lib.spmvtk_k_tune(b"ell_flat_rows", rows)
-        for fmt in (sp.Format.ELL, sp.Format.COO_ROW, sp.Format.ELL_ROWMAJOR):
+        for fmt in (sp.Format.ELL,):
             t = m.transform_kernel_seconds(fmt, 9)
             print(f"cfg{cfg} rows={rows} {fmt.name}: {t*1e6:8.1f} us", flush=True)
     m.free()
-lib.spmvtk_k_tune(b"ell_flat_rows", 64)
+lib.spmvtk_k_tune(b"ell_flat_rows", 0)
