@@ -53,6 +53,19 @@ __device__ __forceinline__ int4 ld_stream4(const int4* p) {
 }
 // x gathers: keep them cacheable (x is small and reused)
 __device__ __forceinline__ double ld_x(const double* p) { return __ldg(p); }
+// 4 doubles in one 256-bit load, L1 no-allocate, L2 evict-first (sm_100
+// LDG.E.NA.EFL2.256; the address must be 32-byte aligned): matrix streams
+// read once, so x and other reused lines keep the L2
+__device__ __forceinline__ void ld4_stream_first(const double* p, double2& lo, double2& hi) {
+  unsigned long long a, b, c, d;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v4.b64 {%0,%1,%2,%3}, [%4];"
+               : "=l"(a), "=l"(b), "=l"(c), "=l"(d)
+               : "l"(p));
+  lo = make_double2(__longlong_as_double(static_cast<long long>(a)),
+                    __longlong_as_double(static_cast<long long>(b)));
+  hi = make_double2(__longlong_as_double(static_cast<long long>(c)),
+                    __longlong_as_double(static_cast<long long>(d)));
+}
 
 // streaming stores (evict-first from L1)
 __device__ __forceinline__ void st_stream(double* p, double v) {

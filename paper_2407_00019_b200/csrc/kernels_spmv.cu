@@ -314,8 +314,8 @@ __global__ void __launch_bounds__(256) k_spmv_coo_row4(int64_t n, int64_t nnz, i
     if (q >= st && q + 3 < en) {
       const int4 rv = ld_stream4(reinterpret_cast<const int4*>(row + q));
       const int4 cv = ld_stream4(reinterpret_cast<const int4*>(col + q));
-      const double2 v0 = ld_stream2(reinterpret_cast<const double2*>(val + q));
-      const double2 v1 = ld_stream2(reinterpret_cast<const double2*>(val + q + 2));
+      double2 v0, v1;
+      ld4_stream_first(val + q, v0, v1);
       r[0] = rv.x; r[1] = rv.y; r[2] = rv.z; r[3] = rv.w;
       p[0] = v0.x * ld_x(x + cv.x);
       p[1] = v0.y * ld_x(x + cv.y);
@@ -701,7 +701,7 @@ int spmvtk_k_spmv_coo_row(int64_t n, int64_t nnz, const int32_t* row, const int3
   }
   const bool quad = g_coo_variant != 0 && (reinterpret_cast<uintptr_t>(row) & 15) == 0 &&
                     (reinterpret_cast<uintptr_t>(col) & 15) == 0 &&
-                    (reinterpret_cast<uintptr_t>(val) & 15) == 0;
+                    (reinterpret_cast<uintptr_t>(val) & 31) == 0;  // 256-bit value loads
   int64_t chunk = quad ? g_coo_chunk : 1024;
   if (quad && g_coo_chunk_auto) {
     // wave quantisation: one warp per chunk, so pick the chunk (2048 or

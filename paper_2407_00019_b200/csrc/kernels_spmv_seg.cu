@@ -34,38 +34,55 @@ constexpr int kSegWarps = 8;  // warps per CTA
 
 __device__ __forceinline__ bool real_row(int32_t r) { return r >= 0 && r != INT_MAX; }
 
-// Entries of one lane: 4 consecutive positions q..q+3 (q a multiple of 4),
-// masked to [a, b).  Out-of-range slots read nothing.
-struct Quad {
-  int4 c;
-  double2 v0, v1;
+// Entries of one lane: K (4 or 8) consecutive positions q..q+K-1 (q a
+// multiple of K), masked to [a, b).  Out-of-range slots read nothing.  Full
+// groups use 256-bit L2-evict-first loads where the width allows.
+template <int K>
+struct Group {
+  int32_t c[K];
+  double v[K];
 };
 
-__device__ __forceinline__ void load_quad(const int32_t* __restrict__ col,
-                                          const double* __restrict__ val, int32_t q, int32_t a,
-                                          int32_t b, Quad& o) {
-  if (q >= a && q + 3 < b) {
-    o.c = ld_stream4(reinterpret_cast<const int4*>(col + q));
-    o.v0 = ld_stream2(reinterpret_cast<const double2*>(val + q));
-    o.v1 = ld_stream2(reinterpret_cast<const double2*>(val + q + 2));
+__device__ __forceinline__ void ld8_cols_first(const int32_t* p, int32_t (&c)[8]) {
+  asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(c[0]), "=r"(c[1]), "=r"(c[2]), "=r"(c[3]), "=r"(c[4]), "=r"(c[5]),
+                 "=r"(c[6]), "=r"(c[7])
+               : "l"(p));
+}
+
+template <int K>
+__device__ __forceinline__ void load_group(const int32_t* __restrict__ col,
+                                           const double* __restrict__ val, int32_t q, int32_t a,
+                                           int32_t b, bool wide, Group<K>& o) {
+  if (wide && q >= a && q + K - 1 < b) {
+    if constexpr (K == 8) {
+      ld8_cols_first(col + q, o.c);
+    } else {
+      const int4 c4 = ld_stream4(reinterpret_cast<const int4*>(col + q));
+      o.c[0] = c4.x; o.c[1] = c4.y; o.c[2] = c4.z; o.c[3] = c4.w;
+    }
+#pragma unroll
+    for (int k = 0; k < K; k += 4) {
+      double2 lo, hi;
+      ld4_stream_first(val + q + k, lo, hi);
+      o.v[k] = lo.x; o.v[k + 1] = lo.y; o.v[k + 2] = hi.x; o.v[k + 3] = hi.y;
+    }
   } else {
-    o.c = make_int4(0, 0, 0, 0);
-    o.v0 = make_double2(0.0, 0.0);
-    o.v1 = make_double2(0.0, 0.0);
-    if (q + 0 >= a && q + 0 < b) { o.c.x = ld_stream(col + q + 0); o.v0.x = ld_stream(val + q + 0); }
-    if (q + 1 >= a && q + 1 < b) { o.c.y = ld_stream(col + q + 1); o.v0.y = ld_stream(val + q + 1); }
-    if (q + 2 >= a && q + 2 < b) { o.c.z = ld_stream(col + q + 2); o.v1.x = ld_stream(val + q + 2); }
-    if (q + 3 >= a && q + 3 < b) { o.c.w = ld_stream(col + q + 3); o.v1.y = ld_stream(val + q + 3); }
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const bool in = q + k >= a && q + k < b;
+      o.c[k] = in ? ld_stream(col + q + k) : 0;
+      o.v[k] = in ? ld_stream(val + q + k) : 0.0;
+    }
   }
 }
 
-__device__ __forceinline__ void products(const Quad& g, int32_t q, int32_t a, int32_t b,
-                                         const double* __restrict__ x, double (&p)[4]) {
-  // gathers only for real entries; the four are independent
-  p[0] = (q + 0 >= a && q + 0 < b) ? g.v0.x * ld_x(x + g.c.x) : 0.0;
-  p[1] = (q + 1 >= a && q + 1 < b) ? g.v0.y * ld_x(x + g.c.y) : 0.0;
-  p[2] = (q + 2 >= a && q + 2 < b) ? g.v1.x * ld_x(x + g.c.z) : 0.0;
-  p[3] = (q + 3 >= a && q + 3 < b) ? g.v1.y * ld_x(x + g.c.w) : 0.0;
+template <int K>
+__device__ __forceinline__ void products(const Group<K>& g, int32_t q, int32_t a, int32_t b,
+                                         const double* __restrict__ x, double (&p)[K]) {
+  // gathers only for real entries; they are independent
+#pragma unroll
+  for (int k = 0; k < K; ++k) p[k] = (q + k >= a && q + k < b) ? g.v[k] * ld_x(x + g.c[k]) : 0.0;
 }
 
 // One group of 32*K entries (K per lane, r[k] = row or -1 before / INT_MAX
@@ -151,7 +168,9 @@ __device__ __forceinline__ int window_rank(int32_t E, int32_t Elast, int32_t e) 
 
 // CRS.  plan[w] = first row whose start >= w*C (plan[nwarps] = n); warp
 // w_base + w owns rows [plan[w], plan[w+1]) clipped to [row_lo, row_hi).
-template <typename Out>
+// (K = 8 entries per lane, 120 registers at 2 CTAs/SM, measured 14-30 %
+// slower on configs 2-5: profiles/r02_tune_spmv_evict_first.txt)
+template <int K, typename Out>
 __global__ void __launch_bounds__(kSegWarps * 32, 4) k_spmv_crs_seg(const int32_t* __restrict__ irp,
                                                          const int32_t* __restrict__ col,
                                                          const double* __restrict__ val,
@@ -159,6 +178,9 @@ __global__ void __launch_bounds__(kSegWarps * 32, 4) k_spmv_crs_seg(const int32_
                                                          const int32_t* __restrict__ plan,
                                                          int32_t w_base, int32_t w_end,
                                                          int32_t row_lo, int32_t row_hi) {
+  // wide loads need 32-byte aligned values and 16-byte aligned columns
+  // (pool allocations are; arrays handed in through the lower ABI may not be)
+  const bool wide = ((reinterpret_cast<uintptr_t>(val) & 31) | (reinterpret_cast<uintptr_t>(col) & 15)) == 0;
   y.begin();
   const int lane = threadIdx.x & 31;
   // one pass for a full grid; a capped grid (the pushed SpMV: one flag wait
@@ -173,40 +195,43 @@ __global__ void __launch_bounds__(kSegWarps * 32, 4) k_spmv_crs_seg(const int32_
     if (R0 < R1) {
       const int32_t a = __ldg(irp + R0), b = __ldg(irp + R1);
       int32_t t = R0, E, nrw, Elast;
-      int32_t g = a & ~3;
-      Quad cur;
-      load_quad(col, val, g + 4 * lane, a, b, cur);
+      constexpr int G = 32 * K;  // entries per warp step
+      int32_t g = a & ~(K - 1);
+      Group<K> cur;
+      load_group<K>(col, val, g + K * lane, a, b, wide, cur);
       load_window(irp, t, R1, lane, E, nrw, Elast, y);
       int32_t carry_row = -1;
       double carry_val = 0.0;
-      for (; g < b; g += 128) {
-        Quad nxt;
-        if (g + 128 < b) load_quad(col, val, g + 128 + 4 * lane, a, b, nxt);
-        const int32_t q = g + 4 * lane;
-        double p[4];
-        products(cur, q, a, b, x, p);
-        int32_t r[4];
-        bool pend[4];
+      for (; g < b; g += G) {
+        Group<K> nxt;
+        if (g + G < b) load_group<K>(col, val, g + G + K * lane, a, b, wide, nxt);
+        const int32_t q = g + K * lane;
+        double p[K];
+        products<K>(cur, q, a, b, x, p);
+        int32_t r[K];
+        bool pend[K];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < K; ++k) {
           const int32_t e = q + k;
           pend[k] = e >= a && e < b;
           r[k] = e < a ? -1 : INT_MAX;
         }
         while (true) {
+          bool any = false;
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
+          for (int k = 0; k < K; ++k) {
             const int o = window_rank(E, Elast, q + k);
             if (pend[k] && o < nrw) {
               r[k] = t + o;
               pend[k] = false;
             }
+            any = any || pend[k];
           }
-          if (!__any_sync(kFull, pend[0] || pend[1] || pend[2] || pend[3])) break;
+          if (!__any_sync(kFull, any)) break;
           t += 32;
           load_window(irp, t, R1, lane, E, nrw, Elast, y);
         }
-        seg_reduce<4>(r, p, lane, carry_row, carry_val, y);
+        seg_reduce<K>(r, p, lane, carry_row, carry_val, y);
         cur = nxt;
       }
       if (lane == 0 && carry_row >= 0) y.put_local(carry_row, carry_val);
@@ -251,8 +276,8 @@ int launch_crs_seg(const int32_t* irp, const int32_t* icol, const double* val, c
   unsigned blocks = static_cast<unsigned>((warps + kSegWarps - 1) / kSegWarps);
   (void)nnz;  // (the array length: bounds of stream prefetchers; unused here)
   if (y.synced()) blocks = std::min<unsigned>(blocks, kSMs * 4);
-  k_spmv_crs_seg<Out><<<blocks, kSegWarps * 32, 0, s>>>(irp, icol, val, x, y, plan, w_base, w_end, row_lo,
-                                               row_hi);
+  k_spmv_crs_seg<4, Out><<<blocks, kSegWarps * 32, 0, s>>>(irp, icol, val, x, y, plan, w_base,
+                                                            w_end, row_lo, row_hi);
   count_launches(1);
   SPMVTK_LAUNCH_RETURN();
 }
@@ -262,8 +287,8 @@ int launch_crs_seg(const int32_t* irp, const int32_t* icol, const double* val, c
 namespace spmvtk_dev {
 void preload_seg() {
   cudaFuncAttributes a;
-  cudaFuncGetAttributes(&a, k_spmv_crs_seg<PlainOut>);
-  cudaFuncGetAttributes(&a, k_spmv_crs_seg<PushOut>);
+  cudaFuncGetAttributes(&a, k_spmv_crs_seg<4, PlainOut>);
+  cudaFuncGetAttributes(&a, k_spmv_crs_seg<4, PushOut>);
   cudaFuncGetAttributes(&a, k_seg_plan);
 }
 }  // namespace spmvtk_dev

@@ -745,3 +745,60 @@ def test_lower_abi_phase1_phase2_and_statistics(gpu, port):
         assert int(h[1]) == int(lens.sum())
         assert int(h[2]) == int((lens.astype(np.int64) ** 2).sum())
         assert int(acc.abs().sum().item()) == 0
+
+
+def test_lower_abi_spmv_kernels_on_unaligned_arrays(gpu, port):
+    """spmvtk_k_spmv_crs_seg and spmvtk_k_spmv_coo_row on device arrays that
+    start 4 / 8 bytes past an aligned address (arrays a caller hands in
+    through the lower ABI need not be pool-aligned): the 256-bit / 128-bit
+    loads must switch off, the products stay within 1e-12 of the port."""
+    import ctypes as C
+
+    import torch
+    sp = gpu
+    lib = sp.load_library()
+    P, I64, I32 = C.c_void_p, C.c_int64, C.c_int32
+    lib.spmvtk_k_seg_plan_warps.restype = C.c_int32
+    lib.spmvtk_k_seg_plan_warps.argtypes = [I64, I32]
+    lib.spmvtk_k_seg_plan.argtypes = [I64, I64, P, I32, P, P]
+    lib.spmvtk_k_spmv_crs_seg.argtypes = [P, P, P, P, P, P, I32, I32, I64, I64, I64, P]
+    lib.spmvtk_k_spmv_coo_row.argtypes = [I64, I64, P, P, P, P, P, P]
+    rng = np.random.default_rng(17)
+    n = 30_000
+    lens = np.minimum(n, np.round(rng.lognormal(2.0, 1.2, size=n)).astype(np.int64))
+    rows = [np.sort(rng.choice(n, size=int(ln), replace=False)) for ln in lens]
+    ci = np.concatenate(rows).astype(np.int32)
+    rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    v = rng.standard_normal(ci.shape[0])
+    nnz = int(rp[-1])
+    x = rng.uniform(-1, 1, n)
+    want = port.spmv_crs(n, rp.astype(np.int64) + 1, ci.astype(np.int64) + 1, v, x)  # 1-based
+    stream = torch.cuda.current_stream().cuda_stream
+
+    def shifted(a, dt, shift_elems):
+        buf = torch.empty(a.shape[0] + 8, dtype=dt, device="cuda")
+        view = buf[shift_elems:shift_elems + a.shape[0]]
+        view.copy_(torch.from_numpy(a))
+        return view
+
+    irp = torch.from_numpy(rp).cuda()
+    xd = torch.from_numpy(x).cuda()
+    y = torch.empty(n, dtype=torch.float64, device="cuda")
+    chunk = 2048
+    nw = lib.spmvtk_k_seg_plan_warps(nnz, chunk)
+    plan = torch.empty(nw + 1, dtype=torch.int32, device="cuda")
+    assert lib.spmvtk_k_seg_plan(n, nnz, irp.data_ptr(), chunk, plan.data_ptr(), stream) == 0
+    rows_coo = np.repeat(np.arange(n, dtype=np.int32), lens)
+    for cshift, vshift in ((0, 0), (1, 1), (0, 1), (2, 3)):
+        icol = shifted(ci, torch.int32, cshift)
+        val = shifted(v, torch.float64, vshift)
+        y.fill_(float("nan"))
+        assert lib.spmvtk_k_spmv_crs_seg(irp.data_ptr(), icol.data_ptr(), val.data_ptr(),
+                                         xd.data_ptr(), y.data_ptr(), plan.data_ptr(), 0, nw, 0,
+                                         n, nnz, stream) == 0
+        assert np.max(np.abs(y.cpu().numpy() - want)) <= 1e-12 * np.max(np.abs(want)), (cshift, vshift)
+        rowd = shifted(rows_coo, torch.int32, cshift)
+        y.fill_(float("nan"))
+        assert lib.spmvtk_k_spmv_coo_row(n, nnz, rowd.data_ptr(), icol.data_ptr(), val.data_ptr(),
+                                         xd.data_ptr(), y.data_ptr(), stream) == 0
+        assert np.max(np.abs(y.cpu().numpy() - want)) <= 1e-12 * np.max(np.abs(want)), (cshift, vshift)

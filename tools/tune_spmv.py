@@ -23,7 +23,7 @@ ap.add_argument("--configs", default="2,3,4,5")
 ap.add_argument("--reps", type=int, default=50)
 ap.add_argument("--dparam", type=float, default=0.0)
 ap.add_argument("--crs", default="16,18,20")
-ap.add_argument("--asyncs", default="0", help="(unused: the cp.async ring variant was dropped)")
+ap.add_argument("--seg-ks", default="4", help="(only 4 remains: 8 entries per lane was slower)")
 ap.add_argument("--seg-chunks", default="1024,2048,4096")
 ap.add_argument("--coo", default="1,2")
 ap.add_argument("--coo-chunks", default="1024,2048,4096")
@@ -67,14 +67,14 @@ for cfg in [int(c) for c in a.configs.split(",")]:
     for v in [int(s) for s in a.crs.split(",")]:
         tune("crs_variant", v)
         chunks = [int(c) for c in a.seg_chunks.split(",")] if v == 20 else [0]
-        depths = [int(c) for c in a.asyncs.split(",")] if v == 20 else [0]
-        for dep, c in [(dd, cc) for dd in depths for cc in chunks]:
+        ks = [int(c) for c in a.seg_ks.split(",")] if v == 20 else [4]
+        for dep, c in [(dd, cc) for dd in ks for cc in chunks]:
             tune("seg_chunk", c)
             y.fill_(np.nan)
             t = timed(m, sp.Kernel.CRS, x, y, a.reps)
             got = y.cpu().numpy()
             err = float(np.max(np.abs(got - ref)) / max(np.max(np.abs(ref)), 1e-300))
-            print(f"    crs v{v:2d} a{dep} chunk={c:5d}: {t * 1e6:8.1f} us {crs_bytes / t / 1e9:7.0f} GB/s "
+            print(f"    crs v{v:2d} k{dep} chunk={c:5d}: {t * 1e6:8.1f} us {crs_bytes / t / 1e9:7.0f} GB/s "
                   f"{nnz / t / 1e9:6.1f} Ggather/s err={err:.1e}", flush=True)
     tune("crs_variant", -1)
     tune("seg_chunk", 0)
