@@ -28,6 +28,7 @@ ap.add_argument("--seg-chunks", default="1024,2048,4096")
 ap.add_argument("--coo", default="1,2")
 ap.add_argument("--coo-chunks", default="1024,2048,4096")
 ap.add_argument("--coo-segs", default="0")
+ap.add_argument("--ell", type=int, default=1, help="also time ELL-inner (where it fits)")
 a = ap.parse_args()
 lib = sp.load_library()
 sp.set_stream(torch.cuda.current_stream().cuda_stream)
@@ -94,4 +95,15 @@ for cfg in [int(c) for c in a.configs.split(",")]:
     tune("coo_variant", 1)
     tune("coo_chunk", 0)
     coo.free()
+    if a.ell and st.max_row * n * 12 < (40 << 30):
+        ell = m.convert(sp.Format.ELL)
+        nz = ell.describe().band_count
+        ell_bytes = 12 * n * nz + 16 * n
+        y.fill_(np.nan)
+        t = timed(ell, sp.Kernel.ELL_INNER, x, y, a.reps)
+        got = y.cpu().numpy()
+        err = float(np.max(np.abs(got - ref)) / max(np.max(np.abs(ref)), 1e-300))
+        print(f"    ell inner : {t * 1e6:8.1f} us {ell_bytes / t / 1e9:7.0f} GB/s "
+              f"{nnz / t / 1e9:6.1f} Ggather/s err={err:.1e}", flush=True)
+        ell.free()
     m.free()
