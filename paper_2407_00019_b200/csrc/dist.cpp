@@ -205,14 +205,22 @@ struct Push {
 };
 
 namespace {
-void barrier(const spmvtk_dist& d) {
+// a barrier that also agrees on a flag: true on every rank iff `ok` on all
+// (so a local failure turns into the same error on every rank instead of
+// leaving the others inside a collective)
+bool all_ok(const spmvtk_dist& d, bool ok) {
   rt::DevArray<int> one(1, "barrier");
   cudaStream_t st = rt::stream();
-  rt::check(cudaMemsetAsync(one.get(), 0, sizeof(int), st), "barrier");
+  rt::check(cudaMemsetAsync(one.get(), ok ? 1 : 0, sizeof(int), st), "barrier");
   rt::DevArray<int> all(static_cast<std::size_t>(d.world), "barrier");
   nccl_check(nccl().allGather(one.get(), all.get(), 1, ncclInt32, d.comm, st), "barrier");
-  rt::sync();
+  std::vector<int> h(static_cast<std::size_t>(d.world));
+  rt::copy_to_host(h.data(), all.get(), h.size() * sizeof(int));
+  for (int v : h)
+    if (v == 0) return false;
+  return true;
 }
+void barrier(const spmvtk_dist& d) { (void)all_ok(d, true); }
 }  // namespace
 
 Push* push_create(const spmvtk_dist& d, const dev::Matrix& shard, spmvtk_kernel kernel,
@@ -269,7 +277,8 @@ Push* push_create(const spmvtk_dist& d, const dev::Matrix& shard, spmvtk_kernel 
       throw Error(ErrorCode::Validation, "push exchange: rank " + std::to_string(w) +
                                              " could not share its buffers");
   p->peer.resize(static_cast<std::size_t>(d.world));
-  for (int w = 0; w < d.world; ++w) {
+  std::string open_error;
+  for (int w = 0; w < d.world && open_error.empty(); ++w) {
     for (int b = 0; b < 3; ++b) {
       if (w == d.rank) {
         p->peer[static_cast<std::size_t>(w)][static_cast<std::size_t>(b)] = p->own[b];
@@ -280,12 +289,20 @@ Push* push_create(const spmvtk_dist& d, const dev::Matrix& shard, spmvtk_kernel 
                           static_cast<std::size_t>(b) * SPMVTK_IPC_HANDLE_BYTES,
                   sizeof(h));
       void* ptr = nullptr;
-      rt::check(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess),
-                "cudaIpcOpenMemHandle");
+      const cudaError_t e = cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess);
+      if (e != cudaSuccess) {
+        cudaGetLastError();
+        open_error = std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(e);
+        break;
+      }
       p->opened.push_back(ptr);
       p->peer[static_cast<std::size_t>(w)][static_cast<std::size_t>(b)] = ptr;
     }
   }
+  if (!all_ok(d, open_error.empty()))
+    throw Error(ErrorCode::Validation,
+                "push exchange: a rank could not map its peers' buffers" +
+                    (open_error.empty() ? std::string() : " (here: " + open_error + ")"));
   if (sparse && d.world > 1) {  // which ranks read each of my rows
     rt::DevArray<std::uint8_t> need(static_cast<std::size_t>(std::max<std::int64_t>(p->n, 1)),
                                     "push mask");
@@ -373,7 +390,7 @@ double push_iterate(Push& p, double* x, std::int64_t steps) {
                    "push drain");
   std::uint32_t status = 0;
   rt::copy_to_host(&status, p.status.get(), 4);
-  if (status != 0)
+  if (!all_ok(d, status == 0))  // agreed, so no rank is left in the broadcasts below
     throw Error(ErrorCode::Validation, "push exchange: a step flag wait timed out");
   // x_steps: own rows from my buffer, the other blocks from their owners
   // (with the sparse mask a buffer only holds the rows this rank reads)
