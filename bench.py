@@ -65,6 +65,66 @@ def ncu_traffic(config: int, kernel: str):
     return None
 
 
+def ncu_probe_main(args) -> int:
+    """`bench.py --ncu-probe FORMAT`: the config's matrix in FORMAT, then two
+    SpMVs of it (a warm-up and the captured one) -- the process ncu profiles
+    for roofline.traffic."""
+    import torch
+
+    from paper_2407_00019_b200 import spmvtk as sp
+    torch.cuda.set_device(0)
+    sp.set_stream(torch.cuda.current_stream().cuda_stream)
+    m = sp.HostCrs(args.config, args.param, 0.0, args.seed).upload()
+    hname, kname = {name: (h, k) for name, h, k in SPMV_KINDS}[args.ncu_probe]
+    fmt = {"crs": None, "coo-row": "COO_ROW", "coo-col": "COO_COL", "ell": "ELL",
+           "ell-row": "ELL_ROWMAJOR"}[hname]
+    h = m if fmt is None else m.convert(getattr(sp.Format, fmt))
+    n = m.describe().n
+    x = torch.from_numpy(sp.gen_vector(n, args.seed + 1)).cuda()
+    y = torch.empty(n, dtype=torch.float64, device="cuda")
+    for _ in range(2):
+        h.spmv_device(getattr(sp.Kernel, kname), x.data_ptr(), y.data_ptr())
+    torch.cuda.synchronize()
+    return 0
+
+
+def ncu_traffic_live(args, fmt: str, timeout: float = 300.0):
+    """DRAM read+write bytes of one launch of the `fmt` SpMV kernel, captured
+    by ncu in this run (a child process: --ncu-probe; cold caches, as ncu
+    flushes them between kernels), or None when ncu is unavailable/fails."""
+    import shutil
+    import subprocess
+    ncu = shutil.which("ncu") or ("/usr/local/cuda/bin/ncu"
+                                  if os.path.exists("/usr/local/cuda/bin/ncu") else None)
+    if ncu is None:
+        return None
+    cmd = [ncu, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum",
+           "--clock-control", "none", "-k", "regex:k_spmv", "--launch-skip", "1", "-c", "1",
+           "--csv", sys.executable, os.path.join(ROOT, "bench.py"), "--ncu-probe", fmt,
+           "--config", str(args.config), "--param", str(args.param), "--seed", str(args.seed)]
+    try:
+        out = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout).stdout
+        import csv
+        import io
+        rows = [r for r in csv.reader(io.StringIO("\n".join(
+            l for l in out.splitlines() if l.startswith('"')))) if r]
+        hdr = rows[0]
+        ix = {k: i for i, k in enumerate(hdr)}
+        vals, kernel = {}, None
+        for r in rows[1:]:
+            unit = r[ix["Metric Unit"]]
+            v = float(r[ix["Metric Value"]].replace(",", ""))
+            v *= {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-9,
+                  "us": 1e-6, "usecond": 1e-6, "msecond": 1e-3, "nsecond": 1e-9}.get(unit, 1)
+            vals[r[ix["Metric Name"]]] = v
+            kernel = r[ix["Kernel Name"]].split("(")[0]
+        return {"bytes": vals["dram__bytes_read.sum"] + vals["dram__bytes_write.sum"],
+                "read": vals["dram__bytes_read.sum"], "write": vals["dram__bytes_write.sum"],
+                "us": vals.get("gpu__time_duration.sum", 0.0) * 1e6, "kernel": kernel}
+    except Exception:
+        return None
+
+
 def hbm_peak():
     try:
         with open(PEAKS_FILE) as f:
@@ -625,7 +685,16 @@ def impl_ours(args):
         except Exception as e:  # reported, not fatal for the headline
             also["config1_graph"] = {"error": f"{type(e).__name__}: {e}"[:200]}
 
-    traffic = ncu_traffic(args.config, best)
+    # roofline.traffic: one launch of the headline kernel captured by ncu in
+    # this run (after every timed region); the committed capture otherwise
+    live = None if args.no_ncu else ncu_traffic_live(args, best)
+    if live:
+        traffic = (live["bytes"], f"live ncu capture in this run: {live['kernel']}, one launch, "
+                                  f"cold caches, {live['us']:.1f} us under ncu "
+                                  f"(read {live['read'] / 1e6:.1f} MB, write "
+                                  f"{live['write'] / 1e6:.1f} MB)")
+    else:
+        traffic = ncu_traffic(args.config, best)
     line = {
         "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True,
@@ -664,6 +733,9 @@ def main():
     ap.add_argument("--seed", type=int, default=2407)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-also", action="store_true", help="skip the configs 1-3 side tables")
+    ap.add_argument("--no-ncu", action="store_true",
+                    help="roofline.traffic from the committed capture, no live ncu run")
+    ap.add_argument("--ncu-probe", default=None, help=argparse.SUPPRESS)
     ap.add_argument("--force-dist", action="store_true",
                     help="use the row-block/NCCL path even on one rank (testing)")
     args = ap.parse_args()
@@ -671,6 +743,8 @@ def main():
         args.warmup = 3
     if args.param is None:
         args.param = DEFAULT_PARAM[args.config]
+    if args.ncu_probe:
+        return ncu_probe_main(args)
     if args.impl == "reference":
         return impl_reference(args)
     return impl_ours(args)
