@@ -614,7 +614,12 @@ def impl_ours(args):
     t_e2e_sync = (time.perf_counter() - t0) / e2e_steps
     h.spmv_device(k, x.data_ptr(), y.data_ptr())
     torch.cuda.synchronize()
-    assert np.allclose(yn, y.cpu().numpy(), rtol=1e-12, atol=0), "e2e result mismatch"
+    # max-norm relative error (the parity tests' criterion): COO-col adds
+    # through fp64 atomics, so its order of additions -- and single entries
+    # near cancellation -- may differ between two launches
+    yd = y.cpu().numpy()
+    assert np.max(np.abs(yn - yd)) <= 1e-12 * max(np.max(np.abs(yd)), 1e-300), \
+        "e2e result mismatch"
     # streaming: spmvtk_pipeline_submit keeps products in flight, so one
     # product's copy-in, another's SpMV and a third's copy-out overlap (PCIe
     # is full duplex); every step still copies its own x in and its y out
@@ -633,7 +638,9 @@ def impl_ours(args):
         xd = xs[i].cuda()
         h.spmv_device(k, xd.data_ptr(), y.data_ptr())
         torch.cuda.synchronize()
-        assert np.array_equal(ys[i].numpy(), y.cpu().numpy()), "streaming e2e mismatch"
+        yd = y.cpu().numpy()
+        assert np.max(np.abs(ys[i].numpy() - yd)) <= 1e-12 * max(np.max(np.abs(yd)), 1e-300), \
+            "streaming e2e mismatch"
     pipe.free()
 
     # ---- CPU baseline: the reference itself on this host (bounded sample),
