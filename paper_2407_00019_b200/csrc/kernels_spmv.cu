@@ -154,6 +154,57 @@ __global__ void __launch_bounds__(256) k_spmv_vec2(int64_t n, Rows rows,
   y.done();
 }
 
+// W lanes per row, aligned entry QUADS: a lane's four values come in one
+// 256-bit L2-evict-first load, its four columns in one 128-bit load (the
+// base arrays must be 32- / 16-byte aligned: checked at launch).  The row's
+// first (4 - a % 4) % 4 entries are peeled, one per lane.
+template <int W, typename Rows, typename Out = PlainOut>
+__global__ void __launch_bounds__(256) k_spmv_vec4(int64_t n, Rows rows,
+                                                   const int32_t* __restrict__ col,
+                                                   const double* __restrict__ val,
+                                                   const double* __restrict__ x,
+                                                   Out y, int64_t long_limit,
+                                                   int32_t* long_rows) {
+  y.begin();
+  const int lane = threadIdx.x & (W - 1);
+  const unsigned mask = subwarp_mask(W);
+  const int64_t nsub = (static_cast<int64_t>(gridDim.x) * blockDim.x) / W;
+  for (int64_t r = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / W; r < n;
+       r += nsub) {
+    int64_t a, b;
+    rows.get(r, a, b);
+    if (b - a > long_limit) {
+      if (lane == 0) long_rows[1 + atomicAdd(long_rows, 1)] = static_cast<int32_t>(r);
+      continue;
+    }
+    const int32_t len = static_cast<int32_t>(b - a);
+    const int32_t head = min(len, static_cast<int32_t>((4 - (a & 3)) & 3));
+    double acc = 0.0;
+    for (int32_t t = lane; t < head; t += W)
+      acc = fma(ld_stream(val + a + t), ld_x(x + ld_stream(col + a + t)), acc);
+    const double* __restrict__ vr = val + a + head;  // 32-byte aligned
+    const int32_t* __restrict__ cr = col + a + head;
+    const int32_t body = len - head;
+    for (int32_t q = 4 * lane; q < body; q += 4 * W) {
+      if (q + 3 < body) {
+        double2 lo, hi;
+        ld4_stream_first(vr + q, lo, hi);
+        const int4 c = ld_stream4(reinterpret_cast<const int4*>(cr + q));
+        acc = fma(lo.x, ld_x(x + c.x), acc);
+        acc = fma(lo.y, ld_x(x + c.y), acc);
+        acc = fma(hi.x, ld_x(x + c.z), acc);
+        acc = fma(hi.y, ld_x(x + c.w), acc);
+      } else {
+        for (int32_t t = q; t < body; ++t) acc = fma(ld_stream(vr + t), ld_x(x + ld_stream(cr + t)), acc);
+      }
+    }
+#pragma unroll
+    for (int o = W / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(mask, acc, o, W);
+    if (lane == 0) y.put(r, acc);
+  }
+  y.done();
+}
+
 // block per long row (queue filled by k_spmv_vec / k_spmv_multi)
 template <typename Out = PlainOut>
 __global__ void __launch_bounds__(256) k_spmv_crs_long(const int32_t* __restrict__ irp,
@@ -576,9 +627,13 @@ int g_crs_variant = -1;  // tuning override (spmvtk_k_tune), -1 = heuristic
 
 // The sub-warp CRS kernels (row-major ELL runs the same code on fixed-stride
 // rows).  Variants: 12 = k_spmv_vec<4,2> (scalar loads), 16/17/18 =
-// k_spmv_vec2 with 8/16/4 lanes per row (128-bit entry pairs).  Measured on
-// B200 (profiles/r01_tune_crs*.txt): few lanes per row (more rows in flight)
-// win unless rows are long; pair loads from ~6 entries per row up.
+// k_spmv_vec2 with 8/16/4 lanes per row (128-bit entry pairs), 21/22/23/24 =
+// k_spmv_vec4 with 4/8/2/16 lanes (256-bit evict-first value quads).
+// Measured on B200 (profiles/r01_tune_crs*.txt, r02_tune_spmv_quads.txt):
+// few lanes per row (more rows in flight) win unless rows are long; pair
+// loads from ~6 entries per row up; quads with 8 lanes for rows of ~32
+// (config 5 at D = 0: 286 -> 269 us) and for row-major ELL with nz % 4 == 0
+// (config 2, nz = 24: 91 -> 83 us).
 template <typename Rows, typename Out>
 void dispatch_vec(double mean, int64_t max_row, int64_t n, Rows rows, const int32_t* col,
                   const double* val, const double* x, Out y, int64_t long_limit,
@@ -588,13 +643,35 @@ void dispatch_vec(double mean, int64_t max_row, int64_t n, Rows rows, const int3
     if (static_cast<double>(max_row) > 8.0 * mean + 8.0) v = 16;  // skewed: W=8 pairs
     else if (mean <= 6.0) v = 12;                               // W=4 scalar
     else if (mean <= 30.0) v = 18;                              // W=4 pairs
-    else if (mean <= 64.0) v = 16;                              // W=8 pairs
+    else if (mean <= 64.0) v = 22;                              // W=8 quads
     else v = 17;                                                // W=16 pairs
     if constexpr (!std::is_same_v<Rows, CrsRows>) {
+      // row-major ELL: rows of exactly nz slots; when nz % 4 == 0 every row
+      // starts on a quad, so the quad kernel has no peeled entries
+      if (max_row % 4 == 0 && max_row >= 12 && max_row <= 64) v = max_row <= 16 ? 21 : 22;
       if (g_rm_variant >= 0) v = g_rm_variant;
     }
   }
+  const bool quads = (reinterpret_cast<uintptr_t>(val) & 31) == 0 &&
+                     (reinterpret_cast<uintptr_t>(col) & 15) == 0;
+  if (!quads && v >= 21 && v <= 24) v = 18;
   switch (v) {
+    case 21:
+      k_spmv_vec4<4, Rows, Out><<<grid_for(n * 4, 256, 8), 256, 0, s>>>(
+          n, rows, col, val, x, y, long_limit, long_rows);
+      break;
+    case 22:
+      k_spmv_vec4<8, Rows, Out><<<grid_for(n * 8, 256, 8), 256, 0, s>>>(
+          n, rows, col, val, x, y, long_limit, long_rows);
+      break;
+    case 23:
+      k_spmv_vec4<2, Rows, Out><<<grid_for(n * 2, 256, 8), 256, 0, s>>>(
+          n, rows, col, val, x, y, long_limit, long_rows);
+      break;
+    case 24:
+      k_spmv_vec4<16, Rows, Out><<<grid_for(n * 16, 256, 8), 256, 0, s>>>(
+          n, rows, col, val, x, y, long_limit, long_rows);
+      break;
     case 12:
       k_spmv_vec<4, 2, Rows, Out><<<grid_for(n * 4, 256, 8), 256, 0, s>>>(
           n, rows, col, val, x, y, long_limit, long_rows);

@@ -1,4 +1,7 @@
-"""Times row-major ELL SpMV variants (spmvtk_k_tune("rm_variant", v))."""
+"""Times row-major ELL SpMV variants (spmvtk_k_tune("rm_variant", v)).
+
+    python tools/tune_rm.py [-1,12,16,...]
+"""
 import os
 import sys
 
@@ -18,7 +21,7 @@ for cfg, param in ((2, 1 << 20), (3, 128), (5, 1 << 21)):
     x = torch.rand(d.n, dtype=torch.float64, device="cuda")
     y = torch.empty_like(x)
     b = 12 * d.n * nz + 16 * d.n
-    for v in (-1, 11, 12, 0, 15, 16, 17, 18, 19):
+    for v in [int(t) for t in (sys.argv[1] if len(sys.argv) > 1 else "-1,12,16,17,18,21,22,23,24").split(",")]:
         lib.spmvtk_k_tune(b"rm_variant", v)
         for _ in range(5):
             e.spmv_device(sp.Kernel.ELL_ROWMAJOR, x.data_ptr(), y.data_ptr())
