@@ -172,6 +172,9 @@ int spmvtk_k_spmv_crs_seg(const int32_t* irp, const int32_t* icol, const double*
                           int64_t nnz, void* stream);
 /* The CRS kernel choice: 1 = segmented (plan needed), 0 = sub-warp per row. */
 int spmvtk_k_crs_use_seg(double mean_row, int64_t max_row);
+/* ell-outer's band chunks when forced through spmvtk_k_tune("ell_splits", k)
+ * (0 = chosen by occupancy: split only when row pairs cannot fill the GPU). */
+int spmvtk_k_ell_splits_forced(void);
 /* Row length above which spmvtk_k_spmv_crs hands a row to the block-per-row
  * pass (long_rows must then be non-NULL when max_row exceeds it). */
 int64_t spmvtk_k_crs_long_limit(double mean_row);

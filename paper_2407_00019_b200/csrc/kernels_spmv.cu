@@ -624,6 +624,7 @@ void coo_row4_capacity() {
 }
 int g_rm_variant = -1;  // row-major ELL variant override (tuning)
 int g_crs_variant = -1;  // tuning override (spmvtk_k_tune), -1 = heuristic
+int g_ell_splits = 0;    // ell-outer band chunks forced (0 = by occupancy)
 
 // The sub-warp CRS kernels (row-major ELL runs the same code on fixed-stride
 // rows).  Variants: 12 = k_spmv_vec<4,2> (scalar loads), 16/17/18 =
@@ -875,10 +876,12 @@ int spmvtk_k_crs_use_seg(double mean_row, int64_t max_row) {
   if (g_crs_variant >= 0) return g_crs_variant == 20 ? 1 : 0;
   // row-skewed matrices (power-law rows, config 4): the entry-balanced kernel
   // (366 vs 436 us on config 4); otherwise the sub-warp kernels win (config 2
-  // 93 vs 95, config 3 135 vs 230, config 5 286 vs 314 us;
-  // profiles/r02_tune_spmv_seg.txt)
+  // 93 vs 95, config 3 135 vs 230, config 5 269 (quads) vs 303 us;
+  // profiles/r02_tune_spmv_seg.txt, r02_tune_spmv_quads.txt)
   return (static_cast<double>(max_row) > 8.0 * mean_row + 8.0 && mean_row >= 4.0) ? 1 : 0;
 }
+
+int spmvtk_k_ell_splits_forced(void) { return g_ell_splits; }
 
 int64_t spmvtk_k_crs_long_limit(double mean_row) {
   // rows this much longer than average would serialise one sub-warp: they go
@@ -899,6 +902,10 @@ int spmvtk_k_tune(const char* key, int value) {
   if (key && std::string(key) == "coo_chunk") {  // <= 0: automatic
     g_coo_chunk_auto = value <= 0;
     g_coo_chunk = value >= 128 ? (value / 128) * 128 : 2048;
+    return 0;
+  }
+  if (key && std::string(key) == "ell_splits") {  // force ell-outer's band chunks (testing)
+    g_ell_splits = value > 0 ? value : 0;
     return 0;
   }
   if (key && std::string(key) == "seg_chunk") {

@@ -86,6 +86,8 @@ Matrix* derived(const Matrix& src, spmvtk_format f, std::int64_t nnz) {
 }
 
 int ell_splits(std::int64_t n, std::int32_t nz) {
+  if (const int forced = spmvtk_k_ell_splits_forced(); forced > 0)
+    return std::max(1, std::min<int>(forced, nz));
   // band split only pays when row pairs alone cannot fill 148 SMs x 2048
   const std::int64_t want = 148LL * 2048;
   const std::int64_t pairs = (n + 1) / 2;

@@ -74,6 +74,16 @@ def check_all(sp, port, h, n, rp, ci, v, x, ell=True):
         assert np.array_equal(e.array(sp.Array.ROW_ENTRY_COUNT), cnt)
         for k in (sp.Kernel.ELL_INNER, sp.Kernel.ELL_OUTER):
             assert max_rel_error(e.spmv(x, k)[0], want) <= TOL
+        # ell-outer with its band split forced (spmv_ell_outer's partition of
+        # the bands into chunks + ascending reduction of the partials,
+        # spmv.cpp:138-158): at these sizes the occupancy rule never splits
+        lib = sp.load_library()
+        try:
+            for chunks in (2, 3, 7):
+                assert lib.spmvtk_k_tune(b"ell_splits", chunks) == 0
+                assert max_rel_error(e.spmv(x, sp.Kernel.ELL_OUTER)[0], want) <= TOL, chunks
+        finally:
+            lib.spmvtk_k_tune(b"ell_splits", 0)
         e.free()
         del ev, ec
         er = m.convert(sp.Format.ELL_ROWMAJOR)
