@@ -628,8 +628,9 @@ int g_ell_splits = 0;    // ell-outer band chunks forced (0 = by occupancy)
 
 // The sub-warp CRS kernels (row-major ELL runs the same code on fixed-stride
 // rows).  Variants: 12 = k_spmv_vec<4,2> (scalar loads), 16/17/18 =
-// k_spmv_vec2 with 8/16/4 lanes per row (128-bit entry pairs), 21/22/23/24 =
-// k_spmv_vec4 with 4/8/2/16 lanes (256-bit evict-first value quads).
+// k_spmv_vec2 with 8/16/4 lanes per row (128-bit entry pairs), 21/22 =
+// k_spmv_vec4 with 4/8 lanes (256-bit evict-first value quads; 2 and 16
+// lanes measured slower everywhere, r02_tune_spmv_quads.txt, and removed).
 // Measured on B200 (profiles/r01_tune_crs*.txt, r02_tune_spmv_quads.txt):
 // few lanes per row (more rows in flight) win unless rows are long; pair
 // loads from ~6 entries per row up; quads with 8 lanes for rows of ~32
@@ -655,7 +656,7 @@ void dispatch_vec(double mean, int64_t max_row, int64_t n, Rows rows, const int3
   }
   const bool quads = (reinterpret_cast<uintptr_t>(val) & 31) == 0 &&
                      (reinterpret_cast<uintptr_t>(col) & 15) == 0;
-  if (!quads && v >= 21 && v <= 24) v = 18;
+  if (!quads && (v == 21 || v == 22)) v = 18;
   switch (v) {
     case 21:
       k_spmv_vec4<4, Rows, Out><<<grid_for(n * 4, 256, 8), 256, 0, s>>>(
@@ -663,14 +664,6 @@ void dispatch_vec(double mean, int64_t max_row, int64_t n, Rows rows, const int3
       break;
     case 22:
       k_spmv_vec4<8, Rows, Out><<<grid_for(n * 8, 256, 8), 256, 0, s>>>(
-          n, rows, col, val, x, y, long_limit, long_rows);
-      break;
-    case 23:
-      k_spmv_vec4<2, Rows, Out><<<grid_for(n * 2, 256, 8), 256, 0, s>>>(
-          n, rows, col, val, x, y, long_limit, long_rows);
-      break;
-    case 24:
-      k_spmv_vec4<16, Rows, Out><<<grid_for(n * 16, 256, 8), 256, 0, s>>>(
           n, rows, col, val, x, y, long_limit, long_rows);
       break;
     case 12:
