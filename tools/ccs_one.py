@@ -1,5 +1,6 @@
 """One CRS->CCS (or COO-col) conversion of a BASELINE config after a warm-up,
-for ncu launch lists: python tools/ccs_one.py CONFIG [coo]"""
+for ncu launch lists: python tools/ccs_one.py CONFIG [coo]
+(CCS_KNOBS="name=value,..." sets spmvtk_k_tune knobs first)"""
 import os
 import sys
 
@@ -9,6 +10,9 @@ from paper_2407_00019_b200 import spmvtk as sp  # noqa: E402
 PARAM = {1: 256, 2: 1 << 20, 3: 128, 4: 1 << 22, 5: 1 << 21}
 cfg = int(sys.argv[1])
 fmt = sp.Format.COO_COL if len(sys.argv) > 2 and sys.argv[2] == "coo" else sp.Format.CCS
+for kv in filter(None, os.environ.get("CCS_KNOBS", "").split(",")):
+    k, v = kv.split("=")
+    sp.load_library().spmvtk_k_tune(k.encode(), int(v))
 m = sp.HostCrs(cfg, PARAM[cfg], 0.0).upload()
 m.convert(fmt).free()  # warm-up (pool, module load)
 sp.synchronize()
