@@ -69,6 +69,14 @@ int spmvtk_k_crs_to_coo_row(int64_t n, int64_t nnz, const int32_t* irp,
 int spmvtk_k_count_row_descents(const int32_t* irp, int64_t n, const int32_t* col,
                                 unsigned long long* bad, void* stream);
 
+/* The same pass plus the band shape that picks the SM-local ELL kernel:
+ * out[0] descents, out[1] entries equal to the previous column + 1 of their
+ * row, out[2] max(last column - row) + 2^32, out[3] max(row - first column)
+ * + 2^32 over non-empty rows (row = row_offset + local row; out: device, 4
+ * values, zeroed here). */
+int spmvtk_k_row_order_stats(const int32_t* irp, int64_t n, int64_t row_offset,
+                             const int32_t* col, unsigned long long* out, void* stream);
+
 /* CRS -> CCS Phase I (convert.cpp:24-53).  scratch: device buffer of
  * spmvtk_k_ccs_scratch_bytes(n, nnz) bytes.  Row indices come out ascending
  * inside every column, exactly as the reference's cursor scatter.
@@ -175,6 +183,9 @@ int spmvtk_k_crs_use_seg(double mean_row, int64_t max_row);
 /* ell-outer's band chunks when forced through spmvtk_k_tune("ell_splits", k)
  * (0 = chosen by occupancy: split only when row pairs cannot fill the GPU). */
 int spmvtk_k_ell_splits_forced(void);
+/* The SM-local ELL choice forced by spmvtk_k_tune("ell_banded", v): -1 =
+ * automatic (from the handle's band shape), 0 = never, 1 = always. */
+int spmvtk_k_ell_banded_forced(void);
 /* Row length above which spmvtk_k_spmv_crs hands a row to the block-per-row
  * pass (long_rows must then be non-NULL when max_row exceeds it). */
 int64_t spmvtk_k_crs_long_limit(double mean_row);
@@ -193,6 +204,14 @@ int spmvtk_k_spmv_coo_col(int64_t n, int64_t nnz, const int32_t* row,
 int spmvtk_k_spmv_ell_cm(int64_t n, int32_t nz, int64_t ld, const double* val,
                          const int32_t* col, const double* x, double* y,
                          void* stream);
+/* The same product for banded matrices whose columns scatter inside a band
+ * window of x (one 1024-thread CTA per SM, each sweeping one contiguous row
+ * region, so an SM's gathers stay inside one window that L1 holds).  Picked
+ * by the library from the handle's band shape; same results as
+ * spmvtk_k_spmv_ell_cm (each row summed band by band in the same order). */
+int spmvtk_k_spmv_ell_cm_banded(int64_t n, int32_t nz, int64_t ld, const double* val,
+                                const int32_t* col, const double* x, double* y,
+                                void* stream);
 /* spmv_ell_outer (spmv.cpp:138-158): bands split in `splits` contiguous
  * chunks (partition_range rule), per-chunk partial vectors in `partial`
  * (device, splits*n doubles), then an ascending-chunk reduction. */

@@ -28,6 +28,9 @@ __device__ __forceinline__ unsigned subwarp_mask(int W) {
   return ((1u << W) - 1u) << (lane & ~(W - 1));
 }
 
+int g_crs_rowlocal = 0;  // EXPERIMENT: thread-per-row SM-local CRS (threads per CTA)
+int g_ell_banded = -1;  // tuning: SM-local band-major ELL (-1 auto from the band shape)
+
 // ---- vector CRS: W lanes per row (spmv_crs, spmv.cpp:64-75) --------------
 // Row extents come from a policy so the same kernel serves CRS (irp) and
 // row-major ELL (fixed stride nz).  Rows longer than long_limit are handed to
@@ -203,6 +206,49 @@ __global__ void __launch_bounds__(256) k_spmv_vec4(int64_t n, Rows rows,
     if (lane == 0) y.put(r, acc);
   }
   y.done();
+}
+
+// EXPERIMENT (knob crs_rowlocal = threads per CTA): one thread per row,
+// one CTA per SM sweeping a contiguous row region, the row stream read with
+// L1-allocating loads (a thread re-reads its row's lines), so a CTA's
+// threads walk their rows' entries roughly in step (band order) and the x
+// gathers of a banded matrix stay inside an L1-resident slice.
+template <int BS>
+__global__ void __launch_bounds__(BS) k_spmv_crs_rowlocal(int64_t n,
+                                                          const int32_t* __restrict__ irp,
+                                                          const int32_t* __restrict__ col,
+                                                          const double* __restrict__ val,
+                                                          const double* __restrict__ x,
+                                                          double* __restrict__ y) {
+  const int64_t per = ((n + gridDim.x - 1) / gridDim.x + BS - 1) / BS * BS;
+  const int64_t r_end = min(n, static_cast<int64_t>(blockIdx.x + 1) * per);
+  for (int64_t r = static_cast<int64_t>(blockIdx.x) * per + threadIdx.x; r < r_end; r += BS) {
+    int32_t p = __ldg(irp + r);
+    const int32_t b = __ldg(irp + r + 1);
+    double acc = 0.0;
+    for (; p < b && (p & 3); ++p) acc = fma(__ldg(val + p), ld_x(x + __ldg(col + p)), acc);
+    for (; p + 8 <= b; p += 8) {
+      const int4 c0 = __ldg(reinterpret_cast<const int4*>(col + p));
+      const int4 c1 = __ldg(reinterpret_cast<const int4*>(col + p + 4));
+      const double2 v0 = __ldg(reinterpret_cast<const double2*>(val + p));
+      const double2 v1 = __ldg(reinterpret_cast<const double2*>(val + p + 2));
+      const double2 v2 = __ldg(reinterpret_cast<const double2*>(val + p + 4));
+      const double2 v3 = __ldg(reinterpret_cast<const double2*>(val + p + 6));
+      const double g0 = ld_x(x + c0.x), g1 = ld_x(x + c0.y), g2 = ld_x(x + c0.z),
+                   g3 = ld_x(x + c0.w), g4 = ld_x(x + c1.x), g5 = ld_x(x + c1.y),
+                   g6 = ld_x(x + c1.z), g7 = ld_x(x + c1.w);
+      acc = fma(v0.x, g0, acc);
+      acc = fma(v0.y, g1, acc);
+      acc = fma(v1.x, g2, acc);
+      acc = fma(v1.y, g3, acc);
+      acc = fma(v2.x, g4, acc);
+      acc = fma(v2.y, g5, acc);
+      acc = fma(v3.x, g6, acc);
+      acc = fma(v3.y, g7, acc);
+    }
+    for (; p < b; ++p) acc = fma(__ldg(val + p), ld_x(x + __ldg(col + p)), acc);
+    y[r] = acc;
+  }
 }
 
 // block per long row (queue filled by k_spmv_vec / k_spmv_multi)
@@ -553,6 +599,71 @@ __global__ void __launch_bounds__(256) k_spmv_ell_cm(int64_t n, int32_t k_begin,
   }
 }
 
+// Banded matrices (SM-local regions): ONE 1024-thread CTA per SM (grid =
+// kSMs; the block scheduler places them breadth-first, one per SM), each CTA
+// sweeping one contiguous region of rows.  A band-major ELL thread walks its
+// rows band by band, so at any moment an SM's threads gather band k of a few
+// thousand consecutive rows: for columns scattered inside a band window of
+// x (config 5) those gathers stay inside a slice of x that L1 holds, instead
+// of the interleaved grid's 8 CTAs per SM each pulling a different window
+// through L2 (config 5 D = 0: L1 sector hit rate 14 % -> 51 %, L2 requests
+// 58.7 M -> 25.8 M).  R rows per thread: 2 (double2 / int2 loads) or 4 (one
+// 256-bit value load and one int4 column load per band).
+template <int U, int R>
+__global__ void __launch_bounds__(1024) k_spmv_ell_cm_local(int64_t n, int32_t nz, int64_t ld,
+                                                            const double* __restrict__ val,
+                                                            const int32_t* __restrict__ col,
+                                                            const double* __restrict__ x,
+                                                            double* __restrict__ y) {
+  const int64_t groups = (n + R - 1) / R;
+  const int64_t per = ((groups + gridDim.x - 1) / gridDim.x + blockDim.x - 1) / blockDim.x *
+                      blockDim.x;
+  const int64_t g_end = min(groups, static_cast<int64_t>(blockIdx.x + 1) * per);
+  for (int64_t g = static_cast<int64_t>(blockIdx.x) * per + threadIdx.x; g < g_end;
+       g += blockDim.x) {
+    const int64_t i = R * g;
+    if constexpr (R == 2) {
+      double a0, a1;
+      ell_pair<U>(i, 0, nz, ld, val, col, x, a0, a1);
+      y[i] = a0;
+      if (i + 1 < n) y[i + 1] = a1;
+    } else {
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      int32_t k = 0;
+      for (; k + U <= nz; k += U) {
+        double2 lo[U], hi[U];
+        int4 c[U];
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+          const int64_t off = static_cast<int64_t>(k + j) * ld + i;
+          ld4_stream_first(val + off, lo[j], hi[j]);
+          c[j] = ld_stream4(reinterpret_cast<const int4*>(col + off));
+        }
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+          acc[0] = fma(lo[j].x, ld_x(x + c[j].x), acc[0]);
+          acc[1] = fma(lo[j].y, ld_x(x + c[j].y), acc[1]);
+          acc[2] = fma(hi[j].x, ld_x(x + c[j].z), acc[2]);
+          acc[3] = fma(hi[j].y, ld_x(x + c[j].w), acc[3]);
+        }
+      }
+      for (; k < nz; ++k) {
+        const int64_t off = static_cast<int64_t>(k) * ld + i;
+        double2 lo, hi;
+        ld4_stream_first(val + off, lo, hi);
+        const int4 c = ld_stream4(reinterpret_cast<const int4*>(col + off));
+        acc[0] = fma(lo.x, ld_x(x + c.x), acc[0]);
+        acc[1] = fma(lo.y, ld_x(x + c.y), acc[1]);
+        acc[2] = fma(hi.x, ld_x(x + c.z), acc[2]);
+        acc[3] = fma(hi.y, ld_x(x + c.w), acc[3]);
+      }
+#pragma unroll
+      for (int h = 0; h < 4; ++h)
+        if (i + h < n) y[i + h] = acc[h];
+    }
+  }
+}
+
 // band-split variant (spmv_ell_outer): chunk s of the bands writes
 // partial[s*n + i]; then an ascending-chunk reduction (reduce_partials,
 // spmv.cpp:56-62) makes the result independent of scheduling.
@@ -695,6 +806,19 @@ int spmvtk_k_spmv_crs(int64_t n, const int32_t* irp, const int32_t* icol, const 
                       int32_t* long_rows, void* stream) {
   cudaStream_t s = as_stream(stream);
   if (n <= 0) SPMVTK_LAUNCH_RETURN();
+  if (g_crs_rowlocal > 0 && (reinterpret_cast<uintptr_t>(val) & 15) == 0 &&
+      (reinterpret_cast<uintptr_t>(icol) & 15) == 0) {
+    if (g_crs_rowlocal == 1024)
+      k_spmv_crs_rowlocal<1024><<<kSMs, 1024, 0, s>>>(n, irp, icol, val, x, y);
+    else if (g_crs_rowlocal == 512)
+      k_spmv_crs_rowlocal<512><<<kSMs, 512, 0, s>>>(n, irp, icol, val, x, y);
+    else if (g_crs_rowlocal == 2048)  // two 1024-thread CTAs per SM (interleaved regions)
+      k_spmv_crs_rowlocal<1024><<<kSMs * 2, 1024, 0, s>>>(n, irp, icol, val, x, y);
+    else
+      k_spmv_crs_rowlocal<256><<<kSMs, 256, 0, s>>>(n, irp, icol, val, x, y);
+    count_launches(1);
+    SPMVTK_LAUNCH_RETURN();
+  }
   const int64_t long_limit = spmvtk_k_crs_long_limit(mean_row);
   const bool use_long = long_rows != nullptr && max_row > long_limit;
   if (use_long) cudaMemsetAsync(long_rows, 0, sizeof(int32_t), s);
@@ -826,6 +950,21 @@ int spmvtk_k_spmv_ell_cm(int64_t n, int32_t nz, int64_t ld, const double* val,
   SPMVTK_LAUNCH_RETURN();
 }
 
+int spmvtk_k_spmv_ell_cm_banded(int64_t n, int32_t nz, int64_t ld, const double* val,
+                                const int32_t* col, const double* x, double* y, void* stream) {
+  cudaStream_t s = as_stream(stream);
+  if (n <= 0) SPMVTK_LAUNCH_RETURN();
+  if (nz == 0) {
+    cudaMemsetAsync(y, 0, static_cast<size_t>(n) * sizeof(double), s);
+    SPMVTK_LAUNCH_RETURN();
+  }
+  // 46 registers x 1024 threads: one CTA per SM, so the kSMs CTAs land on
+  // distinct SMs (four rows per thread with 256-bit loads measured no faster)
+  k_spmv_ell_cm_local<4, 2><<<kSMs, 1024, 0, s>>>(n, nz, ld, val, col, x, y);
+  count_launches(1);
+  SPMVTK_LAUNCH_RETURN();
+}
+
 int spmvtk_k_spmv_ell_cm_push(int64_t n, int32_t nz, int64_t ld, const double* val,
                               const int32_t* col, const double* x, const spmvtk_push* push,
                               const spmvtk_push_sync* sync, void* stream) {
@@ -875,6 +1014,7 @@ int spmvtk_k_crs_use_seg(double mean_row, int64_t max_row) {
 }
 
 int spmvtk_k_ell_splits_forced(void) { return g_ell_splits; }
+int spmvtk_k_ell_banded_forced(void) { return g_ell_banded; }
 
 int64_t spmvtk_k_crs_long_limit(double mean_row) {
   // rows this much longer than average would serialise one sub-warp: they go
@@ -884,6 +1024,14 @@ int64_t spmvtk_k_crs_long_limit(double mean_row) {
 }
 
 int spmvtk_k_tune(const char* key, int value) {
+  if (key && std::string(key) == "crs_rowlocal") {  // EXPERIMENT: threads per CTA (0 = off)
+    g_crs_rowlocal = value;
+    return 0;
+  }
+  if (key && std::string(key) == "ell_banded") {  // SM-local ELL: -1 auto, 0 never, 1 always
+    g_ell_banded = value < 0 ? -1 : value > 0 ? 1 : 0;
+    return 0;
+  }
   if (key && std::string(key) == "crs_variant") {
     g_crs_variant = value;
     return 0;

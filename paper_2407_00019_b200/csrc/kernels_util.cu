@@ -5,6 +5,8 @@
 // SMs, warp-shuffle reductions, one atomic per warp.
 #include <atomic>
 
+#include <climits>
+
 #include "common.cuh"
 #include "spmvtk/spmvtk.h"
 #include "spmvtk/spmvtk_kernels.h"
@@ -183,6 +185,58 @@ __global__ void k_row_descents(const int32_t* __restrict__ irp, int64_t n,
   }
   cnt = warp_sum(cnt);
   if (lane == 0 && cnt) atomicAdd(bad, cnt);
+}
+
+// Row order + band shape of a CRS in one pass over its columns (the upload's
+// ordering check, extended): out[0] descents (as k_row_descents), out[1]
+// entries whose column is the previous column + 1 in the same row (stencil-
+// like runs), out[2] max over rows of (last column - global row) + 2^32,
+// out[3] max of (global row - first column) + 2^32 (offsets keep the atomics
+// unsigned; empty rows contribute nothing).
+__global__ void k_row_order_stats(const int32_t* __restrict__ irp, int64_t n, int64_t row0,
+                                  const int32_t* __restrict__ col, unsigned long long* out) {
+  unsigned long long desc = 0, adj = 0;
+  long long right = LLONG_MIN, left = LLONG_MIN;
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t r0 = ((static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * 32;
+       r0 < n; r0 += warps * 32) {
+    const int64_t r1 = r0 + 32 < n ? r0 + 32 : n;
+    const int32_t a = __ldg(irp + r0), b = __ldg(irp + r1);
+    const int32_t end = r0 + lane < r1 ? __ldg(irp + r0 + lane + 1) : INT_MAX;
+    if (r0 + lane < r1) {  // lane's own row: first and last column
+      const int32_t beg = __ldg(irp + r0 + lane);
+      if (end > beg) {
+        const long long g = row0 + r0 + lane;
+        right = max(right, static_cast<long long>(__ldg(col + end - 1)) - g);
+        left = max(left, g - static_cast<long long>(__ldg(col + beg)));
+      }
+    }
+    for (int32_t p0 = a; p0 < b; p0 += 32) {
+      const unsigned bit = (end >= p0 && end < p0 + 32) ? 1u << (end - p0) : 0u;
+      const unsigned starts = __reduce_or_sync(kFull, bit);
+      const int32_t p = p0 + lane;
+      if (p > a && p < b && !((starts >> lane) & 1u)) {
+        const int32_t c = __ldg(col + p), cp = __ldg(col + p - 1);
+        desc += c <= cp;
+        adj += c == cp + 1;
+      }
+    }
+  }
+  desc = warp_sum(desc);
+  adj = warp_sum(adj);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    right = max(right, __shfl_xor_sync(kFull, right, o));
+    left = max(left, __shfl_xor_sync(kFull, left, o));
+  }
+  if (lane == 0) {
+    if (desc) atomicAdd(out, desc);
+    if (adj) atomicAdd(out + 1, adj);
+    const long long off = 1LL << 32;
+    if (right != LLONG_MIN) atomicMax(out + 2, static_cast<unsigned long long>(right + off));
+    if (left != LLONG_MIN) atomicMax(out + 3, static_cast<unsigned long long>(left + off));
+  }
 }
 
 // ---- exclusive scan (tiles of 4096) -----------------------------------------
@@ -453,6 +507,16 @@ int spmvtk_k_count_row_descents(const int32_t* irp, int64_t n, const int32_t* co
   cudaStream_t s = as_stream(stream);
   cudaMemsetAsync(bad, 0, sizeof(unsigned long long), s);
   if (n > 0) k_row_descents<<<grid_for((n + 31) / 32 * 32, 256, 16), 256, 0, s>>>(irp, n, col, bad);
+  SPMVTK_LAUNCH_RETURN();
+}
+
+int spmvtk_k_row_order_stats(const int32_t* irp, int64_t n, int64_t row_offset,
+                             const int32_t* col, unsigned long long* out, void* stream) {
+  cudaStream_t s = as_stream(stream);
+  cudaMemsetAsync(out, 0, 4 * sizeof(unsigned long long), s);
+  if (n > 0)
+    k_row_order_stats<<<grid_for((n + 31) / 32 * 32, 256, 16), 256, 0, s>>>(irp, n, row_offset,
+                                                                            col, out);
   SPMVTK_LAUNCH_RETURN();
 }
 

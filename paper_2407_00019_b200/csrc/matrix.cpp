@@ -178,15 +178,43 @@ void spmv_crs_rows(const Matrix& m, const double* x, double* y, std::int64_t r0,
 bool pairs_ascending(const Matrix& m) {
   std::lock_guard<std::mutex> lk(m.mu);
   if (!m.pairs_ascending) {
+    // one pass: ordering (the fast CCS pipeline's precondition) and, for a
+    // CRS, the band shape (the SM-local ELL kernel's)
     const DevArray<std::int32_t>& idx = m.format == SPMVTK_FORMAT_CCS ? m.row : m.col;
-    DevArray<unsigned long long> bad(1, "ordering check");
-    rt::check_launch(spmvtk_k_count_row_descents(m.ptr.get(), m.n, idx.get(), bad.get(), s()),
+    DevArray<unsigned long long> out(4, "ordering check");
+    rt::check_launch(spmvtk_k_row_order_stats(m.ptr.get(), m.n, m.row_offset, idx.get(),
+                                              out.get(), s()),
                      "ordering check");
-    unsigned long long h = 0;
-    rt::copy_to_host(&h, bad.get(), sizeof(h));
-    m.pairs_ascending = h == 0;
+    unsigned long long h[4] = {0, 0, 0, 0};
+    rt::copy_to_host(h, out.get(), sizeof(h));
+    m.pairs_ascending = h[0] == 0;
+    if (m.format == SPMVTK_FORMAT_CRS && h[2] != 0 && h[3] != 0) {
+      const long long off = 1LL << 32;
+      m.band = Matrix::BandShape{static_cast<long long>(h[2]) - off,
+                                 static_cast<long long>(h[3]) - off, h[1]};
+    }
   }
   return *m.pairs_ascending;
+}
+
+// Band-major ELL of a banded matrix whose columns scatter inside the band:
+// the SM-local kernel (one CTA per SM sweeping a row region) keeps each SM's
+// x gathers inside one band window that L1 holds.  Measured on configs 1-5
+// (profiles/r02_ell_banded.txt): config 5 at D = 0 240 -> 157 us, at D = 0.1
+// 274 -> 238 us; slower where the interleaved grid already has locality
+// (stencil runs of adjacent columns, config 3), where padding makes the
+// product a stream (D >= 0.2), on random columns (config 2) and small n.
+bool ell_banded(const Matrix& m) {
+  const int forced = spmvtk_k_ell_banded_forced();
+  if (forced >= 0) return forced == 1;
+  if (!m.band) return false;
+  const Matrix::BandShape& b = *m.band;
+  const std::int64_t window = b.right + b.left + 1;
+  const double slots = static_cast<double>(m.n) * m.band_count;
+  return m.n >= std::int64_t(148) * 2048 && window > 4096 &&
+         window <= (std::int64_t(1) << 17) &&
+         b.adjacent * 8 < static_cast<std::uint64_t>(m.nnz) &&
+         slots <= 1.6 * static_cast<double>(m.nnz);
 }
 
 namespace {
@@ -438,6 +466,10 @@ Matrix* convert(const Matrix& a, spmvtk_format to, std::uint64_t max_bytes) {
       std::unique_ptr<Matrix> m(derived(a, to, nnz));
       m->band_count = nz;
       m->ld = cm ? round_up(n, 32) : n;
+      {
+        std::lock_guard<std::mutex> lk(a.mu);
+        m->band = a.band;  // measured at upload (pairs_ascending): no work here
+      }
       const std::size_t slots =
           static_cast<std::size_t>(cm ? m->ld : n) * static_cast<std::size_t>(nz);
       // values | col_idx | row_entry_count in one allocation
@@ -660,8 +692,8 @@ void spmv_device(const Matrix& m, spmvtk_kernel kernel, const double* x, double*
       if (m.format != SPMVTK_FORMAT_ELL)
         throw Error(ErrorCode::InvalidArgument, "kernel requires an ELL handle");
       if (kernel == SPMVTK_KERNEL_ELL_INNER) {
-        rt::check_launch(spmvtk_k_spmv_ell_cm(m.n, m.band_count, m.ld, m.val.get(), m.col.get(),
-                                              x, y, st),
+        rt::check_launch((ell_banded(m) ? spmvtk_k_spmv_ell_cm_banded : spmvtk_k_spmv_ell_cm)(
+                             m.n, m.band_count, m.ld, m.val.get(), m.col.get(), x, y, st),
                          "spmv ell-inner");
       } else {
         int splits = ell_splits(m.n, m.band_count);

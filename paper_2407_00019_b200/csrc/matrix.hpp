@@ -48,6 +48,14 @@ struct spmvtk_matrix {
   // CRS / CCS: columns (rows) strictly ascending inside every row (column),
   // hence no duplicate pairs -- the fast CCS pipeline's precondition
   mutable std::optional<bool> pairs_ascending;
+  // CRS (and the ELL built from it): band shape from the same pass --
+  // max(last column - row), max(row - first column), entries that continue
+  // a run of consecutive columns; picks the SM-local ELL kernel
+  struct BandShape {
+    std::int64_t right = 0, left = 0;
+    std::uint64_t adjacent = 0;
+  };
+  mutable std::optional<BandShape> band;
 
   std::uint64_t device_bytes() const {
     return val.bytes() + ptr.bytes() + row.bytes() + col.bytes() + count.bytes();

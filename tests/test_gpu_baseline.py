@@ -245,6 +245,17 @@ def test_config_5_full_size_properties(gpu, d):
     assert np.array_equal(cnt, np.diff(rp))
     for k in (sp.Kernel.ELL_INNER, sp.Kernel.ELL_OUTER):
         assert max_rel_error(e.spmv(x, k)[0], y0) <= TOL
+    # ELL-inner with the SM-local kernel (chosen automatically for the
+    # scattered band of D <= 0.1) and with the interleaved one: bitwise equal
+    lib = sp.load_library()
+    yi = {}
+    for force in (0, 1):
+        assert lib.spmvtk_k_tune(b"ell_banded", force) == 0
+        try:
+            yi[force] = e.spmv(x, sp.Kernel.ELL_INNER)[0]
+        finally:
+            lib.spmvtk_k_tune(b"ell_banded", -1)
+    assert yi[0].tobytes() == yi[1].tobytes()
     e.free()
     c = m.convert(sp.Format.COO_COL)
     assert max_rel_error(c.spmv(x, sp.Kernel.COO_COL_OUTER)[0], y0) <= TOL

@@ -64,6 +64,16 @@ def test_spmv_kernels_stay_inside_x_and_y(gpu, port, kind, n):
         finally:
             lib.spmvtk_k_tune(b"crs_variant", -1)
         assert max_rel_error(y, want) <= 1e-12, (kind, n, variant)
+    # the SM-local band-major ELL kernel (banded matrices), forced: bitwise
+    # the default ELL kernel's result (same per-row band order)
+    ell = handles[3][0]
+    y_def = _guarded_spmv(torch, ell, sp.Kernel.ELL_INNER, x, n)
+    assert lib.spmvtk_k_tune(b"ell_banded", 1) == 0
+    try:
+        y_loc = _guarded_spmv(torch, ell, sp.Kernel.ELL_INNER, x, n)
+    finally:
+        lib.spmvtk_k_tune(b"ell_banded", -1)
+    assert y_loc.tobytes() == y_def.tobytes(), (kind, n, "ell_banded")
     # the row-major ELL variants (the sub-warp kernels on fixed-stride rows)
     rm = handles[-1][0]
     for variant in (12, 16, 17, 18, 21, 22):
