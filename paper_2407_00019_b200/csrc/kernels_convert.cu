@@ -808,13 +808,37 @@ __global__ void __launch_bounds__(256) k_crs_to_ell_cm(int64_t n, int32_t nz, in
   __shared__ int32_t s_ptr[R + 1];
   __shared__ double s_v[R][KC + 1];
   __shared__ int32_t s_c[R][KC + 1];
+  __shared__ int32_t s_maxlen;
   const int64_t r0 = static_cast<int64_t>(blockIdx.x) * R;
+  if (threadIdx.x == 0) s_maxlen = 0;
   for (int t = threadIdx.x; t <= R; t += blockDim.x)
     s_ptr[t] = __ldg(irp + min(r0 + t, n));
   __syncthreads();
-  for (int t = threadIdx.x; t < R; t += blockDim.x)
-    if (r0 + t < n) out_count[r0 + t] = s_ptr[t + 1] - s_ptr[t];
+  for (int t = threadIdx.x; t < R; t += blockDim.x) {
+    const int32_t len = s_ptr[t + 1] - s_ptr[t];
+    if (r0 + t < n) out_count[r0 + t] = len;
+    atomicMax(&s_maxlen, len);
+  }
+  __syncthreads();
+  const int32_t maxlen = s_maxlen;
   for (int32_t k0 = 0; k0 < nz; k0 += KC) {
+    if (k0 >= maxlen) {
+      // bands past every row of the block: padding only, no staging -- a
+      // thread stores a row PAIR (16-byte zero values, 8-byte own-row
+      // columns; R and ld are even, so pairs never straddle ld)
+      const int kc = min(KC, nz - k0);
+      for (int f = threadIdx.x; f < kc * (R / 2); f += blockDim.x) {
+        const int kk = f / (R / 2), row = 2 * (f % (R / 2));
+        const int64_t i = r0 + row;
+        if (i >= ld) continue;
+        const int64_t slot = static_cast<int64_t>(k0 + kk) * ld + i;
+        st_stream2(reinterpret_cast<double2*>(out_val + slot), make_double2(0.0, 0.0));
+        *reinterpret_cast<int2*>(out_col + slot) =
+            make_int2(static_cast<int32_t>(pad_base + (i < n ? i : 0)),
+                      static_cast<int32_t>(pad_base + (i + 1 < n ? i + 1 : 0)));
+      }
+      continue;  // k0 >= maxlen is block-uniform
+    }
     for (int f = threadIdx.x; f < R * KC; f += blockDim.x) {
       const int row = f / KC, kk = f % KC;
       const int32_t len = s_ptr[row + 1] - s_ptr[row];
@@ -850,6 +874,7 @@ __global__ void __launch_bounds__(256) k_crs_to_ell_cm(int64_t n, int32_t nz, in
 // rows per CTA of the flat band-major conversion: 0 = auto (256 rows for
 // nz <= 8, else 64, measured faster than 128); 64 / 128 force one
 int g_ell_flat_rows = 0;
+int g_ell_wide_flat = 1;  // tuning: one-pass staging also for 33..128 bands (0 = chunked kernel)
 
 template <int ROWS, int THREADS, int MAXNZ = 32>
 __global__ void __launch_bounds__(THREADS) k_crs_to_ell_cm_flat(int64_t n, int32_t nz, int64_t ld,
@@ -1049,6 +1074,10 @@ int spmvtk_k_tune_convert(const char* key, int value) {
     g_ell_flat_rows = value == 64 ? 64 : value == 128 ? 128 : 0;
     return 0;
   }
+  if (key && std::string(key) == "ell_wide_flat") {
+    g_ell_wide_flat = value != 0;
+    return 0;
+  }
   if (key && std::string(key) == "ccs_stage_threads") {
     g_stage_threads = value == 512 ? 512 : 1024;
     return 0;
@@ -1246,6 +1275,25 @@ int spmvtk_k_crs_to_ell_cm(int64_t n, int32_t nz, int64_t ld, const int32_t* irp
       k_crs_to_ell_cm_flat<128, 512><<<blocks, 512, (4096 + 128) * 12, s>>>(
           n, nz, ld, irp, icol, val, out_val, out_col, out_count, pad_base);
     }
+  } else if (nz <= 128 && g_ell_wide_flat) {
+    // 33..128 bands (config 5 at D <= ~0.3): the same one-pass staging with
+    // 4096 staged entries per CTA -- 64 rows of <= 64 or 32 rows of <= 128
+    static const bool attrs = [] {
+      cudaFuncSetAttribute(k_crs_to_ell_cm_flat<64, 256, 64>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (4096 + 128) * 12);
+      cudaFuncSetAttribute(k_crs_to_ell_cm_flat<32, 256, 128>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (4096 + 128) * 12);
+      return true;
+    }();
+    (void)attrs;
+    if (nz <= 64)
+      k_crs_to_ell_cm_flat<64, 256, 64><<<static_cast<unsigned>((ld + 63) / 64), 256,
+                                          (4096 + 128) * 12, s>>>(
+          n, nz, ld, irp, icol, val, out_val, out_col, out_count, pad_base);
+    else
+      k_crs_to_ell_cm_flat<32, 256, 128><<<static_cast<unsigned>((ld + 31) / 32), 256,
+                                           (4096 + 128) * 12, s>>>(
+          n, nz, ld, irp, icol, val, out_val, out_col, out_count, pad_base);
   } else if (nz <= 4) launch(std::integral_constant<int, 4>{});
   else if (nz <= 8) launch(std::integral_constant<int, 8>{});
   else if (nz <= 16) launch(std::integral_constant<int, 16>{});
@@ -1292,6 +1340,8 @@ void preload_convert() {
   cudaFuncGetAttributes(&a, k_crs_to_ell_cm_flat<64, 256>);
   cudaFuncGetAttributes(&a, k_crs_to_ell_cm_flat<256, 256, 8>);
   cudaFuncGetAttributes(&a, k_crs_to_ell_cm_flat<128, 512>);
+  cudaFuncGetAttributes(&a, k_crs_to_ell_cm_flat<64, 256, 64>);
+  cudaFuncGetAttributes(&a, k_crs_to_ell_cm_flat<32, 256, 128>);
   cudaFuncGetAttributes(&a, k_crs_to_ell_rm);
 }
 }  // namespace spmvtk_dev

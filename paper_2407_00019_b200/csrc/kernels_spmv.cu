@@ -28,7 +28,6 @@ __device__ __forceinline__ unsigned subwarp_mask(int W) {
   return ((1u << W) - 1u) << (lane & ~(W - 1));
 }
 
-int g_crs_rowlocal = 0;  // EXPERIMENT: thread-per-row SM-local CRS (threads per CTA)
 int g_ell_banded = -1;  // tuning: SM-local band-major ELL (-1 auto from the band shape)
 
 // ---- vector CRS: W lanes per row (spmv_crs, spmv.cpp:64-75) --------------
@@ -206,49 +205,6 @@ __global__ void __launch_bounds__(256) k_spmv_vec4(int64_t n, Rows rows,
     if (lane == 0) y.put(r, acc);
   }
   y.done();
-}
-
-// EXPERIMENT (knob crs_rowlocal = threads per CTA): one thread per row,
-// one CTA per SM sweeping a contiguous row region, the row stream read with
-// L1-allocating loads (a thread re-reads its row's lines), so a CTA's
-// threads walk their rows' entries roughly in step (band order) and the x
-// gathers of a banded matrix stay inside an L1-resident slice.
-template <int BS>
-__global__ void __launch_bounds__(BS) k_spmv_crs_rowlocal(int64_t n,
-                                                          const int32_t* __restrict__ irp,
-                                                          const int32_t* __restrict__ col,
-                                                          const double* __restrict__ val,
-                                                          const double* __restrict__ x,
-                                                          double* __restrict__ y) {
-  const int64_t per = ((n + gridDim.x - 1) / gridDim.x + BS - 1) / BS * BS;
-  const int64_t r_end = min(n, static_cast<int64_t>(blockIdx.x + 1) * per);
-  for (int64_t r = static_cast<int64_t>(blockIdx.x) * per + threadIdx.x; r < r_end; r += BS) {
-    int32_t p = __ldg(irp + r);
-    const int32_t b = __ldg(irp + r + 1);
-    double acc = 0.0;
-    for (; p < b && (p & 3); ++p) acc = fma(__ldg(val + p), ld_x(x + __ldg(col + p)), acc);
-    for (; p + 8 <= b; p += 8) {
-      const int4 c0 = __ldg(reinterpret_cast<const int4*>(col + p));
-      const int4 c1 = __ldg(reinterpret_cast<const int4*>(col + p + 4));
-      const double2 v0 = __ldg(reinterpret_cast<const double2*>(val + p));
-      const double2 v1 = __ldg(reinterpret_cast<const double2*>(val + p + 2));
-      const double2 v2 = __ldg(reinterpret_cast<const double2*>(val + p + 4));
-      const double2 v3 = __ldg(reinterpret_cast<const double2*>(val + p + 6));
-      const double g0 = ld_x(x + c0.x), g1 = ld_x(x + c0.y), g2 = ld_x(x + c0.z),
-                   g3 = ld_x(x + c0.w), g4 = ld_x(x + c1.x), g5 = ld_x(x + c1.y),
-                   g6 = ld_x(x + c1.z), g7 = ld_x(x + c1.w);
-      acc = fma(v0.x, g0, acc);
-      acc = fma(v0.y, g1, acc);
-      acc = fma(v1.x, g2, acc);
-      acc = fma(v1.y, g3, acc);
-      acc = fma(v2.x, g4, acc);
-      acc = fma(v2.y, g5, acc);
-      acc = fma(v3.x, g6, acc);
-      acc = fma(v3.y, g7, acc);
-    }
-    for (; p < b; ++p) acc = fma(__ldg(val + p), ld_x(x + __ldg(col + p)), acc);
-    y[r] = acc;
-  }
 }
 
 // block per long row (queue filled by k_spmv_vec / k_spmv_multi)
@@ -806,19 +762,6 @@ int spmvtk_k_spmv_crs(int64_t n, const int32_t* irp, const int32_t* icol, const 
                       int32_t* long_rows, void* stream) {
   cudaStream_t s = as_stream(stream);
   if (n <= 0) SPMVTK_LAUNCH_RETURN();
-  if (g_crs_rowlocal > 0 && (reinterpret_cast<uintptr_t>(val) & 15) == 0 &&
-      (reinterpret_cast<uintptr_t>(icol) & 15) == 0) {
-    if (g_crs_rowlocal == 1024)
-      k_spmv_crs_rowlocal<1024><<<kSMs, 1024, 0, s>>>(n, irp, icol, val, x, y);
-    else if (g_crs_rowlocal == 512)
-      k_spmv_crs_rowlocal<512><<<kSMs, 512, 0, s>>>(n, irp, icol, val, x, y);
-    else if (g_crs_rowlocal == 2048)  // two 1024-thread CTAs per SM (interleaved regions)
-      k_spmv_crs_rowlocal<1024><<<kSMs * 2, 1024, 0, s>>>(n, irp, icol, val, x, y);
-    else
-      k_spmv_crs_rowlocal<256><<<kSMs, 256, 0, s>>>(n, irp, icol, val, x, y);
-    count_launches(1);
-    SPMVTK_LAUNCH_RETURN();
-  }
   const int64_t long_limit = spmvtk_k_crs_long_limit(mean_row);
   const bool use_long = long_rows != nullptr && max_row > long_limit;
   if (use_long) cudaMemsetAsync(long_rows, 0, sizeof(int32_t), s);
@@ -1024,10 +967,6 @@ int64_t spmvtk_k_crs_long_limit(double mean_row) {
 }
 
 int spmvtk_k_tune(const char* key, int value) {
-  if (key && std::string(key) == "crs_rowlocal") {  // EXPERIMENT: threads per CTA (0 = off)
-    g_crs_rowlocal = value;
-    return 0;
-  }
   if (key && std::string(key) == "ell_banded") {  // SM-local ELL: -1 auto, 0 never, 1 always
     g_ell_banded = value < 0 ? -1 : value > 0 ? 1 : 0;
     return 0;

@@ -219,7 +219,7 @@ def test_config_5_full_size_parity(gpu, port, d):
     h.free()
 
 
-@pytest.mark.parametrize("d", [0.0, 0.3, 1.0, 2.0])
+@pytest.mark.parametrize("d", [0.0, 0.1, 0.3, 1.0, 2.0])
 def test_config_5_reduced_parity(gpu, port, d):
     sp = gpu
     h, rp, ci, v = host_arrays(sp, 5, 1 << 15, d)
