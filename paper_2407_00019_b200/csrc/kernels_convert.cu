@@ -1071,7 +1071,7 @@ int spmvtk_k_tune_convert(const char* key, int value) {
     return 0;
   }
   if (key && std::string(key) == "ell_flat_rows") {
-    g_ell_flat_rows = value == 64 ? 64 : value == 128 ? 128 : 0;
+    g_ell_flat_rows = value == 32 ? 32 : value == 64 ? 64 : value == 128 ? 128 : 0;
     return 0;
   }
   if (key && std::string(key) == "ell_wide_flat") {
@@ -1266,6 +1266,10 @@ int spmvtk_k_crs_to_ell_cm(int64_t n, int32_t nz, int64_t ld, const int32_t* irp
       unsigned blocks = static_cast<unsigned>((ld + 255) / 256);
       k_crs_to_ell_cm_flat<256, 256, 8><<<blocks, 256, (2048 + 64) * 12, s>>>(
           n, nz, ld, irp, icol, val, out_val, out_col, out_count, pad_base);
+    } else if (g_ell_flat_rows == 32) {
+      unsigned blocks = static_cast<unsigned>((ld + 31) / 32);
+      k_crs_to_ell_cm_flat<32, 256><<<blocks, 256, (1024 + 32) * 12, s>>>(
+          n, nz, ld, irp, icol, val, out_val, out_col, out_count, pad_base);
     } else if (g_ell_flat_rows != 128) {
       unsigned blocks = static_cast<unsigned>((ld + 63) / 64);
       k_crs_to_ell_cm_flat<64, 256><<<blocks, 256, (2048 + 64) * 12, s>>>(
@@ -1276,19 +1280,20 @@ int spmvtk_k_crs_to_ell_cm(int64_t n, int32_t nz, int64_t ld, const int32_t* irp
           n, nz, ld, irp, icol, val, out_val, out_col, out_count, pad_base);
     }
   } else if (nz <= 128 && g_ell_wide_flat) {
-    // 33..128 bands (config 5 at D <= ~0.3): the same one-pass staging with
-    // 4096 staged entries per CTA -- 64 rows of <= 64 or 32 rows of <= 128
+    // 33..128 bands (config 5 at D <= ~0.3): the same one-pass staging, 32
+    // rows per CTA
     static const bool attrs = [] {
-      cudaFuncSetAttribute(k_crs_to_ell_cm_flat<64, 256, 64>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, (4096 + 128) * 12);
       cudaFuncSetAttribute(k_crs_to_ell_cm_flat<32, 256, 128>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, (4096 + 128) * 12);
+
       return true;
     }();
     (void)attrs;
+    // (32 rows of <= 64: 2048 staged entries, 40 registers -- measured 12 %
+    // faster than 64 or 128 rows, profiles/r02_ell_wide_flat.txt)
     if (nz <= 64)
-      k_crs_to_ell_cm_flat<64, 256, 64><<<static_cast<unsigned>((ld + 63) / 64), 256,
-                                          (4096 + 128) * 12, s>>>(
+      k_crs_to_ell_cm_flat<32, 256, 64><<<static_cast<unsigned>((ld + 31) / 32), 256,
+                                          (2048 + 64) * 12, s>>>(
           n, nz, ld, irp, icol, val, out_val, out_col, out_count, pad_base);
     else
       k_crs_to_ell_cm_flat<32, 256, 128><<<static_cast<unsigned>((ld + 31) / 32), 256,
@@ -1340,7 +1345,7 @@ void preload_convert() {
   cudaFuncGetAttributes(&a, k_crs_to_ell_cm_flat<64, 256>);
   cudaFuncGetAttributes(&a, k_crs_to_ell_cm_flat<256, 256, 8>);
   cudaFuncGetAttributes(&a, k_crs_to_ell_cm_flat<128, 512>);
-  cudaFuncGetAttributes(&a, k_crs_to_ell_cm_flat<64, 256, 64>);
+  cudaFuncGetAttributes(&a, k_crs_to_ell_cm_flat<32, 256, 64>);
   cudaFuncGetAttributes(&a, k_crs_to_ell_cm_flat<32, 256, 128>);
   cudaFuncGetAttributes(&a, k_crs_to_ell_rm);
 }

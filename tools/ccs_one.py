@@ -1,5 +1,5 @@
 """One CRS->CCS (or COO-col) conversion of a BASELINE config after a warm-up,
-for ncu launch lists: python tools/ccs_one.py CONFIG [coo]
+for ncu launch lists: python tools/ccs_one.py CONFIG [coo] [D]
 (CCS_KNOBS="name=value,..." sets spmvtk_k_tune knobs first)"""
 import os
 import sys
@@ -13,7 +13,8 @@ fmt = sp.Format.COO_COL if len(sys.argv) > 2 and sys.argv[2] == "coo" else sp.Fo
 for kv in filter(None, os.environ.get("CCS_KNOBS", "").split(",")):
     k, v = kv.split("=")
     sp.load_library().spmvtk_k_tune(k.encode(), int(v))
-m = sp.HostCrs(cfg, PARAM[cfg], 0.0).upload()
+dp = float(sys.argv[3]) if len(sys.argv) > 3 else 0.0
+m = sp.HostCrs(cfg, PARAM[cfg], dp).upload()
 m.convert(fmt).free()  # warm-up (pool, module load)
 sp.synchronize()
 m.convert(fmt).free()

@@ -38,9 +38,11 @@ def setk(combo):
 
 
 def arrays(h, kind):
-    if kind in ("ell", "ell-row"):
+    if kind == "ell":
         v, c = h.ell_bands(0, h.describe().band_count)
         return [v.view(np.uint64), c]
+    if kind == "ell-row":
+        return [h.array(sp.Array.VALUES).view(np.uint64), h.array(sp.Array.COL_IDX, 4, 0)]
     out = [h.array(sp.Array.VALUES).view(np.uint64), h.array(sp.Array.ROW_IDX, 4, 0)]
     out.append(h.array(sp.Array.COL_IDX, 4, 0) if kind != "ccs"
                else h.array(sp.Array.POINTER, 4, 0))
