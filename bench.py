@@ -675,14 +675,17 @@ def impl_ours(args):
     # ---- the other full-size configs, measured in the same run
     also = {}
     if not args.no_also:
-        for cfg in (2, 3):
+        # config 5 at D = 0: the banded matrix where ELL beats CRS (the SM-local
+        # ELL kernel); the rest of config 5's sweep is in the AT graph
+        for cfg, dp in ((2, 0.0), (3, 0.0), (5, 0.0)):
             if cfg == args.config:
                 continue
-            mc = sp.HostCrs(cfg, DEFAULT_PARAM[cfg], 0.0, args.seed).upload()
+            mc = sp.HostCrs(cfg, DEFAULT_PARAM[cfg], dp, args.seed).upload()
             tab, trs, hs, _, _, _ = measure_matrix(sp, torch, mc, args.seed, peak, 200, 5)
             dc = mc.describe()
-            also[f"config{cfg}"] = {"n": dc.n, "nnz": dc.nnz, "d_mat": mc.row_stats().d_mat,
-                                    "best": best_format(tab), "formats": tab, "transforms": trs}
+            key = f"config{cfg}" if cfg != 5 else f"config5_D{dp}"
+            also[key] = {"n": dc.n, "nnz": dc.nnz, "d_mat": mc.row_stats().d_mat,
+                         "best": best_format(tab), "formats": tab, "transforms": trs}
             for name, hh in hs.items():
                 hh.free()
         # config 1 (5 MB, L2-resident, launch-bound): SURVEY.md §8d asks for a
@@ -739,7 +742,8 @@ def main():
     ap.add_argument("--param", type=int, default=None)
     ap.add_argument("--seed", type=int, default=2407)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-also", action="store_true", help="skip the configs 1-3 side tables")
+    ap.add_argument("--no-also", action="store_true",
+                    help="skip the side tables (configs 1-3 and config 5 at D = 0)")
     ap.add_argument("--no-ncu", action="store_true",
                     help="roofline.traffic from the committed capture, no live ncu run")
     ap.add_argument("--ncu-probe", default=None, help=argparse.SUPPRESS)

@@ -699,6 +699,12 @@ void spmv_device(const Matrix& m, spmvtk_kernel kernel, const double* x, double*
         int splits = ell_splits(m.n, m.band_count);
         DevArray<double> partial;
         if (splits > 1) partial.reset(static_cast<std::size_t>(splits) * m.n, "ELL partials");
+        if (splits <= 1 && ell_banded(m)) {  // one band chunk: ell-inner's kernel, as above
+          rt::check_launch(spmvtk_k_spmv_ell_cm_banded(m.n, m.band_count, m.ld, m.val.get(),
+                                                       m.col.get(), x, y, st),
+                           "spmv ell-outer");
+          return;
+        }
         rt::check_launch(spmvtk_k_spmv_ell_cm_split(m.n, m.band_count, m.ld, m.val.get(),
                                                     m.col.get(), x, y, splits, partial.get(), st),
                          "spmv ell-outer");
