@@ -28,8 +28,7 @@ __device__ __forceinline__ unsigned subwarp_mask(int W) {
   return ((1u << W) - 1u) << (lane & ~(W - 1));
 }
 
-int g_ell_banded = -1;
-int g_ell_banded_u = 4;  // EXPERIMENT: bands in flight of the SM-local ELL kernel  // tuning: SM-local band-major ELL (-1 auto from the band shape)
+int g_ell_banded = -1;  // tuning: SM-local band-major ELL (-1 auto from the band shape)
 
 // ---- vector CRS: W lanes per row (spmv_crs, spmv.cpp:64-75) --------------
 // Row extents come from a policy so the same kernel serves CRS (irp) and
@@ -902,16 +901,11 @@ int spmvtk_k_spmv_ell_cm_banded(int64_t n, int32_t nz, int64_t ld, const double*
     cudaMemsetAsync(y, 0, static_cast<size_t>(n) * sizeof(double), s);
     SPMVTK_LAUNCH_RETURN();
   }
-  // 46 registers x 1024 threads: one CTA per SM, so the kSMs CTAs land on
-  // distinct SMs (four rows per thread with 256-bit loads measured no faster)
-  if (g_ell_banded_u == 1)
-    k_spmv_ell_cm_local<1, 2><<<kSMs, 1024, 0, s>>>(n, nz, ld, val, col, x, y);
-  else if (g_ell_banded_u == 3)
-    k_spmv_ell_cm_local<3, 2><<<kSMs, 1024, 0, s>>>(n, nz, ld, val, col, x, y);
-  else if (g_ell_banded_u == 2)
-    k_spmv_ell_cm_local<2, 2><<<kSMs, 1024, 0, s>>>(n, nz, ld, val, col, x, y);
-  else
-    k_spmv_ell_cm_local<4, 2><<<kSMs, 1024, 0, s>>>(n, nz, ld, val, col, x, y);
+  // 1024 threads x 64 registers: one CTA per SM, so the kSMs CTAs land on
+  // distinct SMs.  Two bands in flight per thread (a tighter band front
+  // across the SM's threads) measured 2-7 % faster than four; four rows per
+  // thread with 256-bit loads no faster (profiles/r02_ell_banded.txt)
+  k_spmv_ell_cm_local<2, 2><<<kSMs, 1024, 0, s>>>(n, nz, ld, val, col, x, y);
   count_launches(1);
   SPMVTK_LAUNCH_RETURN();
 }
@@ -975,10 +969,6 @@ int64_t spmvtk_k_crs_long_limit(double mean_row) {
 }
 
 int spmvtk_k_tune(const char* key, int value) {
-  if (key && std::string(key) == "ell_banded_u") {
-    g_ell_banded_u = value;
-    return 0;
-  }
   if (key && std::string(key) == "ell_banded") {  // SM-local ELL: -1 auto, 0 never, 1 always
     g_ell_banded = value < 0 ? -1 : value > 0 ? 1 : 0;
     return 0;
