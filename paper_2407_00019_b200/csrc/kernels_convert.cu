@@ -164,17 +164,18 @@ int g_ccs_slices = 148;           // tuning: slices actually used (one per SM)
 int g_ccs_threads = 1024;         // tuning: threads of the count/scatter CTAs
 constexpr int kBktItems = 12;  // records per sort thread (bucket capacity = threads * 12)
 int g_ccs_sort_threads = 512;  // tuning: 256 or 512 (bucket target = 2/3 of the capacity)
+int g_ccs_sort_items = 0;      // tuning: records per sort thread (0 = from the column window, 8, 12)
 int g_ccs_window = 1;          // tuning: single pass stages slices with <= 1024-bucket windows
 
 // Two-pass or single-pass partition is decided on the device from the
 // number of non-empty (fine bucket, slice) runs counted by k_bkt_count: few
 // runs (banded matrices) keep their write streams L2-resident in one pass;
 // many runs (scattered columns) go through the coarse pass + refine.
-constexpr int32_t kTwoPassRuns = 1 << 17;
+__device__ int32_t d_two_pass_runs = 1 << 17;  // tuning: ccs_two_pass_runs
 constexpr int kStageU = 4;        // 32-entry batches per lane per staged step
 constexpr int kStageMaxB = 1024;  // buckets (or bucket window) of the staged scatter
 __device__ __forceinline__ bool two_pass(const int32_t* runs) {
-  return runs != nullptr && *runs > kTwoPassRuns;
+  return runs != nullptr && *runs > d_two_pass_runs;
 }
 
 __global__ void k_slice_rows(const int32_t* __restrict__ irp, int64_t n, int ns,
@@ -615,14 +616,14 @@ __global__ void __launch_bounds__(kRefineThreads) k_bkt_refine(
 
 // one CTA per bucket; dynamic smem: cnt[cb+1] | s_val | s_row | s_col (kBktCap each)
 constexpr int32_t kRankMax = 256;  // longer columns take the block network
-template <int kBktThreads>
-__global__ void __launch_bounds__(kBktThreads) k_bkt_sort(
+template <int kBktThreads, int kItems = kBktItems, int kMinBlocks = 1>
+__global__ void __launch_bounds__(kBktThreads, kMinBlocks) k_bkt_sort(
     const int4* rec1, const int4* rec2, const int32_t* runs,
     const int32_t* __restrict__ Toff, int64_t n, int shift,
     int nb, int ns, int32_t* __restrict__ col_ptr, int32_t* __restrict__ row_idx,
     double* __restrict__ out_val, int32_t* big_queue, int32_t* big_len,
     int32_t* __restrict__ out_col) {  // out_col: COO-col column indices (Phase II), or null
-  constexpr int kBktCap = kBktThreads * kBktItems;
+  constexpr int kBktCap = kBktThreads * kItems;
   const int4* __restrict__ rec = two_pass(runs) ? rec2 : rec1;
   extern __shared__ unsigned char s_raw[];
   const int cb = 1 << shift;
@@ -640,10 +641,10 @@ __global__ void __launch_bounds__(kBktThreads) k_bkt_sort(
   const bool fits = len <= kBktCap;
   for (int i = threadIdx.x; i <= cb; i += blockDim.x) cnt[i] = 0;
   // records stay in registers between the count and the placement
-  int4 r[kBktItems];
+  int4 r[kItems];
   if (fits) {
 #pragma unroll
-    for (int k = 0; k < kBktItems; ++k) {
+    for (int k = 0; k < kItems; ++k) {
       const int32_t q = static_cast<int32_t>(threadIdx.x) + k * kBktThreads;
       if (q < len) r[k] = ld_stream4(rec + bs + q);
     }
@@ -651,7 +652,7 @@ __global__ void __launch_bounds__(kBktThreads) k_bkt_sort(
   __syncthreads();
   if (fits) {
 #pragma unroll
-    for (int k = 0; k < kBktItems; ++k) {
+    for (int k = 0; k < kItems; ++k) {
       const int32_t q = static_cast<int32_t>(threadIdx.x) + k * kBktThreads;
       if (q < len) atomicAdd(&cnt[r[k].x - c0], 1);
     }
@@ -724,7 +725,7 @@ __global__ void __launch_bounds__(kBktThreads) k_bkt_sort(
   }
   // place by column (shared cursors; order inside a column arbitrary)
 #pragma unroll
-  for (int k = 0; k < kBktItems; ++k) {
+  for (int k = 0; k < kItems; ++k) {
     const int32_t q = static_cast<int32_t>(threadIdx.x) + k * kBktThreads;
     if (q < len) {
       const int32_t col = r[k].x - static_cast<int32_t>(c0);
@@ -1032,12 +1033,12 @@ struct BucketPlan {
   int nc;      // coarse buckets
 };
 int g_ccs_coarse = 9;  // tuning: log2 of the coarse bucket count target (0 = one pass)
-BucketPlan bucket_plan(int64_t n, int64_t nnz) {
+BucketPlan bucket_plan(int64_t n, int64_t nnz, int items) {
   const double per_col = n > 0 ? static_cast<double>(nnz) / static_cast<double>(n) : 1.0;
   int shift = 0;
   // buckets average 2/3 of the sort capacity: skewed column counts (config 5
   // at D = 1) overflow a tighter target into the slow global path
-  const double target = (2.0 / 3.0) * kBktItems * g_ccs_sort_threads;
+  const double target = (2.0 / 3.0) * items * (items == 8 ? 512 : g_ccs_sort_threads);
   while (shift < 12 && static_cast<double>(int64_t(1) << (shift + 1)) * per_col <= target) ++shift;
   while (((n + (int64_t(1) << shift) - 1) >> shift) > 32768) ++shift;
   const int nb = static_cast<int>((n + (int64_t(1) << shift) - 1) >> shift);
@@ -1086,6 +1087,14 @@ int spmvtk_k_tune_convert(const char* key, int value) {
     spmvtk_dev::g_ccs_force_stable = value;
     return 0;
   }
+  if (key && std::string(key) == "ccs_two_pass_runs") {
+    const int32_t v = value > 0 ? value : (1 << 17);
+    return static_cast<int>(cudaMemcpyToSymbol(d_two_pass_runs, &v, sizeof(v)));
+  }
+  if (key && std::string(key) == "ccs_sort_items") {
+    g_ccs_sort_items = value == 8 || value == 12 ? value : 0;
+    return 0;
+  }
   if (key && std::string(key) == "ccs_coarse") {
     g_ccs_coarse = value;
     return 0;
@@ -1093,8 +1102,22 @@ int spmvtk_k_tune_convert(const char* key, int value) {
   return static_cast<int>(cudaErrorInvalidValue);
 }
 
-size_t legacy_ccs_scratch_bytes(int64_t n, int64_t nnz) {
-  const BucketPlan bp = bucket_plan(n, nnz);
+// Records per sort thread: 8 (3 CTAs of 512 threads per SM, buckets of
+// ~2.7 K records) when the columns scatter over most of the matrix -- the
+// sort is latency-bound, more CTAs per SM hide it (config 4 sort 1286 ->
+// 820 us) -- else 12 (banded matrices keep their single-pass partition,
+// which smaller buckets would push into the two-pass one).  col_window: the
+// column spread max(col - row) - min(col - row) + 1, 0 = unknown.
+int sort_items(int64_t n, int64_t nnz, int64_t col_window) {
+  if (g_ccs_sort_items == 8 || g_ccs_sort_items == 12) return g_ccs_sort_items;
+  // same bucket width either way (e.g. > 32 entries per column): only the
+  // sort changes, and the smaller one wins (config 5 at D >= 0.1: -20 %)
+  if (bucket_plan(n, nnz, 8).shift == bucket_plan(n, nnz, 12).shift) return 8;
+  return col_window > 0 && col_window > n / 16 ? 8 : 12;
+}
+
+size_t legacy_ccs_scratch_bytes_items(int64_t n, int64_t nnz, int items) {
+  const BucketPlan bp = bucket_plan(n, nnz, items);
   const size_t t = static_cast<size_t>(bp.nb) * kSlices + 1;
   const size_t tc = static_cast<size_t>(bp.nc) * kSlices + 1;
   const size_t bucketed = 2 * align256(static_cast<size_t>(nnz) * 16) + 256 +
@@ -1103,6 +1126,11 @@ size_t legacy_ccs_scratch_bytes(int64_t n, int64_t nnz) {
                           2 * align256(tc * 4) + 2 * align256((static_cast<size_t>(bp.nb) + 1) * 4) +
                           align256(spmvtk_k_scan_scratch_bytes(static_cast<int64_t>(t))) + 1024;
   return bucketed;
+}
+
+size_t legacy_ccs_scratch_bytes(int64_t n, int64_t nnz) {
+  return std::max(legacy_ccs_scratch_bytes_items(n, nnz, 8),
+                  legacy_ccs_scratch_bytes_items(n, nnz, 12));
 }
 
 namespace {
@@ -1121,14 +1149,15 @@ void launch_staged(int ns, cudaStream_t s, const int32_t* irp, const int32_t* ic
 namespace {
 int crs_to_ccs_impl(int64_t n, int64_t nnz, const int32_t* irp, const int32_t* icol,
                     const double* val, int32_t* col_ptr, int32_t* row_idx, double* out_val,
-                    int32_t* out_col, void* scratch, void* stream) {
+                    int32_t* out_col, void* scratch, void* stream, int64_t col_window) {
   cudaStream_t s = as_stream(stream);
   if (n <= 0) SPMVTK_LAUNCH_RETURN();
   if (nnz == 0) {
     cudaMemsetAsync(col_ptr, 0, static_cast<size_t>(n + 1) * sizeof(int32_t), s);
     SPMVTK_LAUNCH_RETURN();
   }
-  const BucketPlan bp = bucket_plan(n, nnz);
+  const int items = sort_items(n, nnz, col_window);
+  const BucketPlan bp = bucket_plan(n, nnz, items);
   const int ns = std::max(1, std::min(g_ccs_slices, kSlices));
   const int nt = g_ccs_threads == 1024 ? 1024 : 512;
   const int64_t tlen = static_cast<int64_t>(bp.nb) * ns;
@@ -1159,7 +1188,7 @@ int crs_to_ccs_impl(int64_t n, int64_t nnz, const int32_t* irp, const int32_t* i
   const size_t single_smem = std::max(hist_smem, size_t(1024) * kStageU * sizeof(int4));
   const int cb = 1 << bp.shift;
   const size_t sort_smem = ((static_cast<size_t>(cb + 1) * 4 + 15) & ~static_cast<size_t>(15)) +
-                           static_cast<size_t>(g_ccs_sort_threads) * kBktItems * 14;
+                           static_cast<size_t>(items == 8 ? 512 : g_ccs_sort_threads) * items * 14;
   static const bool attrs = [] {  // thread-safe one-time setup
     cudaFuncSetAttribute(k_bkt_count, cudaFuncAttributeMaxDynamicSharedMemorySize, 32768 * 4);
     cudaFuncSetAttribute(k_bkt_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, 32768 * 4);
@@ -1173,6 +1202,8 @@ int crs_to_ccs_impl(int64_t n, int64_t nnz, const int32_t* irp, const int32_t* i
                          static_cast<int>(((4097 * 4 + 15) & ~15) + 512 * kBktItems * 14));
     cudaFuncSetAttribute(k_bkt_sort<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(((4097 * 4 + 15) & ~15) + 256 * kBktItems * 14));
+    cudaFuncSetAttribute(k_bkt_sort<512, 8, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(((4097 * 4 + 15) & ~15) + 512 * 8 * 14));
     return true;
   }();
   (void)attrs;
@@ -1212,7 +1243,11 @@ int crs_to_ccs_impl(int64_t n, int64_t nnz, const int32_t* irp, const int32_t* i
     k_bkt_scatter<<<ns, nt, hist_smem, s>>>(irp, icol, val, slice_row, bp.shift, bp.nb, Toff,
                                             rec, nullptr, false);
   }
-  if (g_ccs_sort_threads == 256)
+  if (items == 8)
+    k_bkt_sort<512, 8, 3><<<bp.nb, 512, sort_smem, s>>>(rec, rec2, runs, Toff, n, bp.shift, bp.nb,
+                                                        ns, col_ptr, row_idx, out_val, big,
+                                                        big_len, out_col);
+  else if (g_ccs_sort_threads == 256)
     k_bkt_sort<256><<<bp.nb, 256, sort_smem, s>>>(rec, rec2, runs, Toff, n, bp.shift, bp.nb, ns,
                                                   col_ptr, row_idx, out_val, big, big_len,
                                                   out_col);
@@ -1227,16 +1262,17 @@ int crs_to_ccs_impl(int64_t n, int64_t nnz, const int32_t* irp, const int32_t* i
 
 int legacy_crs_to_ccs(int64_t n, int64_t nnz, const int32_t* irp, const int32_t* icol,
                       const double* val, int32_t* col_ptr, int32_t* row_idx,
-                      double* out_val, void* scratch, void* stream) {
+                      double* out_val, void* scratch, void* stream, int64_t col_window) {
   return crs_to_ccs_impl(n, nnz, irp, icol, val, col_ptr, row_idx, out_val, nullptr, scratch,
-                         stream);
+                         stream, col_window);
 }
 
 int legacy_crs_to_coo_col(int64_t n, int64_t nnz, const int32_t* irp, const int32_t* icol,
                           const double* val, int32_t* col_ptr, int32_t* row_idx,
-                          int32_t* col_idx, double* out_val, void* scratch, void* stream) {
+                          int32_t* col_idx, double* out_val, void* scratch, void* stream,
+                          int64_t col_window) {
   return crs_to_ccs_impl(n, nnz, irp, icol, val, col_ptr, row_idx, out_val, col_idx, scratch,
-                         stream);
+                         stream, col_window);
 }
 
 int spmvtk_k_crs_to_ell_cm(int64_t n, int32_t nz, int64_t ld, const int32_t* irp,
@@ -1340,6 +1376,7 @@ void preload_convert() {
   cudaFuncGetAttributes(&a, k_bkt_refine);
   cudaFuncGetAttributes(&a, k_bkt_sort<256>);
   cudaFuncGetAttributes(&a, k_bkt_sort<512>);
+  cudaFuncGetAttributes(&a, k_bkt_sort<512, 8, 3>);
   cudaFuncGetAttributes(&a, k_bkt_sort_big);
   cudaFuncGetAttributes(&a, k_crs_to_ell_cm<32>);
   cudaFuncGetAttributes(&a, k_crs_to_ell_cm_flat<64, 256>);
