@@ -383,15 +383,20 @@ __device__ __forceinline__ void bkt_scatter_staged(
     int32_t blo, int nbw, const int32_t* __restrict__ Toff, int4* __restrict__ rec,
     int4* s_rec /* kStageThreads * kStageU records */) {
   constexpr int kP = kStageMaxB / kStageThreads;  // buckets owned per thread
-  __shared__ int32_t s_cur[kStageMaxB], s_cnt[kStageMaxB], s_off[kStageMaxB];
+  // run cursors double-buffered by step parity: the owner of a bucket
+  // advances next step's cursor while this step's copy-out still reads its
+  // own, so no barrier separates the copy-out from the next step (5 barriers
+  // per step instead of 7; each thread zeroes its counters as it reads them)
+  __shared__ int32_t s_cur[2][kStageMaxB], s_cnt[kStageMaxB], s_off[kStageMaxB];
   __shared__ int32_t s_wsum[kStageThreads / 32];
+  __shared__ int32_t s_total;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int nwarps = kStageThreads / 32;
 #pragma unroll
   for (int j = 0; j < kP; ++j) {
     const int b = tid * kP + j;
     if (b < nbw) {
-      s_cur[b] = Toff[static_cast<int64_t>(b + blo) * gridDim.x + blockIdx.x];
+      s_cur[0][b] = Toff[static_cast<int64_t>(b + blo) * gridDim.x + blockIdx.x];
       s_cnt[b] = 0;
     }
   }
@@ -455,6 +460,7 @@ __device__ __forceinline__ void bkt_scatter_staged(
     for (int j = 0; j < kP; ++j) {
       const int b = tid * kP + j;
       loc[j] = b < nbw ? s_cnt[b] : 0;
+      if (b < nbw) s_cnt[b] = 0;  // read once: free for the next step's counts
       x += loc[j];
     }
     int32_t inc = x;
@@ -474,14 +480,19 @@ __device__ __forceinline__ void bkt_scatter_staged(
         if (lane >= d) wi += t;
       }
       if (lane < nwarps) s_wsum[lane] = wi - wv;
+      if (lane == nwarps - 1) s_total = wi;
     }
     __syncthreads();
+    const int par = st & 1;
     {
       int32_t e = s_wsum[warp] + inc - x;
 #pragma unroll
       for (int j = 0; j < kP; ++j) {
         const int b = tid * kP + j;
-        if (b < nbw) s_off[b] = e;
+        if (b < nbw) {
+          s_off[b] = e;
+          s_cur[par ^ 1][b] = s_cur[par][b] + loc[j];
+        }
         e += loc[j];
       }
     }
@@ -492,27 +503,21 @@ __device__ __forceinline__ void bkt_scatter_staged(
         s_rec[s_off[(c[u] >> shift) - blo] + rk[u]] =
             make_int4(c[u], row[u], __double2loint(v[u]), __double2hiint(v[u]));
     __syncthreads();
-    const int32_t count = s_off[nbw - 1] + s_cnt[nbw - 1];
+    const int32_t count = s_total;
     for (int32_t i = tid; i < count; i += kStageThreads) {
       const int4 r = s_rec[i];
       const int b = (r.x >> shift) - blo;
-      rec[s_cur[b] + i - s_off[b]] = r;
+      rec[s_cur[par][b] + i - s_off[b]] = r;
     }
-    __syncthreads();
-#pragma unroll
-    for (int j = 0; j < kP; ++j) {
-      const int b = tid * kP + j;
-      if (b < nbw) {
-        s_cur[b] += s_cnt[b];
-        s_cnt[b] = 0;
-      }
-    }
+    // no barrier: the next step's first shared writes (its counts) come after
+    // this step's reads of s_cnt, and its offsets, cursors and staged records
+    // only after its own first barrier, which every thread reaches after its
+    // copy-out
 #pragma unroll
     for (int u = 0; u < kStageU; ++u) {
       c[u] = cn[u];
       v[u] = vn[u];
     }
-    __syncthreads();
   }
 }
 
