@@ -93,14 +93,6 @@ int spmvtk_k_crs_to_ccs(int64_t n, int64_t nnz, const int32_t* irp,
  * :55-66) in one pass: as spmvtk_k_crs_to_ccs, and the sort that places each
  * entry also writes its column into col_idx (no separate col_ptr expansion).
  * Same scratch as spmvtk_k_crs_to_ccs. */
-/* Either of the two above (col_idx NULL: CCS, else COO-col) with the
- * matrix's column spread max(col - row) - min(col - row) + 1 (0 = unknown),
- * which sizes the sort's buckets: smaller buckets and more CTAs per SM when
- * columns scatter over most of the matrix. */
-int spmvtk_k_crs_to_ccs_w(int64_t n, int64_t nnz, const int32_t* irp,
-                          const int32_t* icol, const double* val, int32_t* col_ptr,
-                          int32_t* row_idx, int32_t* col_idx, double* out_val,
-                          int64_t col_window, void* scratch, void* stream);
 /* 1 when the "ccs_stable" tuning knob routes every conversion to the stable
  * pipeline (testing). */
 int spmvtk_k_ccs_force_stable(void);

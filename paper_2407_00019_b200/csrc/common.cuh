@@ -199,11 +199,10 @@ extern "C" {
 size_t legacy_ccs_scratch_bytes(int64_t n, int64_t nnz);
 int legacy_crs_to_ccs(int64_t n, int64_t nnz, const int32_t* irp, const int32_t* icol,
                       const double* val, int32_t* col_ptr, int32_t* row_idx, double* out_val,
-                      void* scratch, void* stream, int64_t col_window);
+                      void* scratch, void* stream);
 int legacy_crs_to_coo_col(int64_t n, int64_t nnz, const int32_t* irp, const int32_t* icol,
                           const double* val, int32_t* col_ptr, int32_t* row_idx,
-                          int32_t* col_idx, double* out_val, void* scratch, void* stream,
-                          int64_t col_window);
+                          int32_t* col_idx, double* out_val, void* scratch, void* stream);
 }
 namespace spmvtk_dev {
 // Host-side count of the SpMV kernels this library launched (spmvtk_k_launch_count).

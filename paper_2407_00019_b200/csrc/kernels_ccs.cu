@@ -613,25 +613,14 @@ size_t spmvtk_k_ccs_scratch_bytes(int64_t n, int64_t nnz) {
 int spmvtk_k_crs_to_ccs(int64_t n, int64_t nnz, const int32_t* irp, const int32_t* icol,
                         const double* val, int32_t* col_ptr, int32_t* row_idx,
                         double* out_val, void* scratch, void* stream) {
-  return legacy_crs_to_ccs(n, nnz, irp, icol, val, col_ptr, row_idx, out_val, scratch, stream,
-                           0);
+  return legacy_crs_to_ccs(n, nnz, irp, icol, val, col_ptr, row_idx, out_val, scratch, stream);
 }
 
 int spmvtk_k_crs_to_coo_col(int64_t n, int64_t nnz, const int32_t* irp, const int32_t* icol,
                             const double* val, int32_t* col_ptr, int32_t* row_idx,
                             int32_t* col_idx, double* out_val, void* scratch, void* stream) {
   return legacy_crs_to_coo_col(n, nnz, irp, icol, val, col_ptr, row_idx, col_idx, out_val,
-                               scratch, stream, 0);
-}
-
-int spmvtk_k_crs_to_ccs_w(int64_t n, int64_t nnz, const int32_t* irp, const int32_t* icol,
-                          const double* val, int32_t* col_ptr, int32_t* row_idx,
-                          int32_t* col_idx, double* out_val, int64_t col_window, void* scratch,
-                          void* stream) {
-  return col_idx ? legacy_crs_to_coo_col(n, nnz, irp, icol, val, col_ptr, row_idx, col_idx,
-                                         out_val, scratch, stream, col_window)
-                 : legacy_crs_to_ccs(n, nnz, irp, icol, val, col_ptr, row_idx, out_val, scratch,
-                                     stream, col_window);
+                               scratch, stream);
 }
 
 int spmvtk_k_crs_to_ccs_stable(int64_t n, int64_t nnz, const int32_t* irp, const int32_t* icol,

@@ -164,6 +164,7 @@ int g_ccs_slices = 148;           // tuning: slices actually used (one per SM)
 int g_ccs_threads = 1024;         // tuning: threads of the count/scatter CTAs
 constexpr int kBktItems = 12;  // records per sort thread (bucket capacity = threads * 12)
 int g_ccs_sort_threads = 512;  // tuning: 256 or 512 (bucket target = 2/3 of the capacity)
+int g_ccs_sort_768 = 1;        // tuning: 768-thread sort for the 12-record plan (0 = 512 x 12)
 int g_ccs_sort_items = 0;      // tuning: records per sort thread (0 = from the column window, 8, 12)
 int g_ccs_window = 1;          // tuning: single pass stages slices with <= 1024-bucket windows
 
@@ -1096,6 +1097,10 @@ int spmvtk_k_tune_convert(const char* key, int value) {
     const int32_t v = value > 0 ? value : (1 << 17);
     return static_cast<int>(cudaMemcpyToSymbol(d_two_pass_runs, &v, sizeof(v)));
   }
+  if (key && std::string(key) == "ccs_sort_768") {
+    g_ccs_sort_768 = value != 0;
+    return 0;
+  }
   if (key && std::string(key) == "ccs_sort_items") {
     g_ccs_sort_items = value == 8 || value == 12 ? value : 0;
     return 0;
@@ -1107,18 +1112,18 @@ int spmvtk_k_tune_convert(const char* key, int value) {
   return static_cast<int>(cudaErrorInvalidValue);
 }
 
-// Records per sort thread: 8 (3 CTAs of 512 threads per SM, buckets of
-// ~2.7 K records) when the columns scatter over most of the matrix -- the
-// sort is latency-bound, more CTAs per SM hide it (config 4 sort 1286 ->
-// 820 us) -- else 12 (banded matrices keep their single-pass partition,
-// which smaller buckets would push into the two-pass one).  col_window: the
-// column spread max(col - row) - min(col - row) + 1, 0 = unknown.
-int sort_items(int64_t n, int64_t nnz, int64_t col_window) {
+// Records per sort thread.  The sort is latency-bound (50 % occupancy,
+// shared-memory and barrier stalls), so it runs with 48 warps per SM either
+// way: 8 records x 512 threads x 3 CTAs (buckets of ~2.7 K records) when
+// that bucket plan equals the 12-record one (config 4, config 5 at D >= 1:
+// only the sort changes, 1286 -> 820 us on config 4), else the 12-record plan
+// (buckets of ~4 K) sorted by 768 threads x 8 records x 2 CTAs (config 2
+// -7 % against the smaller buckets; config 3 and config 5 at D <= 0.5 -16 %,
+// whose smaller buckets would also push the single-pass partition into the
+// two-pass one).  profiles/r02_ccs_sort_items.txt
+int sort_items(int64_t n, int64_t nnz) {
   if (g_ccs_sort_items == 8 || g_ccs_sort_items == 12) return g_ccs_sort_items;
-  // same bucket width either way (e.g. > 32 entries per column): only the
-  // sort changes, and the smaller one wins (config 5 at D >= 0.1: -20 %)
-  if (bucket_plan(n, nnz, 8).shift == bucket_plan(n, nnz, 12).shift) return 8;
-  return col_window > 0 && col_window > n / 16 ? 8 : 12;
+  return bucket_plan(n, nnz, 8).shift == bucket_plan(n, nnz, 12).shift ? 8 : 12;
 }
 
 size_t legacy_ccs_scratch_bytes_items(int64_t n, int64_t nnz, int items) {
@@ -1154,14 +1159,14 @@ void launch_staged(int ns, cudaStream_t s, const int32_t* irp, const int32_t* ic
 namespace {
 int crs_to_ccs_impl(int64_t n, int64_t nnz, const int32_t* irp, const int32_t* icol,
                     const double* val, int32_t* col_ptr, int32_t* row_idx, double* out_val,
-                    int32_t* out_col, void* scratch, void* stream, int64_t col_window) {
+                    int32_t* out_col, void* scratch, void* stream) {
   cudaStream_t s = as_stream(stream);
   if (n <= 0) SPMVTK_LAUNCH_RETURN();
   if (nnz == 0) {
     cudaMemsetAsync(col_ptr, 0, static_cast<size_t>(n + 1) * sizeof(int32_t), s);
     SPMVTK_LAUNCH_RETURN();
   }
-  const int items = sort_items(n, nnz, col_window);
+  const int items = sort_items(n, nnz);
   const BucketPlan bp = bucket_plan(n, nnz, items);
   const int ns = std::max(1, std::min(g_ccs_slices, kSlices));
   const int nt = g_ccs_threads == 1024 ? 1024 : 512;
@@ -1209,6 +1214,8 @@ int crs_to_ccs_impl(int64_t n, int64_t nnz, const int32_t* irp, const int32_t* i
                          static_cast<int>(((4097 * 4 + 15) & ~15) + 256 * kBktItems * 14));
     cudaFuncSetAttribute(k_bkt_sort<512, 8, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(((4097 * 4 + 15) & ~15) + 512 * 8 * 14));
+    cudaFuncSetAttribute(k_bkt_sort<768, 8, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(((4097 * 4 + 15) & ~15) + 768 * 8 * 14));
     return true;
   }();
   (void)attrs;
@@ -1252,6 +1259,12 @@ int crs_to_ccs_impl(int64_t n, int64_t nnz, const int32_t* irp, const int32_t* i
     k_bkt_sort<512, 8, 3><<<bp.nb, 512, sort_smem, s>>>(rec, rec2, runs, Toff, n, bp.shift, bp.nb,
                                                         ns, col_ptr, row_idx, out_val, big,
                                                         big_len, out_col);
+  else if (g_ccs_sort_768 && (1 << bp.shift) <= 768 && g_ccs_sort_threads == 512)
+    // the 12-record plan's buckets (capacity 6144) sorted by 768 threads x 8
+    // records: 48 warps per SM instead of 32, same partition
+    k_bkt_sort<768, 8, 2><<<bp.nb, 768, sort_smem, s>>>(rec, rec2, runs, Toff, n, bp.shift, bp.nb,
+                                                        ns, col_ptr, row_idx, out_val, big,
+                                                        big_len, out_col);
   else if (g_ccs_sort_threads == 256)
     k_bkt_sort<256><<<bp.nb, 256, sort_smem, s>>>(rec, rec2, runs, Toff, n, bp.shift, bp.nb, ns,
                                                   col_ptr, row_idx, out_val, big, big_len,
@@ -1267,17 +1280,16 @@ int crs_to_ccs_impl(int64_t n, int64_t nnz, const int32_t* irp, const int32_t* i
 
 int legacy_crs_to_ccs(int64_t n, int64_t nnz, const int32_t* irp, const int32_t* icol,
                       const double* val, int32_t* col_ptr, int32_t* row_idx,
-                      double* out_val, void* scratch, void* stream, int64_t col_window) {
+                      double* out_val, void* scratch, void* stream) {
   return crs_to_ccs_impl(n, nnz, irp, icol, val, col_ptr, row_idx, out_val, nullptr, scratch,
-                         stream, col_window);
+                         stream);
 }
 
 int legacy_crs_to_coo_col(int64_t n, int64_t nnz, const int32_t* irp, const int32_t* icol,
                           const double* val, int32_t* col_ptr, int32_t* row_idx,
-                          int32_t* col_idx, double* out_val, void* scratch, void* stream,
-                          int64_t col_window) {
+                          int32_t* col_idx, double* out_val, void* scratch, void* stream) {
   return crs_to_ccs_impl(n, nnz, irp, icol, val, col_ptr, row_idx, out_val, col_idx, scratch,
-                         stream, col_window);
+                         stream);
 }
 
 int spmvtk_k_crs_to_ell_cm(int64_t n, int32_t nz, int64_t ld, const int32_t* irp,
@@ -1382,6 +1394,7 @@ void preload_convert() {
   cudaFuncGetAttributes(&a, k_bkt_sort<256>);
   cudaFuncGetAttributes(&a, k_bkt_sort<512>);
   cudaFuncGetAttributes(&a, k_bkt_sort<512, 8, 3>);
+  cudaFuncGetAttributes(&a, k_bkt_sort<768, 8, 2>);
   cudaFuncGetAttributes(&a, k_bkt_sort_big);
   cudaFuncGetAttributes(&a, k_crs_to_ell_cm<32>);
   cudaFuncGetAttributes(&a, k_crs_to_ell_cm_flat<64, 256>);

@@ -228,22 +228,16 @@ void launch_ccs(const Matrix& a, const std::int32_t* seg_idx, std::int32_t* col_
   const bool stable = spmvtk_k_ccs_force_stable() || !pairs_ascending(a);
   const std::int64_t n = a.n, nnz = a.nnz;
   int rc;
-  // the column spread sizes the sort's buckets (measured at upload)
-  std::int64_t window = 0;
-  {
-    std::lock_guard<std::mutex> lk(a.mu);
-    if (a.band) window = a.band->right + a.band->left + 1;
-  }
   if (col_out)
     rc = stable ? spmvtk_k_crs_to_coo_col_stable(n, nnz, a.ptr.get(), seg_idx, a.val.get(),
                                                  col_ptr, row_out, col_out, val_out, scratch, st)
-                : spmvtk_k_crs_to_ccs_w(n, nnz, a.ptr.get(), seg_idx, a.val.get(), col_ptr,
-                                        row_out, col_out, val_out, window, scratch, st);
+                : spmvtk_k_crs_to_coo_col(n, nnz, a.ptr.get(), seg_idx, a.val.get(), col_ptr,
+                                          row_out, col_out, val_out, scratch, st);
   else
     rc = stable ? spmvtk_k_crs_to_ccs_stable(n, nnz, a.ptr.get(), seg_idx, a.val.get(), col_ptr,
                                              row_out, val_out, scratch, st)
-                : spmvtk_k_crs_to_ccs_w(n, nnz, a.ptr.get(), seg_idx, a.val.get(), col_ptr,
-                                        row_out, nullptr, val_out, window, scratch, st);
+                : spmvtk_k_crs_to_ccs(n, nnz, a.ptr.get(), seg_idx, a.val.get(), col_ptr,
+                                      row_out, val_out, scratch, st);
   rt::check_launch(rc, col_out ? "CRS->COO-col" : "CRS->CCS");
 }
 }  // namespace
