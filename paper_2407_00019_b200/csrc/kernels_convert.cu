@@ -164,7 +164,6 @@ int g_ccs_slices = 148;           // tuning: slices actually used (one per SM)
 int g_ccs_threads = 1024;         // tuning: threads of the count/scatter CTAs
 constexpr int kBktItems = 12;  // records per sort thread (bucket capacity = threads * 12)
 int g_ccs_sort_threads = 512;  // tuning: 256 or 512 (bucket target = 2/3 of the capacity)
-int g_ccs_sort_768 = 1;        // tuning: 768-thread sort for the 12-record plan (0 = 512 x 12)
 int g_ccs_sort_items = 0;      // tuning: records per sort thread (0 = from the column window, 8, 12)
 int g_ccs_window = 1;          // tuning: single pass stages slices with <= 1024-bucket windows
 
@@ -1097,10 +1096,6 @@ int spmvtk_k_tune_convert(const char* key, int value) {
     const int32_t v = value > 0 ? value : (1 << 17);
     return static_cast<int>(cudaMemcpyToSymbol(d_two_pass_runs, &v, sizeof(v)));
   }
-  if (key && std::string(key) == "ccs_sort_768") {
-    g_ccs_sort_768 = value != 0;
-    return 0;
-  }
   if (key && std::string(key) == "ccs_sort_items") {
     g_ccs_sort_items = value == 8 || value == 12 ? value : 0;
     return 0;
@@ -1112,15 +1107,13 @@ int spmvtk_k_tune_convert(const char* key, int value) {
   return static_cast<int>(cudaErrorInvalidValue);
 }
 
-// Records per sort thread.  The sort is latency-bound (50 % occupancy,
-// shared-memory and barrier stalls), so it runs with 48 warps per SM either
-// way: 8 records x 512 threads x 3 CTAs (buckets of ~2.7 K records) when
-// that bucket plan equals the 12-record one (config 4, config 5 at D >= 1:
-// only the sort changes, 1286 -> 820 us on config 4), else the 12-record plan
-// (buckets of ~4 K) sorted by 768 threads x 8 records x 2 CTAs (config 2
-// -7 % against the smaller buckets; config 3 and config 5 at D <= 0.5 -16 %,
-// whose smaller buckets would also push the single-pass partition into the
-// two-pass one).  profiles/r02_ccs_sort_items.txt
+// Records per sort thread: 8 (512 threads x 3 CTAs per SM, buckets of
+// ~2.7 K records) when that bucket plan equals the 12-record one (config 4,
+// config 5 at D >= 0.1: only the sort changes, 1-2 % faster), else 12 (512
+// threads x 2 CTAs; __launch_bounds__ min 2 keeps it at 64 registers -- the
+// compiler otherwise takes 89 and one CTA per SM, 20 % slower).  Smaller
+// buckets elsewhere would push banded matrices into the two-pass partition.
+// profiles/r02_ccs_sort_items.txt
 int sort_items(int64_t n, int64_t nnz) {
   if (g_ccs_sort_items == 8 || g_ccs_sort_items == 12) return g_ccs_sort_items;
   return bucket_plan(n, nnz, 8).shift == bucket_plan(n, nnz, 12).shift ? 8 : 12;
@@ -1208,14 +1201,12 @@ int crs_to_ccs_impl(int64_t n, int64_t nnz, const int32_t* irp, const int32_t* i
                          1024 * kStageU * static_cast<int>(sizeof(int4)));
     cudaFuncSetAttribute(k_bkt_scatter_staged<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          512 * kStageU * static_cast<int>(sizeof(int4)));
-    cudaFuncSetAttribute(k_bkt_sort<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_bkt_sort<512, kBktItems, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(((4097 * 4 + 15) & ~15) + 512 * kBktItems * 14));
     cudaFuncSetAttribute(k_bkt_sort<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(((4097 * 4 + 15) & ~15) + 256 * kBktItems * 14));
     cudaFuncSetAttribute(k_bkt_sort<512, 8, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(((4097 * 4 + 15) & ~15) + 512 * 8 * 14));
-    cudaFuncSetAttribute(k_bkt_sort<768, 8, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(((4097 * 4 + 15) & ~15) + 768 * 8 * 14));
     return true;
   }();
   (void)attrs;
@@ -1259,18 +1250,12 @@ int crs_to_ccs_impl(int64_t n, int64_t nnz, const int32_t* irp, const int32_t* i
     k_bkt_sort<512, 8, 3><<<bp.nb, 512, sort_smem, s>>>(rec, rec2, runs, Toff, n, bp.shift, bp.nb,
                                                         ns, col_ptr, row_idx, out_val, big,
                                                         big_len, out_col);
-  else if (g_ccs_sort_768 && (1 << bp.shift) <= 768 && g_ccs_sort_threads == 512)
-    // the 12-record plan's buckets (capacity 6144) sorted by 768 threads x 8
-    // records: 48 warps per SM instead of 32, same partition
-    k_bkt_sort<768, 8, 2><<<bp.nb, 768, sort_smem, s>>>(rec, rec2, runs, Toff, n, bp.shift, bp.nb,
-                                                        ns, col_ptr, row_idx, out_val, big,
-                                                        big_len, out_col);
   else if (g_ccs_sort_threads == 256)
     k_bkt_sort<256><<<bp.nb, 256, sort_smem, s>>>(rec, rec2, runs, Toff, n, bp.shift, bp.nb, ns,
                                                   col_ptr, row_idx, out_val, big, big_len,
                                                   out_col);
   else
-    k_bkt_sort<512><<<bp.nb, 512, sort_smem, s>>>(rec, rec2, runs, Toff, n, bp.shift, bp.nb, ns,
+    k_bkt_sort<512, kBktItems, 2><<<bp.nb, 512, sort_smem, s>>>(rec, rec2, runs, Toff, n, bp.shift, bp.nb, ns,
                                                   col_ptr, row_idx, out_val, big, big_len,
                                                   out_col);
   k_bkt_sort_big<<<kSMs, 512, 0, s>>>(col_ptr, n, bp.shift, row_idx, out_val, big, big_len);
@@ -1392,9 +1377,8 @@ void preload_convert() {
   cudaFuncGetAttributes(&a, k_bkt_scatter_staged<512>);
   cudaFuncGetAttributes(&a, k_bkt_refine);
   cudaFuncGetAttributes(&a, k_bkt_sort<256>);
-  cudaFuncGetAttributes(&a, k_bkt_sort<512>);
+  cudaFuncGetAttributes(&a, k_bkt_sort<512, kBktItems, 2>);
   cudaFuncGetAttributes(&a, k_bkt_sort<512, 8, 3>);
-  cudaFuncGetAttributes(&a, k_bkt_sort<768, 8, 2>);
   cudaFuncGetAttributes(&a, k_bkt_sort_big);
   cudaFuncGetAttributes(&a, k_crs_to_ell_cm<32>);
   cudaFuncGetAttributes(&a, k_crs_to_ell_cm_flat<64, 256>);
