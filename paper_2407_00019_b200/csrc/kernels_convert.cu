@@ -218,25 +218,44 @@ __global__ void __launch_bounds__(1024) k_bkt_count(const int32_t* __restrict__ 
   const int32_t e0 = irp[slice_row[blockIdx.x]], e1 = irp[slice_row[blockIdx.x + 1]];
   const int32_t step = static_cast<int32_t>(blockDim.x);
   const int lane = threadIdx.x & 31;
-  int32_t p = e0 + static_cast<int32_t>(threadIdx.x);
   int32_t chg = 0, smp = 0;
-  // warp-uniform main loop (its last lane bounds it), 4 loads in flight
-  for (int it = 0; p - lane + 31 + 3 * step < e1; p += 4 * step, ++it) {
-    const int32_t c0 = ld_stream(icol + p), c1 = ld_stream(icol + p + step);
-    const int32_t c2 = ld_stream(icol + p + 2 * step), c3 = ld_stream(icol + p + 3 * step);
+  // 16-byte loads over the 4-aligned body, two per thread in flight (8
+  // columns); the unaligned head and the tail one column per thread
+  // (aligned by address: the lower ABI accepts any 4-byte aligned icol)
+  const int32_t mis = static_cast<int32_t>((reinterpret_cast<uintptr_t>(icol) >> 2) & 3);
+  const int32_t a0 = min(e1, ((e0 + mis + 3) & ~3) - mis);
+  const int32_t a1 = max(a0, ((e1 + mis) & ~3) - mis);
+  for (int32_t p = e0 + static_cast<int32_t>(threadIdx.x); p < a0; p += step)
+    atomicAdd(&s_hist[ld_stream(icol + p) >> shift], 1);
+  for (int32_t p = a1 + static_cast<int32_t>(threadIdx.x); p < e1; p += step)
+    atomicAdd(&s_hist[ld_stream(icol + p) >> shift], 1);
+  const int4* __restrict__ q4 = reinterpret_cast<const int4*>(icol + a0);
+  const int32_t nq = (a1 - a0) >> 2;
+  int32_t q = static_cast<int32_t>(threadIdx.x);
+  for (int it = 0; q + step < nq; q += 2 * step, ++it) {
+    const int4 u = ld_stream4(q4 + q), w = ld_stream4(q4 + q + step);
     if (win && (it & 7) == 0) {  // sample: is an entry in its CRS predecessor's bucket?
-      const int32_t prev = __shfl_up_sync(kFull, c0 >> shift, 1);
-      if (lane) {
-        ++smp;
-        chg += prev != (c0 >> shift);
-      }
+      smp += 3;
+      chg += ((u.y >> shift) != (u.x >> shift)) + ((u.z >> shift) != (u.y >> shift)) +
+             ((u.w >> shift) != (u.z >> shift));
     }
-    atomicAdd(&s_hist[c0 >> shift], 1);
-    atomicAdd(&s_hist[c1 >> shift], 1);
-    atomicAdd(&s_hist[c2 >> shift], 1);
-    atomicAdd(&s_hist[c3 >> shift], 1);
+    atomicAdd(&s_hist[u.x >> shift], 1);
+    atomicAdd(&s_hist[u.y >> shift], 1);
+    atomicAdd(&s_hist[u.z >> shift], 1);
+    atomicAdd(&s_hist[u.w >> shift], 1);
+    atomicAdd(&s_hist[w.x >> shift], 1);
+    atomicAdd(&s_hist[w.y >> shift], 1);
+    atomicAdd(&s_hist[w.z >> shift], 1);
+    atomicAdd(&s_hist[w.w >> shift], 1);
   }
-  for (; p < e1; p += step) atomicAdd(&s_hist[ld_stream(icol + p) >> shift], 1);
+  for (; q < nq; q += step) {
+    const int4 u = ld_stream4(q4 + q);
+    atomicAdd(&s_hist[u.x >> shift], 1);
+    atomicAdd(&s_hist[u.y >> shift], 1);
+    atomicAdd(&s_hist[u.z >> shift], 1);
+    atomicAdd(&s_hist[u.w >> shift], 1);
+  }
+  (void)lane;
   __syncthreads();
   int32_t nz = 0, lo = nb, hi = -1;
   for (int b = threadIdx.x; b < nb; b += blockDim.x) {

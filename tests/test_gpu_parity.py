@@ -732,6 +732,17 @@ def test_lower_abi_phase1_phase2_and_statistics(gpu, port):
     cc2 = torch.empty_like(cc)
     assert lib.spmvtk_k_expand_ptr(cp.data_ptr(), n, nnz, cc2.data_ptr(), stream) == 0
     assert torch.equal(ri2, ri) and torch.equal(cc2, cc) and torch.equal(cv2, cv)
+    # column indices starting 4/8/12 bytes past a 16-byte boundary (the
+    # bucket count reads them with 16-byte loads over the aligned body)
+    for shift in (1, 2, 3):
+        buf = torch.empty(nnz + 4, dtype=torch.int32, device="cuda")
+        icol_u = buf[shift:shift + nnz]
+        icol_u.copy_(icol)
+        ri3, cv3 = torch.empty_like(ri), torch.empty_like(cv)
+        assert lib.spmvtk_k_crs_to_ccs(n, nnz, irp.data_ptr(), icol_u.data_ptr(), val.data_ptr(),
+                                       cp.data_ptr(), ri3.data_ptr(), cv3.data_ptr(),
+                                       scratch.data_ptr(), stream) == 0
+        assert torch.equal(ri3, ri) and torch.equal(cv3, cv), shift
     # row statistics through mapped memory, twice (the accumulator resets)
     acc = torch.zeros(4, dtype=torch.int64, device="cuda")
     host = torch.zeros(4, dtype=torch.int64).pin_memory()
