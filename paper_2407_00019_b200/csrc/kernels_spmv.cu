@@ -557,66 +557,32 @@ __global__ void __launch_bounds__(256) k_spmv_ell_cm(int64_t n, int32_t k_begin,
 
 // Banded matrices (SM-local regions): ONE 1024-thread CTA per SM (grid =
 // kSMs; the block scheduler places them breadth-first, one per SM), each CTA
-// sweeping one contiguous region of rows.  A band-major ELL thread walks its
-// rows band by band, so at any moment an SM's threads gather band k of a few
-// thousand consecutive rows: for columns scattered inside a band window of
-// x (config 5) those gathers stay inside a slice of x that L1 holds, instead
-// of the interleaved grid's 8 CTAs per SM each pulling a different window
-// through L2 (config 5 D = 0: L1 sector hit rate 14 % -> 51 %, L2 requests
-// 58.7 M -> 25.8 M).  R rows per thread: 2 (double2 / int2 loads) or 4 (one
-// 256-bit value load and one int4 column load per band).
-template <int U, int R>
+// sweeping one contiguous region of row pairs.  A band-major ELL thread walks
+// its rows band by band, so at any moment an SM's threads gather band k of a
+// few thousand consecutive rows: for columns scattered inside a band window
+// of x (config 5) those gathers stay inside a slice of x that L1 holds,
+// instead of the interleaved grid's 8 CTAs per SM each pulling a different
+// window through L2 (config 5 D = 0: L1 sector hit rate 14 % -> 51 %, L2
+// requests 58.7 M -> 25.8 M).  Same per-row band order as k_spmv_ell_cm, so
+// the results are bitwise equal.  (Four rows per thread with 256-bit value
+// loads measured no faster; profiles/r02_ell_banded.txt.)
+template <int U>
 __global__ void __launch_bounds__(1024, 1) k_spmv_ell_cm_local(int64_t n, int32_t nz, int64_t ld,
-                                                            const double* __restrict__ val,
-                                                            const int32_t* __restrict__ col,
-                                                            const double* __restrict__ x,
-                                                            double* __restrict__ y) {
-  const int64_t groups = (n + R - 1) / R;
-  const int64_t per = ((groups + gridDim.x - 1) / gridDim.x + blockDim.x - 1) / blockDim.x *
+                                                               const double* __restrict__ val,
+                                                               const int32_t* __restrict__ col,
+                                                               const double* __restrict__ x,
+                                                               double* __restrict__ y) {
+  const int64_t pairs = (n + 1) / 2;
+  const int64_t per = ((pairs + gridDim.x - 1) / gridDim.x + blockDim.x - 1) / blockDim.x *
                       blockDim.x;
-  const int64_t g_end = min(groups, static_cast<int64_t>(blockIdx.x + 1) * per);
+  const int64_t g_end = min(pairs, static_cast<int64_t>(blockIdx.x + 1) * per);
   for (int64_t g = static_cast<int64_t>(blockIdx.x) * per + threadIdx.x; g < g_end;
        g += blockDim.x) {
-    const int64_t i = R * g;
-    if constexpr (R == 2) {
-      double a0, a1;
-      ell_pair<U>(i, 0, nz, ld, val, col, x, a0, a1);
-      y[i] = a0;
-      if (i + 1 < n) y[i + 1] = a1;
-    } else {
-      double acc[4] = {0.0, 0.0, 0.0, 0.0};
-      int32_t k = 0;
-      for (; k + U <= nz; k += U) {
-        double2 lo[U], hi[U];
-        int4 c[U];
-#pragma unroll
-        for (int j = 0; j < U; ++j) {
-          const int64_t off = static_cast<int64_t>(k + j) * ld + i;
-          ld4_stream_first(val + off, lo[j], hi[j]);
-          c[j] = ld_stream4(reinterpret_cast<const int4*>(col + off));
-        }
-#pragma unroll
-        for (int j = 0; j < U; ++j) {
-          acc[0] = fma(lo[j].x, ld_x(x + c[j].x), acc[0]);
-          acc[1] = fma(lo[j].y, ld_x(x + c[j].y), acc[1]);
-          acc[2] = fma(hi[j].x, ld_x(x + c[j].z), acc[2]);
-          acc[3] = fma(hi[j].y, ld_x(x + c[j].w), acc[3]);
-        }
-      }
-      for (; k < nz; ++k) {
-        const int64_t off = static_cast<int64_t>(k) * ld + i;
-        double2 lo, hi;
-        ld4_stream_first(val + off, lo, hi);
-        const int4 c = ld_stream4(reinterpret_cast<const int4*>(col + off));
-        acc[0] = fma(lo.x, ld_x(x + c.x), acc[0]);
-        acc[1] = fma(lo.y, ld_x(x + c.y), acc[1]);
-        acc[2] = fma(hi.x, ld_x(x + c.z), acc[2]);
-        acc[3] = fma(hi.y, ld_x(x + c.w), acc[3]);
-      }
-#pragma unroll
-      for (int h = 0; h < 4; ++h)
-        if (i + h < n) y[i + h] = acc[h];
-    }
+    const int64_t i = 2 * g;
+    double a0, a1;
+    ell_pair<U>(i, 0, nz, ld, val, col, x, a0, a1);
+    y[i] = a0;
+    if (i + 1 < n) y[i + 1] = a1;
   }
 }
 
@@ -905,7 +871,7 @@ int spmvtk_k_spmv_ell_cm_banded(int64_t n, int32_t nz, int64_t ld, const double*
   // distinct SMs.  Two bands in flight per thread (a tighter band front
   // across the SM's threads) measured 2-7 % faster than four; four rows per
   // thread with 256-bit loads no faster (profiles/r02_ell_banded.txt)
-  k_spmv_ell_cm_local<2, 2><<<kSMs, 1024, 0, s>>>(n, nz, ld, val, col, x, y);
+  k_spmv_ell_cm_local<2><<<kSMs, 1024, 0, s>>>(n, nz, ld, val, col, x, y);
   count_launches(1);
   SPMVTK_LAUNCH_RETURN();
 }
@@ -1013,6 +979,7 @@ int spmvtk_k_preload(void) {
   cudaFuncGetAttributes(&a, k_spmv_crs_long<PushOut>);
   cudaFuncGetAttributes(&a, k_spmv_ell_cm<4, PushOut>);
   cudaFuncGetAttributes(&a, k_spmv_ell_cm<4>);
+  cudaFuncGetAttributes(&a, k_spmv_ell_cm_local<2>);
   cudaFuncGetAttributes(&a, k_spmv_ell_cm_part<4>);
   cudaFuncGetAttributes(&a, k_reduce_partials);
   cudaFuncGetAttributes(&a, k_spmv_coo_row);

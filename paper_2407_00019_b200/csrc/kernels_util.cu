@@ -557,6 +557,7 @@ void preload_util() {
   cudaFuncGetAttributes(&a, k_widen);
   cudaFuncGetAttributes(&a, k_out_of_range);
   cudaFuncGetAttributes(&a, k_descents);
+  cudaFuncGetAttributes(&a, k_row_order_stats);
   cudaFuncGetAttributes(&a, k_scan_lookback);
 }
 }  // namespace spmvtk_dev
