@@ -18,10 +18,27 @@ local kernel so it can be tested on CPU with gloo (tests/test_dist.py).
 """
 from __future__ import annotations
 
+import contextlib
 import math
+import os
+import sys
 from typing import Callable
 
 import numpy as np
+
+
+@contextlib.contextmanager
+def _stdout_to_stderr():
+    """fd 1 -> fd 2 for the duration (C libraries print through fd 1)."""
+    sys.stdout.flush()
+    saved = os.dup(1)
+    os.dup2(2, 1)
+    try:
+        yield
+    finally:
+        sys.stdout.flush()
+        os.dup2(saved, 1)
+        os.close(saved)
 
 
 def block_rows(n: int, world: int) -> int:
@@ -387,8 +404,6 @@ def bench_main(args, rank: int, world: int, local: int) -> int:
     torch.distributed only carries the communicator id, the barriers and the
     max-over-ranks of the timings."""
     import json
-    import os
-    import sys
     import time
 
     import torch
@@ -401,12 +416,17 @@ def bench_main(args, rank: int, world: int, local: int) -> int:
                        spmv_bytes, workload_config)
 
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    sp.set_stream(torch.cuda.current_stream().cuda_stream)
-    lib = sp.load_library()
-    uid = [sp.Dist.unique_id() if rank == 0 else None]
-    dist.broadcast_object_list(uid, src=0)
-    comm = sp.Dist(rank, world, uid[0])
+    # NCCL writes its version banner to fd 1 at communicator init when the
+    # environment asks for it (NCCL_DEBUG); the bench's stdout must hold
+    # exactly one JSON line, so both inits run with fd 1 pointed at stderr
+    with _stdout_to_stderr():
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        sp.set_stream(torch.cuda.current_stream().cuda_stream)
+        lib = sp.load_library()
+        uid = [sp.Dist.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = sp.Dist(rank, world, uid[0])
+        dist.barrier()
     shard = comm.shard(args.config, args.param, 0.0, args.seed)
     desc = shard.describe()
     n, rows, r0 = desc.ncols, desc.n, desc.row_offset
